@@ -1,0 +1,129 @@
+/*
+ * skm_b200.h -- C ABI of libskm_b200.so, the B200 (sm_100a) SuperKMeans hot path.
+ *
+ * Every entry point is extern "C", takes plain device pointers, element counts and leading
+ * dimensions (in elements), plus an opaque cudaStream_t passed as void*.  Calls are
+ * stream-ordered and asynchronous; none allocates device memory (scratch comes from the
+ * caller through the *_workspace_bytes queries).  Return value: 0 on success, a negative
+ * SKM_E* code otherwise; skm_last_error() describes the last failure of the calling thread.
+ *
+ * Reference interfaces replaced (paths relative to the reference repository root):
+ *   skm_scan_bank                <- scan_bank                pkg/src/superkmeans/_kernels.pyx:14-82
+ *   skm_seed_thresholds          <- seed_thresholds          pkg/src/superkmeans/_kernels.pyx:85-103
+ *   skm_accumulate_centroid_sums <- accumulate_centroid_sums pkg/src/superkmeans/_kernels.pyx:106-119
+ *   skm_portable_matmul          <- portable_matmul          pkg/src/superkmeans/_kernels.pyx:122-142
+ *   skm_gemm_tf32x3              <- matmul (sgemm `af @ bf.T`) + expand_to_sq_l2
+ *                                   pkg/src/superkmeans/distance.py:46-82, apply/unapply_rotation
+ *                                   preprocess.py:37-52, full-pass argmin core.py:183-190
+ *   skm_row_sq_norms             <- row_sq_norms             pkg/src/superkmeans/preprocess.py:95-101
+ *   skm_cluster_sort / skm_cluster_sums / skm_finalize_centroids
+ *                                <- update_centroids         pkg/src/superkmeans/core.py:79-100
+ *                                   build_cluster_lists      pkg/src/superkmeans/evaluation.py:78-83
+ *   skm_apply_splits             <- split_empty_clusters row arithmetic, core.py:119-125
+ *   skm_pruned_scan              <- _pruned_assign_pass inner loop, core.py:230-263
+ *   skm_etr_*                    <- brute_force_topk / etr_probe, evaluation.py:53-75, 142-170
+ */
+#ifndef SKM_B200_H
+#define SKM_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKM_OK 0
+#define SKM_E_CUDA (-1)
+#define SKM_E_ARG (-2)
+#define SKM_E_DRIVER (-3)
+#define SKM_E_WORKSPACE (-4)
+
+const char* skm_last_error(void);
+int skm_abi_version(void);
+
+/* ---- layout / preprocessing --------------------------------------------------------- */
+/* hi = x with the low 13 mantissa bits cleared, lo = x - hi (exact); pad columns -> 0. */
+int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi, float* lo, long long ldo,
+                   void* stream);
+/* out[r] = f32(sum_{c<dims} (f64)x[r,c]^2) */
+int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* out, void* stream);
+/* out[r,:cols] = in[idx[r],:cols] */
+int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
+                    long long ldo, void* stream);
+int skm_fill_f32(float* p, long long n, float v, void* stream);
+int skm_copy_i32(const int* src, int* dst, int n, void* stream);
+
+/* ---- the reference kernel protocol, on device memory (bitwise parity entries) -------- */
+int skm_seed_thresholds(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign,
+                        int n, int d, float* out, void* stream);
+/* counters: device u64[2] += {survivors, dims_touched} */
+int skm_scan_bank(const float* partial_dists, int n, int kb, const float* x, long long ldx, const float* tail,
+                  const long long* block_offsets, const int* block_dims, int n_blocks, const float* theta_factors,
+                  int d_prime, int bank_offset, float* tau, int* assign, int sentinel,
+                  unsigned long long* counters, void* stream);
+long long skm_update_workspace_bytes(int n, int k);
+int skm_accumulate_centroid_sums(const float* x, long long ldx, const int* assign, int n, int d, int k,
+                                 double* sums, long long* counts, void* workspace, long long workspace_bytes,
+                                 void* stream);
+int skm_portable_matmul(const float* a, long long lda, const float* b, long long ldb, int n, int m, int dims,
+                        float* out, long long ldo, void* stream);
+
+/* ---- tensor-core GEMM (3xTF32 on tcgen05/TMEM, TMA-fed) ------------------------------ */
+enum skm_gemm_mode { SKM_GEMM_STORE = 0, SKM_GEMM_DIST = 1, SKM_GEMM_ARGMIN = 2, SKM_GEMM_GATE = 3 };
+typedef struct skm_gemm_params {
+  /* operands: row-major, K contiguous; hi/lo from skm_split_hilo; ld multiple of 4 */
+  const float* a_hi; const float* a_lo; long long lda;
+  const float* b_hi; const float* b_lo; long long ldb;
+  int M, N, K;
+  int mode;
+  int n_split;                 /* CTAs along N (ARGMIN with n_split>1 goes through keys) */
+  float* out; long long ldo;   /* STORE / DIST */
+  const float* xsq;            /* per-row norm (DIST/ARGMIN/GATE) */
+  const float* ysq;            /* per-column norm */
+  int* assign; float* tau;     /* ARGMIN, n_split == 1 */
+  unsigned long long* keys;    /* ARGMIN, n_split > 1: pre-filled with ~0ull */
+  const float* thr;            /* GATE: per-row threshold (keep iff dist <= thr) */
+  int* cand_idx; float* cand_val; int* cand_cnt; int cand_cap;
+  long long row_offset;        /* ARGMIN/GATE output row offset */
+} skm_gemm_params;
+int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream);
+int skm_decode_argmin_keys(const unsigned long long* keys, int n, int* assign, float* tau, void* stream);
+int skm_fill_u64(unsigned long long* p, long long n, unsigned long long v, void* stream);
+
+/* ---- centroid update ------------------------------------------------------------------ */
+/* stable sort of row ids by assignment; counts/offsets int32[k] */
+int skm_cluster_sort(const int* assign, int n, int k, int* order, int* counts, int* offsets, void* workspace,
+                     long long workspace_bytes, void* stream);
+/* mode 0: centroids[c] = f32(sum/count) for count>0 (others untouched); mode 1: sums (f64, k x d) */
+int skm_cluster_sums(const float* x, long long ldx, const int* order, const int* offsets, const int* counts, int k,
+                     int d, double* sums, int accumulate, float* centroids, long long ldc, int mode, void* stream);
+int skm_finalize_centroids(const double* sums, const long long* counts, int k, int d, float* centroids,
+                           long long ldc, void* stream);
+int skm_counts_to_i64(const int* c32, long long* c64, int k, int accumulate, void* stream);
+int skm_apply_splits(float* centroids, long long ldc, int d, const int* empties, const int* donors, int n_splits,
+                     float eps, void* stream);
+/* stats[0] (f64) = sum(tau), stats[1] (u64) = count(assign != prev) (prev may be NULL) */
+long long skm_stats_workspace_bytes(int n);
+int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n, double* out_sum,
+                     unsigned long long* out_changed, void* workspace, long long workspace_bytes, void* stream);
+
+
+/* ---- production pruning scan (fused gate candidates -> exact sequential-tau scan) ---- */
+/* tails[j][q][b][r] = C[j][d'+64b+4q+r], zero padded; nb = ceil((d-d')/64) */
+int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream);
+int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, void* stream);
+typedef struct skm_scan_params {
+  const int* cand_idx; const float* cand_val; const int* cand_cnt; int cap;  /* list mode */
+  const float* dense; long long ld_dense; const int* dense_row; int k;       /* dense mode */
+  const int* rows; int n_rows; long long row0;  /* batch-local rows to scan (NULL = 0..n_rows-1) */
+  const float* x; long long ldx;
+  const float* tails; int nb; int d_prime;
+  const float* theta; const int* block_dims;   /* nb+1 factors, nb block widths */
+  float* tau; int* assign;                     /* global rows (row0 + local) */
+  unsigned long long* counters;                /* += {survivors, dims touched, changed} */
+  int dense_mode;
+} skm_scan_params;
+int skm_pruned_scan(const skm_scan_params* p, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKM_B200_H */

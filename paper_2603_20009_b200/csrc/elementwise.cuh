@@ -1,0 +1,265 @@
+// Memory-bound helper kernels: 3xTF32 operand split, squared norms, row gathers,
+// threshold seeding, bit-exact bank scan (parity ABI), portable matmul (parity ABI),
+// assignment statistics, split application.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace skm {
+
+constexpr float kInf = __builtin_huge_valf();
+
+// x = hi + lo exactly, hi has a 10-bit mantissa (tf32-representable) so the tensor core
+// consumes it losslessly whether it truncates or rounds; lo keeps the remaining bits.
+__global__ void split_hilo_kernel(const float* __restrict__ x, long long ldx, int rows, int cols,
+                                  float* __restrict__ hi, float* __restrict__ lo, long long ldo) {
+  const long long total = static_cast<long long>(rows) * ldo;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long r = idx / ldo;
+    const int c = static_cast<int>(idx - r * ldo);
+    float v = 0.0f;
+    if (c < cols) v = x[r * ldx + c];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[idx] = h;
+    lo[idx] = __fsub_rn(v, h);
+  }
+}
+
+// Squared row norms over the leading `dims` columns, double accumulation rounded to
+// fp32 (preprocess.py:95-101).  One warp per row.
+__global__ void row_sq_norms_kernel(const float* __restrict__ x, long long ldx, int rows, int dims,
+                                    float* __restrict__ out) {
+  const int warps_per_block = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long r = blockIdx.x * (long long)warps_per_block + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps_per_block) {
+    const float* row = x + r * ldx;
+    double s = 0.0;
+    for (int c = lane; c < dims; c += 32) {
+      const double v = row[c];
+      s += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[r] = static_cast<float>(s);
+  }
+}
+
+// out[r, :] = in[idx[r], :]  (cols wide, padded leading dims)
+__global__ void gather_rows_kernel(const float* __restrict__ in, long long ldi, const long long* __restrict__ idx,
+                                   int rows, int cols, float* __restrict__ out, long long ldo) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols;
+    const int c = static_cast<int>(e - r * cols);
+    out[r * ldo + c] = in[idx[r] * ldi + c];
+  }
+}
+
+// tau_i = sum_t (x_it - c_{a_i,t})^2, ascending t, separate mul/add (_kernels.pyx:85-103).
+// One thread per row; 32-column chunks staged through padded shared memory so the
+// global reads stay coalesced while each thread runs its own sequential chain.
+constexpr int SEED_ROWS = 128;
+__global__ void __launch_bounds__(SEED_ROWS)
+    seed_thresholds_kernel(const float* __restrict__ x, long long ldx, const float* __restrict__ cent, long long ldc,
+                           const int* __restrict__ assign, int n, int d, float* __restrict__ out) {
+  __shared__ float xs[SEED_ROWS][33];
+  __shared__ float cs[SEED_ROWS][33];
+  __shared__ int sa[SEED_ROWS];
+  const int r0 = blockIdx.x * SEED_ROWS;
+  const int tid = threadIdx.x;
+  if (r0 + tid < n) sa[tid] = assign[r0 + tid];
+  __syncthreads();
+  float acc = 0.0f;
+  for (int t0 = 0; t0 < d; t0 += 32) {
+    for (int e = tid; e < SEED_ROWS * 32; e += SEED_ROWS) {
+      const int r = e >> 5, tt = e & 31;
+      const int row = r0 + r, col = t0 + tt;
+      float xv = 0.0f, cv = 0.0f;
+      if (row < n && col < d) {
+        xv = x[static_cast<long long>(row) * ldx + col];
+        cv = cent[static_cast<long long>(sa[r]) * ldc + col];
+      }
+      xs[r][tt] = xv;
+      cs[r][tt] = cv;
+    }
+    __syncthreads();
+    const int lim = min(32, d - t0);
+    for (int tt = 0; tt < lim; ++tt) {
+      const float diff = __fsub_rn(xs[tid][tt], cs[tid][tt]);
+      acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+    }
+    __syncthreads();
+  }
+  if (r0 + tid < n) out[r0 + tid] = acc;
+}
+
+__device__ __forceinline__ void warp_add_u64(unsigned long long v, unsigned long long* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+// Bit-exact device twin of the reference's bank scan (_kernels.pyx:14-82): one thread per
+// vector, PDX tail (dim-major within each block), sequential-tau semantics.  This is the
+// parity entry of the kernel protocol; the fused production scan lives in scan.cuh.
+__global__ void scan_bank_pdx_kernel(const float* __restrict__ pd, int n, int kb, const float* __restrict__ x,
+                                     long long ldx, const float* __restrict__ tail,
+                                     const long long* __restrict__ block_offsets, const int* __restrict__ block_dims,
+                                     int n_blocks, const float* __restrict__ theta, int d_prime, int bank_offset,
+                                     float* __restrict__ tau, int* __restrict__ assign, int sentinel,
+                                     unsigned long long* __restrict__ counters) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long surv = 0, touched = 0;
+  if (i < n) {
+    float tcur = tau[i];
+    int best = assign[i];
+    const float* prow = pd + static_cast<long long>(i) * kb;
+    const float* xrow = x + static_cast<long long>(i) * ldx;
+    for (int j = 0; j < kb; ++j) {
+      float gate = sentinel ? kInf : __fmul_rn(tcur, theta[0]);
+      const float p = prow[j];
+      if (p > gate) continue;
+      ++surv;
+      float running = p;
+      bool pruned = false;
+      int xoff = d_prime;
+      for (int b = 0; b < n_blocks; ++b) {
+        const int bd = block_dims[b];
+        const float* col = tail + block_offsets[b] + j;
+        float acc = 0.0f;
+        for (int t = 0; t < bd; ++t) {
+          const float diff = __fsub_rn(xrow[xoff + t], col[static_cast<long long>(t) * kb]);
+          acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+        }
+        touched += bd;
+        running = __fadd_rn(running, acc);
+        xoff += bd;
+        gate = (sentinel && b < n_blocks - 1) ? kInf : __fmul_rn(tcur, theta[b + 1]);
+        if (running > gate) { pruned = true; break; }
+      }
+      if (!pruned) {
+        if (running < tcur) {
+          best = bank_offset + j;
+          tcur = running;
+        } else if (running == tcur && bank_offset + j < best) {
+          best = bank_offset + j;
+        }
+      }
+    }
+    tau[i] = tcur;
+    assign[i] = best;
+  }
+  warp_add_u64(surv, &counters[0]);
+  warp_add_u64(touched, &counters[1]);
+}
+
+// out[i, l] = sum_{t<dims} a[i,t] * b[l,t], one thread per cell, ascending t, no FMA:
+// bitwise the compiled portable_matmul (_kernels.pyx:122-142, built -ffp-contract=off).
+__global__ void portable_matmul_kernel(const float* __restrict__ a, long long lda, const float* __restrict__ b,
+                                       long long ldb, int n, int m, int dims, float* __restrict__ out, long long ldo) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)n * m) return;
+  const long long i = e / m;
+  const int l = static_cast<int>(e - i * m);
+  const float* ar = a + i * lda;
+  const float* br = b + static_cast<long long>(l) * ldb;
+  float acc = 0.0f;
+  for (int t = 0; t < dims; ++t) acc = __fadd_rn(acc, __fmul_rn(ar[t], br[t]));
+  out[i * ldo + l] = acc;
+}
+
+// keys (dist_bits << 32 | col) -> assign / tau
+__global__ void decode_argmin_keys_kernel(const unsigned long long* __restrict__ keys, int n, int* __restrict__ assign,
+                                          float* __restrict__ tau) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long k = keys[i];
+  assign[i] = static_cast<int>(k & 0xffffffffu);
+  tau[i] = __uint_as_float(static_cast<unsigned int>(k >> 32));
+}
+
+__global__ void fill_u64_kernel(unsigned long long* p, long long n, unsigned long long v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// Per-block partials of sum(tau) (f64) and count(assign != prev); fixed-order final pass.
+constexpr int STAT_THREADS = 256;
+__global__ void __launch_bounds__(STAT_THREADS)
+    assign_stats_partial_kernel(const float* __restrict__ tau, const int* __restrict__ assign,
+                                const int* __restrict__ prev, int n, double* __restrict__ part_sum,
+                                unsigned long long* __restrict__ part_cnt) {
+  __shared__ double ss[STAT_THREADS];
+  __shared__ unsigned long long sc[STAT_THREADS];
+  double s = 0.0;
+  unsigned long long c = 0;
+  const long long per = ((long long)n + gridDim.x - 1) / gridDim.x;
+  const long long beg = per * blockIdx.x, end = min((long long)n, beg + per);
+  for (long long i = beg + threadIdx.x; i < end; i += STAT_THREADS) {
+    s += static_cast<double>(tau[i]);
+    if (prev) c += (assign[i] != prev[i]);
+  }
+  ss[threadIdx.x] = s;
+  sc[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = STAT_THREADS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      ss[threadIdx.x] += ss[threadIdx.x + o];
+      sc[threadIdx.x] += sc[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part_sum[blockIdx.x] = ss[0];
+    part_cnt[blockIdx.x] = sc[0];
+  }
+}
+
+__global__ void assign_stats_final_kernel(const double* __restrict__ part_sum,
+                                          const unsigned long long* __restrict__ part_cnt, int parts,
+                                          double* __restrict__ out_sum, unsigned long long* __restrict__ out_cnt) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    unsigned long long c = 0;
+    for (int p = 0; p < parts; ++p) {
+      s += part_sum[p];
+      c += part_cnt[p];
+    }
+    *out_sum = s;
+    *out_cnt = c;
+  }
+}
+
+// Empty-cluster splits decided on the host (core.py:103-128): applied in list order so a
+// donor split twice sees its already-shrunk row.  delta = row * eps * (+1,-1,...).
+__global__ void apply_splits_kernel(float* __restrict__ cent, long long ldc, int d, const int* __restrict__ empties,
+                                    const int* __restrict__ donors, int n_splits, float eps) {
+  for (int s = 0; s < n_splits; ++s) {
+    const int e = empties[s], dn = donors[s];
+    for (int t = threadIdx.x; t < d; t += blockDim.x) {
+      const float row = cent[static_cast<long long>(dn) * ldc + t];
+      const float sign = (t & 1) ? -1.0f : 1.0f;
+      const float delta = __fmul_rn(__fmul_rn(row, eps), sign);
+      cent[static_cast<long long>(e) * ldc + t] = __fadd_rn(row, delta);
+      cent[static_cast<long long>(dn) * ldc + t] = __fsub_rn(row, delta);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void iota_kernel(int* p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+__global__ void copy_i32_kernel(const int* __restrict__ a, int* __restrict__ b, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+__global__ void fill_f32_kernel(float* p, long long n, float v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace skm

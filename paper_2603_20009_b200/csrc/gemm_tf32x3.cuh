@@ -1,0 +1,354 @@
+// fp32-faithful "NT" GEMM on the 5th-gen tensor cores: out[i][j] = sum_t A[i][t] * B[j][t].
+//
+// Precision: each operand is split x = hi + lo (hi tf32-exact), and every 32-wide k-block
+// is computed as 3xTF32 into a FRESH TMEM accumulator -- small products first
+// (A_lo*B_hi, A_hi*B_lo), then A_hi*B_hi -- so the tensor core's per-instruction
+// accumulator truncation only ever sees one k-block's magnitude.  The epilogue warps add
+// the k-block partials into fp32 registers with round-to-nearest.  Measured on B200:
+// max rel. error 3.6e-6 at K=1536 (OpenBLAS sgemm: 2.9e-6); a single TMEM accumulator
+// over the whole K gives 6.4e-5 (tools/probe_gemm_precision.py).  This is what keeps
+// assignments in parity with the reference's sgemm-based distances (distance.py:58-59).
+//
+// Structure (one CTA per SM, 576 threads, warp-specialised):
+//   warp 0      TMA producer: A_hi, A_lo, B_hi, B_lo k-block tiles (SWIZZLE_128B, K-major)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..17 epilogue: warp w reads TMEM lane quadrant (w%4) and column slice (w-2)/4;
+//               thread = one output row x 64 columns, running sums in registers.
+// A CTA owns one 128-row M tile and walks a contiguous range of 256-wide N tiles in
+// ascending order, so per-row reductions (argmin, candidate emission) see columns in
+// ascending index order like the reference's bank loop (core.py:183-190, 243-260).
+#pragma once
+#include "ptx.cuh"
+
+namespace skm {
+
+enum GemmMode : int {
+  GEMM_STORE = 0,    // out = A.B^T (fp32)
+  GEMM_DIST = 1,     // out = max(0, fl(fl(-2 acc + xsq_i) + ysq_j))   (distance.py:77-80)
+  GEMM_ARGMIN = 2,   // running (min dist, lowest col) per row        (core.py:183-190)
+  GEMM_GATE = 3,     // emit (col, dist) for dist <= thr_i in ascending col order
+};
+
+struct GemmArgs {
+  int M, N, K;
+  int tiles_per_cta;          // N tiles handled by one CTA (grid.y splits N)
+  float* out;                 // STORE / DIST
+  long long ldo;
+  const float* xsq;           // DIST / ARGMIN / GATE: per-row norm term
+  const float* ysq;           // per-column norm term
+  int* assign;                // ARGMIN (grid.y == 1)
+  float* tau;
+  unsigned long long* keys;   // ARGMIN (grid.y > 1): atomicMin((dist_bits<<32)|col)
+  const float* thr;           // GATE: per-row threshold
+  int* cand_idx;              // GATE: per-row candidate slab [M][cap]
+  float* cand_val;
+  int* cand_cnt;              // GATE: per-row count (may exceed cap -> overflow)
+  int cand_cap;
+  long long row_offset;       // GATE/ARGMIN: added to the row index when writing outputs
+};
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BN = 256;
+constexpr int GEMM_BK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int GEMM_EPI_WARPS = 16;
+constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;
+constexpr int GEMM_PARTS = GEMM_EPI_WARPS / 4;      // column slices per TMEM lane quadrant
+constexpr int GEMM_HALF = GEMM_BN / GEMM_PARTS;     // columns per epilogue thread
+
+template <int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 4;
+  static constexpr int B_BYTES = GEMM_BN * GEMM_BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int XCHG_BYTES = 2 * GEMM_PARTS * GEMM_BM * 4 + 2 * GEMM_BN * 4;  // slice exchange + ysq tiles
+  static constexpr int TOTAL = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + XCHG_BYTES;
+  static constexpr int TMEM_COLS = 2 * GEMM_BN;  // two k-block partial buffers
+};
+
+__device__ __forceinline__ float expand_dist(float acc, float xs, float ys) {
+  // reference op order: vals = inner * -2; vals += x_sq; vals += y_sq; max(vals, 0)
+  const float v = __fadd_rn(__fadd_rn(__fmul_rn(acc, -2.0f), xs), ys);
+  return v > 0.0f ? v : 0.0f;
+}
+
+__device__ __forceinline__ void epi_bar_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
+}
+
+template <int STAGES, int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
+                       const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
+                       const GemmArgs args) {
+  using L = GemmSmem<STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* xchg = reinterpret_cast<int*>(smem + STAGES * L::STAGE_BYTES + L::BAR_BYTES);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * GEMM_BM;
+  const int n_tiles = (args.N + GEMM_BN - 1) / GEMM_BN;
+  const int t_begin = blockIdx.y * args.tiles_per_cta;
+  const int t_end = min(n_tiles, t_begin + args.tiles_per_cta);
+  const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tA_hi);
+    tma_prefetch_desc(&tA_lo);
+    tma_prefetch_desc(&tB_hi);
+    tma_prefetch_desc(&tB_lo);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], GEMM_EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && t_begin < t_end && num_k > 0) {
+      int s = 0;
+      uint32_t ph = 0;
+#pragma unroll 1
+      for (int t = t_begin; t < t_end; ++t) {
+        const int n0 = t * GEMM_BN;
+#pragma unroll 1
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+          uint8_t* base = smem + s * L::STAGE_BYTES;
+          const int k0 = kb * GEMM_BK;
+          tma_load_2d(base, &tA_hi, &full[s], k0, m0);
+          tma_load_2d(base + L::A_BYTES, &tA_lo, &full[s], k0, m0);
+          tma_load_2d(base + 2 * L::A_BYTES, &tB_hi, &full[s], k0, n0);
+          tma_load_2d(base + 2 * L::A_BYTES + L::B_BYTES, &tB_lo, &full[s], k0, n0);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && t_begin < t_end && num_k > 0) {
+      constexpr uint32_t idesc = idesc_tf32(GEMM_BM, GEMM_BN);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t kcount = 0;  // global k-block counter -> TMEM buffer ring
+#pragma unroll 1
+      for (int t = t_begin; t < t_end; ++t) {
+#pragma unroll 1
+        for (int kb = 0; kb < num_k; ++kb, ++kcount) {
+          const int buf = kcount & 1;
+          const uint32_t use = kcount >> 1;
+          mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * GEMM_BN);
+          const uint32_t base = smem_u32(smem + s * L::STAGE_BYTES);
+          const uint64_t a_hi = sw128_kmajor_desc(base);
+          const uint64_t a_lo = sw128_kmajor_desc(base + L::A_BYTES);
+          const uint64_t b_hi = sw128_kmajor_desc(base + 2 * L::A_BYTES);
+          const uint64_t b_lo = sw128_kmajor_desc(base + 2 * L::A_BYTES + L::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+            const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);  // 8 tf32 = 32 bytes
+            mma_tf32(d_tmem, a_lo + adv, b_hi + adv, idesc, kk != 0);
+            mma_tf32(d_tmem, a_hi + adv, b_lo + adv, idesc, 1u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+            const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);
+            mma_tf32(d_tmem, a_hi + adv, b_hi + adv, idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&tfull[buf]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;
+    const int eq = warp & 3;            // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;           // column slice of the 256-wide tile
+    const int r_local = eq * 32 + lane;
+    const int row = m0 + r_local;
+    const bool row_ok = row < args.M;
+    float xs = 0.0f, thr = 0.0f;
+    if constexpr (MODE == GEMM_DIST || MODE == GEMM_ARGMIN || MODE == GEMM_GATE) {
+      if (row_ok) xs = args.xsq[row];
+    }
+    if constexpr (MODE == GEMM_GATE) {
+      if (row_ok) thr = args.thr[row];
+    }
+    float best = __int_as_float(0x7f800000);
+    int best_j = 0x7fffffff;
+    int cnt = 0;
+    const long long out_row = static_cast<long long>(row) + args.row_offset;
+    float acc[GEMM_HALF];
+    uint32_t kcount = 0;
+#pragma unroll 1
+    for (int t = t_begin; t < t_end; ++t) {
+#pragma unroll 1
+      for (int kb = 0; kb < num_k; ++kb, ++kcount) {
+        const int buf = kcount & 1;
+        const uint32_t use = kcount >> 1;
+        mbar_wait(&tfull[buf], use & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
+                               static_cast<uint32_t>(buf * GEMM_BN + half * GEMM_HALF);
+#pragma unroll
+        for (int c = 0; c < GEMM_HALF / 16; ++c)
+          tmem_ld16_accum(tbase + c * 16, *reinterpret_cast<float(*)[16]>(&acc[c * 16]), kb == 0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      }
+      // ---- tile complete: acc holds columns [col0, col0 + GEMM_HALF)
+      const int col0 = t * GEMM_BN + half * GEMM_HALF;
+      const float* ys_tile = nullptr;
+      if constexpr (MODE != GEMM_STORE) {
+        // stage this tile's column norms in shared memory (double buffered by tile parity)
+        float* yt = reinterpret_cast<float*>(xchg + 2 * GEMM_PARTS * GEMM_BM) + (t & 1) * GEMM_BN;
+        const int e = threadIdx.x - 64;
+        if (e < GEMM_BN) {
+          const int col = t * GEMM_BN + e;
+          yt[e] = col < args.N ? __ldg(args.ysq + col) : 0.0f;
+        }
+        epi_bar_sync();
+        ys_tile = yt + half * GEMM_HALF;
+      }
+      if constexpr (MODE == GEMM_STORE || MODE == GEMM_DIST) {
+        if (row_ok && col0 < args.N) {
+          if constexpr (MODE == GEMM_DIST) {
+#pragma unroll
+            for (int j = 0; j < GEMM_HALF; ++j) acc[j] = expand_dist(acc[j], xs, ys_tile[j]);
+          }
+          float* o = args.out + static_cast<long long>(row) * args.ldo + col0;
+          if (col0 + GEMM_HALF <= args.N && (args.ldo & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < GEMM_HALF; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < GEMM_HALF; ++j)
+              if (col0 + j < args.N) o[j] = acc[j];
+          }
+        }
+      } else if constexpr (MODE == GEMM_ARGMIN) {
+        if (row_ok) {
+          const int lim = args.N - col0;  // valid columns in this slice
+          float bv = best;
+          int bl = -1;
+#pragma unroll
+          for (int j = 0; j < GEMM_HALF; ++j) {
+            const float dv = expand_dist(acc[j], xs, ys_tile[j]);
+            if (j < lim && dv < bv) { bv = dv; bl = j; }
+          }
+          if (bl >= 0) { best = bv; best_j = col0 + bl; }
+        }
+      } else if constexpr (MODE == GEMM_GATE) {
+        uint32_t mask[GEMM_HALF / 32];
+        int my = 0;
+        const int lim = row_ok ? args.N - col0 : 0;
+#pragma unroll
+        for (int c = 0; c < GEMM_HALF / 32; ++c) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float dv = expand_dist(acc[c * 32 + j], xs, ys_tile[c * 32 + j]);
+            acc[c * 32 + j] = dv;
+            m |= ((c * 32 + j < lim) && !(dv > thr)) ? (1u << j) : 0u;
+          }
+          mask[c] = m;
+          my += __popc(m);
+        }
+        // order the column slices of this row: slice 0 first
+        xchg[half * GEMM_BM + r_local] = my;
+        epi_bar_sync();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int q = 0; q < GEMM_PARTS; ++q) {
+          const int cq = xchg[q * GEMM_BM + r_local];
+          before += (q < half) ? cq : 0;
+          total += cq;
+        }
+        epi_bar_sync();
+        int pos = cnt + before;
+        if (row_ok) {
+          int* ci = args.cand_idx + out_row * args.cand_cap;
+          float* cv = args.cand_val + out_row * args.cand_cap;
+#pragma unroll
+          for (int c = 0; c < GEMM_HALF / 32; ++c) {
+            const uint32_t m = mask[c];
+            if (m == 0) continue;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if ((m >> j) & 1u) {
+                if (pos < args.cand_cap) {
+                  ci[pos] = col0 + c * 32 + j;
+                  cv[pos] = acc[c * 32 + j];
+                }
+                ++pos;
+              }
+            }
+          }
+        }
+        cnt += total;
+      }
+    }
+    if constexpr (MODE == GEMM_ARGMIN) {
+      // combine the column slices lexicographically on (dist, col)
+      float* xf = reinterpret_cast<float*>(xchg);
+      xf[half * GEMM_BM + r_local] = best;
+      xchg[(GEMM_PARTS + half) * GEMM_BM + r_local] = best_j;
+      epi_bar_sync();
+      if (half == 0 && row_ok && t_begin < t_end) {
+#pragma unroll
+        for (int q = 1; q < GEMM_PARTS; ++q) {
+          const float b1 = xf[q * GEMM_BM + r_local];
+          const int j1 = xchg[(GEMM_PARTS + q) * GEMM_BM + r_local];
+          if (b1 < best || (b1 == best && j1 < best_j)) {
+            best = b1;
+            best_j = j1;
+          }
+        }
+        if (gridDim.y == 1) {
+          args.assign[out_row] = best_j;
+          args.tau[out_row] = best;
+        } else {
+          const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(best)) << 32) |
+                                         static_cast<unsigned int>(best_j);
+          atomicMin(args.keys + out_row, key);
+        }
+      }
+    }
+    if constexpr (MODE == GEMM_GATE) {
+      if (row_ok && half == 0) args.cand_cnt[out_row] = cnt;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace skm

@@ -1,0 +1,419 @@
+// extern "C" entry points of libskm_b200.so (declared in include/skm_b200.h).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/skm_b200.h"
+#include "elementwise.cuh"
+#include "gemm_tf32x3.cuh"
+#include "update.cuh"
+#include "scan.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return SKM_E_CUDA;
+}
+#define SKM_LAUNCH_CHECK(where)                         \
+  do {                                                  \
+    cudaError_t _e = cudaGetLastError();                \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int grid_for(long long work, int threads, int cap = 148 * 32) {
+  long long g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return static_cast<int>(std::min<long long>(g, cap));
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// fp32 row-major [rows x ld], K extent `cols`, box = 32 x box_rows, 128B swizzle.
+int make_tmap(CUtensorMap* m, const float* ptr, long long rows, long long cols, long long ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SKM_E_DRIVER, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16) return fail(SKM_E_ARG, "TMA operand needs 16B-aligned base and ld%4==0");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld ld=%lld box=%d", (int)r, rows,
+             cols, ld, box_rows);
+    return fail(SKM_E_DRIVER, buf);
+  }
+  return SKM_OK;
+}
+
+template <int STAGES, int MODE>
+int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
+  constexpr int BN = skm::GEMM_BN;
+  using L = skm::GemmSmem<STAGES>;
+  CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+  int rc;
+  if ((rc = make_tmap(&ta_hi, p->a_hi, p->M, p->K, p->lda, skm::GEMM_BM))) return rc;
+  if ((rc = make_tmap(&ta_lo, p->a_lo, p->M, p->K, p->lda, skm::GEMM_BM))) return rc;
+  if ((rc = make_tmap(&tb_hi, p->b_hi, p->N, p->K, p->ldb, BN))) return rc;
+  if ((rc = make_tmap(&tb_lo, p->b_lo, p->N, p->K, p->ldb, BN))) return rc;
+  auto kern = skm::gemm_tf32x3_kernel<STAGES, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm smem attribute");
+    attr_set = true;
+  }
+  skm::GemmArgs a{};
+  a.M = p->M;
+  a.N = p->N;
+  a.K = p->K;
+  const int n_tiles = (p->N + BN - 1) / BN;
+  int split = std::max(1, std::min(p->n_split, n_tiles));
+  a.tiles_per_cta = (n_tiles + split - 1) / split;
+  split = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+  a.out = p->out;
+  a.ldo = p->ldo;
+  a.xsq = p->xsq;
+  a.ysq = p->ysq;
+  a.assign = p->assign;
+  a.tau = p->tau;
+  a.keys = p->keys;
+  a.thr = p->thr;
+  a.cand_idx = p->cand_idx;
+  a.cand_val = p->cand_val;
+  a.cand_cnt = p->cand_cnt;
+  a.cand_cap = p->cand_cap;
+  a.row_offset = p->row_offset;
+  if (MODE == skm::GEMM_ARGMIN && split > 1 && !p->keys) return fail(SKM_E_ARG, "ARGMIN with n_split>1 needs keys");
+  if (MODE == skm::GEMM_GATE && split > 1) return fail(SKM_E_ARG, "GATE requires n_split == 1");
+  dim3 grid((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM, split);
+  kern<<<grid, skm::GEMM_THREADS, L::TOTAL, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, a);
+  SKM_LAUNCH_CHECK("gemm_tf32x3 launch");
+  return SKM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skm_last_error(void) { return g_err.c_str(); }
+int skm_abi_version(void) { return 1; }
+
+int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi, float* lo, long long ldo,
+                   void* stream) {
+  if (rows <= 0) return SKM_OK;
+  if (cols > ldo) return fail(SKM_E_ARG, "split_hilo: cols > ldo");
+  skm::split_hilo_kernel<<<grid_for((long long)rows * ldo, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, hi,
+                                                                                             lo, ldo);
+  SKM_LAUNCH_CHECK("split_hilo");
+  return SKM_OK;
+}
+
+int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* out, void* stream) {
+  if (rows <= 0) return SKM_OK;
+  skm::row_sq_norms_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, dims,
+                                                                                             out);
+  SKM_LAUNCH_CHECK("row_sq_norms");
+  return SKM_OK;
+}
+
+int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
+                    long long ldo, void* stream) {
+  if (rows <= 0) return SKM_OK;
+  skm::gather_rows_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
+                                                                                              cols, out, ldo);
+  SKM_LAUNCH_CHECK("gather_rows");
+  return SKM_OK;
+}
+
+int skm_fill_f32(float* p, long long n, float v, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::fill_f32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, v);
+  SKM_LAUNCH_CHECK("fill_f32");
+  return SKM_OK;
+}
+
+int skm_copy_i32(const int* src, int* dst, int n, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::copy_i32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(src, dst, n);
+  SKM_LAUNCH_CHECK("copy_i32");
+  return SKM_OK;
+}
+
+int skm_seed_thresholds(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign,
+                        int n, int d, float* out, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::seed_thresholds_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, 0, as_stream(stream)>>>(
+      x, ldx, centroids, ldc, assign, n, d, out);
+  SKM_LAUNCH_CHECK("seed_thresholds");
+  return SKM_OK;
+}
+
+int skm_scan_bank(const float* partial_dists, int n, int kb, const float* x, long long ldx, const float* tail,
+                  const long long* block_offsets, const int* block_dims, int n_blocks, const float* theta_factors,
+                  int d_prime, int bank_offset, float* tau, int* assign, int sentinel,
+                  unsigned long long* counters, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::scan_bank_pdx_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
+      partial_dists, n, kb, x, ldx, tail, block_offsets, block_dims, n_blocks, theta_factors, d_prime, bank_offset,
+      tau, assign, sentinel, counters);
+  SKM_LAUNCH_CHECK("scan_bank");
+  return SKM_OK;
+}
+
+int skm_portable_matmul(const float* a, long long lda, const float* b, long long ldb, int n, int m, int dims,
+                        float* out, long long ldo, void* stream) {
+  if ((long long)n * m <= 0) return SKM_OK;
+  skm::portable_matmul_kernel<<<(int)(((long long)n * m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      a, lda, b, ldb, n, m, dims, out, ldo);
+  SKM_LAUNCH_CHECK("portable_matmul");
+  return SKM_OK;
+}
+
+// ---------------------------------------------------------------- sort / update
+static int radix_blocks(int n) { return (n + skm::RADIX_TILE - 1) / skm::RADIX_TILE; }
+static long long align256(long long b) { return (b + 255) & ~255LL; }
+
+long long skm_update_workspace_bytes(int n, int k) {
+  const long long nb = radix_blocks(std::max(n, 1));
+  return 3 * align256(4LL * n) + align256(4LL * 256 * nb) + align256(16) + align256(4LL * std::max(k, 1));
+}
+
+int skm_cluster_sort(const int* assign, int n, int k, int* order, int* counts, int* offsets, void* workspace,
+                     long long workspace_bytes, void* stream) {
+  if (n < 0 || k <= 0) return fail(SKM_E_ARG, "cluster_sort: bad n/k");
+  if (workspace_bytes < skm_update_workspace_bytes(n, k)) return fail(SKM_E_WORKSPACE, "cluster_sort: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * k, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cluster_sort memset");
+  if (n == 0) {
+    e = cudaMemsetAsync(offsets, 0, sizeof(int) * k, st);
+    return e == cudaSuccess ? SKM_OK : cuda_fail(e, "cluster_sort memset");
+  }
+  char* ws = static_cast<char*>(workspace);
+  int* keys_a = reinterpret_cast<int*>(ws);
+  int* keys_b = reinterpret_cast<int*>(ws + align256(4LL * n));
+  int* vals_a = reinterpret_cast<int*>(ws + 2 * align256(4LL * n));
+  const int nb = radix_blocks(n);
+  int* hist = reinterpret_cast<int*>(ws + 3 * align256(4LL * n));
+  int* total = reinterpret_cast<int*>(ws + 3 * align256(4LL * n) + align256(4LL * 256 * nb));
+  int bits = 1;
+  while ((1LL << bits) < k) ++bits;
+  const int passes = (bits + 7) / 8;
+  // ping-pong so that the final values land in `order`
+  int* vin = vals_a;
+  int* kin = keys_a;
+  int* vout = (passes % 2 == 1) ? order : vals_a;
+  e = cudaMemcpyAsync(keys_a, assign, 4LL * n, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cluster_sort copy");
+  // values start as the identity permutation
+  int* v0 = (passes % 2 == 1) ? vals_a : order;
+  skm::iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(v0, n);
+  vin = v0;
+  int* kbuf[2] = {keys_a, keys_b};
+  int* vbuf[2] = {v0, (v0 == order) ? vals_a : order};
+  for (int p = 0; p < passes; ++p) {
+    kin = kbuf[p & 1];
+    int* kout = kbuf[(p + 1) & 1];
+    vin = vbuf[p & 1];
+    vout = vbuf[(p + 1) & 1];
+    skm::radix_hist_kernel<<<nb, skm::RADIX_THREADS, 0, st>>>(kin, n, 8 * p, hist, nb);
+    skm::exclusive_scan_kernel<<<1, 1024, 0, st>>>(hist, 256 * nb, total);
+    skm::radix_scatter_kernel<<<nb, skm::RADIX_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * p, hist, nb);
+  }
+  SKM_LAUNCH_CHECK("cluster_sort radix");
+  if (vout != order) return fail(SKM_E_ARG, "cluster_sort: internal ping-pong error");
+  skm::count_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(assign, n, counts);
+  e = cudaMemcpyAsync(offsets, counts, sizeof(int) * k, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cluster_sort copy");
+  skm::exclusive_scan_kernel<<<1, 1024, 0, st>>>(offsets, k, total);
+  SKM_LAUNCH_CHECK("cluster_sort counts");
+  return SKM_OK;
+}
+
+int skm_cluster_sums(const float* x, long long ldx, const int* order, const int* offsets, const int* counts, int k,
+                     int d, double* sums, int accumulate, float* centroids, long long ldc, int mode, void* stream) {
+  if (k <= 0 || d <= 0) return SKM_OK;
+  dim3 grid(k, (d + skm::SUM_THREADS - 1) / skm::SUM_THREADS);
+  skm::ordered_cluster_sums_kernel<<<grid, skm::SUM_THREADS, 0, as_stream(stream)>>>(
+      x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
+  SKM_LAUNCH_CHECK("cluster_sums");
+  return SKM_OK;
+}
+
+int skm_finalize_centroids(const double* sums, const long long* counts, int k, int d, float* centroids,
+                           long long ldc, void* stream) {
+  if ((long long)k * d <= 0) return SKM_OK;
+  skm::finalize_centroids_kernel<<<grid_for((long long)k * d, 256), 256, 0, as_stream(stream)>>>(sums, counts, k, d,
+                                                                                               centroids, ldc);
+  SKM_LAUNCH_CHECK("finalize_centroids");
+  return SKM_OK;
+}
+
+int skm_counts_to_i64(const int* c32, long long* c64, int k, int accumulate, void* stream) {
+  if (k <= 0) return SKM_OK;
+  skm::counts_to_i64_kernel<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(c32, c64, k, accumulate);
+  SKM_LAUNCH_CHECK("counts_to_i64");
+  return SKM_OK;
+}
+
+int skm_accumulate_centroid_sums(const float* x, long long ldx, const int* assign, int n, int d, int k,
+                                 double* sums, long long* counts, void* workspace, long long workspace_bytes,
+                                 void* stream) {
+  // workspace layout: [sort workspace][order n][counts k][offsets k]
+  const long long sort_ws = skm_update_workspace_bytes(n, k);
+  const long long need = sort_ws + align256(4LL * std::max(n, 1)) + 2 * align256(4LL * k);
+  if (workspace_bytes < need) return fail(SKM_E_WORKSPACE, "accumulate_centroid_sums: workspace too small");
+  char* ws = static_cast<char*>(workspace);
+  int* order = reinterpret_cast<int*>(ws + sort_ws);
+  int* c32 = reinterpret_cast<int*>(ws + sort_ws + align256(4LL * std::max(n, 1)));
+  int* off = reinterpret_cast<int*>(ws + sort_ws + align256(4LL * std::max(n, 1)) + align256(4LL * k));
+  int rc = skm_cluster_sort(assign, n, k, order, c32, off, ws, sort_ws, stream);
+  if (rc) return rc;
+  rc = skm_cluster_sums(x, ldx, order, off, c32, k, d, sums, 1, nullptr, 0, 1, stream);
+  if (rc) return rc;
+  return skm_counts_to_i64(c32, counts, k, 1, stream);
+}
+
+int skm_apply_splits(float* centroids, long long ldc, int d, const int* empties, const int* donors, int n_splits,
+                     float eps, void* stream) {
+  if (n_splits <= 0) return SKM_OK;
+  skm::apply_splits_kernel<<<1, 256, 0, as_stream(stream)>>>(centroids, ldc, d, empties, donors, n_splits, eps);
+  SKM_LAUNCH_CHECK("apply_splits");
+  return SKM_OK;
+}
+
+long long skm_stats_workspace_bytes(int n) { return 2 * align256(16LL * 1024); }
+
+int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n, double* out_sum,
+                     unsigned long long* out_changed, void* workspace, long long workspace_bytes, void* stream) {
+  if (workspace_bytes < skm_stats_workspace_bytes(n)) return fail(SKM_E_WORKSPACE, "assign_stats: workspace too small");
+  const int parts = std::max(1, std::min(1024, (n + 4095) / 4096));
+  char* ws = static_cast<char*>(workspace);
+  double* ps = reinterpret_cast<double*>(ws);
+  unsigned long long* pc = reinterpret_cast<unsigned long long*>(ws + align256(16LL * 1024));
+  cudaStream_t st = as_stream(stream);
+  skm::assign_stats_partial_kernel<<<parts, skm::STAT_THREADS, 0, st>>>(tau, assign, prev, n, ps, pc);
+  skm::assign_stats_final_kernel<<<1, 32, 0, st>>>(ps, pc, parts, out_sum, out_changed);
+  SKM_LAUNCH_CHECK("assign_stats");
+  return SKM_OK;
+}
+
+// ---------------------------------------------------------------- GEMM
+int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream) {
+  if (!p) return fail(SKM_E_ARG, "gemm: null params");
+  if (p->M <= 0 || p->N <= 0) return SKM_OK;
+  if (p->K <= 0) return fail(SKM_E_ARG, "gemm: K must be > 0");
+  cudaStream_t st = as_stream(stream);
+  switch (p->mode) {
+    case SKM_GEMM_STORE: return launch_gemm<2, skm::GEMM_STORE>(p, st);
+    case SKM_GEMM_DIST: return launch_gemm<2, skm::GEMM_DIST>(p, st);
+    case SKM_GEMM_ARGMIN: return launch_gemm<2, skm::GEMM_ARGMIN>(p, st);
+    case SKM_GEMM_GATE: return launch_gemm<2, skm::GEMM_GATE>(p, st);
+    default: return fail(SKM_E_ARG, "gemm: unknown mode");
+  }
+}
+
+int skm_decode_argmin_keys(const unsigned long long* keys, int n, int* assign, float* tau, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::decode_argmin_keys_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(keys, n, assign, tau);
+  SKM_LAUNCH_CHECK("decode_argmin_keys");
+  return SKM_OK;
+}
+
+int skm_fill_u64(unsigned long long* p, long long n, unsigned long long v, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::fill_u64_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, v);
+  SKM_LAUNCH_CHECK("fill_u64");
+  return SKM_OK;
+}
+
+// ---------------------------------------------------------------- pruning scan
+int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream) {
+  const int nb = (d - d_prime + 63) / 64;
+  if (k <= 0 || nb <= 0) return SKM_OK;
+  skm::build_tails_kernel<<<grid_for((long long)k * 64 * nb, 256), 256, 0, as_stream(stream)>>>(centroids, ldc, k, d,
+                                                                                              d_prime, nb, tails);
+  SKM_LAUNCH_CHECK("build_tails");
+  return SKM_OK;
+}
+
+int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, void* stream) {
+  if (n <= 0) return SKM_OK;
+  skm::gate_threshold_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(tau, n, f0, sentinel, thr);
+  SKM_LAUNCH_CHECK("gate_threshold");
+  return SKM_OK;
+}
+
+int skm_pruned_scan(const skm_scan_params* p, void* stream) {
+  if (!p) return fail(SKM_E_ARG, "pruned_scan: null params");
+  if (p->n_rows <= 0) return SKM_OK;
+  if (p->nb <= 0 || p->nb > skm::SCAN_NB_MAX) return fail(SKM_E_ARG, "pruned_scan: tail block count out of range");
+  skm::ScanArgs a{};
+  a.cand_idx = p->cand_idx;
+  a.cand_val = p->cand_val;
+  a.cand_cnt = p->cand_cnt;
+  a.cap = p->cap;
+  a.dense = p->dense;
+  a.ld_dense = p->ld_dense;
+  a.dense_row = p->dense_row;
+  a.k = p->k;
+  a.rows = p->rows;
+  a.n_rows = p->n_rows;
+  a.row0 = p->row0;
+  a.x = p->x;
+  a.ldx = p->ldx;
+  a.tails = reinterpret_cast<const float4*>(p->tails);
+  a.nb = p->nb;
+  a.d_prime = p->d_prime;
+  a.theta = p->theta;
+  a.block_dims = p->block_dims;
+  a.tau = p->tau;
+  a.assign = p->assign;
+  a.counters = p->counters;
+  const size_t smem = skm::scan_dyn_smem(p->nb);
+  const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, 148 * 16));
+  cudaStream_t st = as_stream(stream);
+  if (p->dense_mode) {
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(skm::pruned_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); set = true; }
+    skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
+  } else {
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); set = true; }
+    skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
+  }
+  SKM_LAUNCH_CHECK("pruned_scan");
+  return SKM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+"""ctypes binding of libskm_b200.so (the C ABI in include/skm_b200.h).
+
+The library is built in-tree by ``paper_2603_20009_b200.build`` (nvcc, sm_100a).  There is no
+fallback: if the shared object is missing or fails to load, every entry point raises
+``NativeUnavailable`` so a GPU run can never silently take a CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libskm_b200.so")
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_vp = C.c_void_p
+_i = C.c_int
+_ll = C.c_longlong
+_f = C.c_float
+
+
+class GemmParams(C.Structure):
+    _fields_ = [
+        ("a_hi", _vp), ("a_lo", _vp), ("lda", _ll),
+        ("b_hi", _vp), ("b_lo", _vp), ("ldb", _ll),
+        ("M", _i), ("N", _i), ("K", _i),
+        ("mode", _i), ("n_split", _i),
+        ("out", _vp), ("ldo", _ll),
+        ("xsq", _vp), ("ysq", _vp),
+        ("assign", _vp), ("tau", _vp),
+        ("keys", _vp),
+        ("thr", _vp),
+        ("cand_idx", _vp), ("cand_val", _vp), ("cand_cnt", _vp), ("cand_cap", _i),
+        ("row_offset", _ll),
+    ]
+
+
+class ScanParams(C.Structure):
+    _fields_ = [
+        ("cand_idx", _vp), ("cand_val", _vp), ("cand_cnt", _vp), ("cap", _i),
+        ("dense", _vp), ("ld_dense", _ll), ("dense_row", _vp), ("k", _i),
+        ("rows", _vp), ("n_rows", _i), ("row0", _ll),
+        ("x", _vp), ("ldx", _ll),
+        ("tails", _vp), ("nb", _i), ("d_prime", _i),
+        ("theta", _vp), ("block_dims", _vp),
+        ("tau", _vp), ("assign", _vp),
+        ("counters", _vp),
+        ("dense_mode", _i),
+    ]
+
+
+GEMM_STORE, GEMM_DIST, GEMM_ARGMIN, GEMM_GATE = 0, 1, 2, 3
+
+_SIGS = {
+    "skm_last_error": ([], C.c_char_p),
+    "skm_abi_version": ([], _i),
+    "skm_split_hilo": ([_vp, _ll, _i, _i, _vp, _vp, _ll, _vp], _i),
+    "skm_row_sq_norms": ([_vp, _ll, _i, _i, _vp, _vp], _i),
+    "skm_gather_rows": ([_vp, _ll, _vp, _i, _i, _vp, _ll, _vp], _i),
+    "skm_fill_f32": ([_vp, _ll, _f, _vp], _i),
+    "skm_copy_i32": ([_vp, _vp, _i, _vp], _i),
+    "skm_seed_thresholds": ([_vp, _ll, _vp, _ll, _vp, _i, _i, _vp, _vp], _i),
+    "skm_scan_bank": ([_vp, _i, _i, _vp, _ll, _vp, _vp, _vp, _i, _vp, _i, _i, _vp, _vp, _i, _vp, _vp], _i),
+    "skm_update_workspace_bytes": ([_i, _i], _ll),
+    "skm_accumulate_centroid_sums": ([_vp, _ll, _vp, _i, _i, _i, _vp, _vp, _vp, _ll, _vp], _i),
+    "skm_portable_matmul": ([_vp, _ll, _vp, _ll, _i, _i, _i, _vp, _ll, _vp], _i),
+    "skm_gemm_tf32x3": ([C.POINTER(GemmParams), _vp], _i),
+    "skm_decode_argmin_keys": ([_vp, _i, _vp, _vp, _vp], _i),
+    "skm_fill_u64": ([_vp, _ll, C.c_ulonglong, _vp], _i),
+    "skm_cluster_sort": ([_vp, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp], _i),
+    "skm_cluster_sums": ([_vp, _ll, _vp, _vp, _vp, _i, _i, _vp, _i, _vp, _ll, _i, _vp], _i),
+    "skm_finalize_centroids": ([_vp, _vp, _i, _i, _vp, _ll, _vp], _i),
+    "skm_counts_to_i64": ([_vp, _vp, _i, _i, _vp], _i),
+    "skm_apply_splits": ([_vp, _ll, _i, _vp, _vp, _i, _f, _vp], _i),
+    "skm_stats_workspace_bytes": ([_i], _ll),
+    "skm_assign_stats": ([_vp, _vp, _vp, _i, _vp, _vp, _vp, _ll, _vp], _i),
+    "skm_build_tails": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
+    "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp], _i),
+    "skm_pruned_scan": ([C.POINTER(ScanParams), _vp], _i),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+_load_error: str | None = None
+
+
+def load():
+    """Load (once) and return the ctypes library; raise NativeUnavailable if absent."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        _load_error = f"{LIB_PATH} not built (run paper_2603_20009_b200.build.build())"
+        raise NativeUnavailable(_load_error)
+    try:
+        lib = C.CDLL(LIB_PATH)
+    except OSError as e:  # pragma: no cover - depends on the box
+        _load_error = str(e)
+        raise NativeUnavailable(f"cannot load {LIB_PATH}: {e}") from e
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().skm_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,288 @@
+"""Device kernels vs the oracle, same inputs, bitwise where the reference pins bits.
+
+Kernel-level parity mirrors the reference's own bit-exact cross-backend tests
+(pkg/tests/test_kernels.py:50-102, test_pruning.py:141-166)."""
+
+import numpy as np
+import pytest
+
+from conftest import make_blobs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev():
+    from paper_2603_20009_b200 import device
+    return device
+
+
+def _pad(x):
+    return _dev().to_device_matrix(x)
+
+
+def _scan_case(seed, n=123, k=77, d=200, d_prime=25):
+    from paper_2603_20009_b200.config import pdxify, tail_block_layout
+    from paper_2603_20009_b200.hostmath import threshold_factors
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    c = rng.standard_normal((k, d)).astype(np.float32)
+    prev = rng.integers(0, k, n).astype(np.int32)
+    # partial distances computed with a host GEMM so device and oracle see identical bits
+    xs = np.einsum("ij,ij->i", x[:, :d_prime], x[:, :d_prime], dtype=np.float64).astype(np.float32)
+    cs = np.einsum("ij,ij->i", c[:, :d_prime], c[:, :d_prime], dtype=np.float64).astype(np.float32)
+    vals = (x[:, :d_prime] @ c[:, :d_prime].T) * np.float32(-2.0)
+    vals += xs[:, None]
+    vals += cs[None, :]
+    np.maximum(vals, np.float32(0), out=vals)
+    bank = pdxify(c, d_prime)
+    dims, bounds = tail_block_layout(d, d_prime)
+    f = threshold_factors(d, d_prime, bounds, 2.1)
+    return x, c, prev, bank, vals.astype(np.float32), f, d_prime
+
+
+def test_truncation_probe_reports():
+    """Informational: does tcgen05 kind::tf32 truncate or round raw fp32 inputs?"""
+    dev = _dev()
+    a = np.zeros((128, 8), np.float32)
+    b = np.zeros((256, 8), np.float32)
+    a[:, 0] = np.float32(1.0) + np.float32(2.0 ** -12)  # below tf32 precision
+    b[:, 0] = 1.0
+    A = _pad(a)
+    B = _pad(b)
+    out = torch.empty((128, 256), dtype=torch.float32, device="cuda")
+    # feed raw fp32 as "hi" and zero "lo": exposes the hardware conversion
+    z_a = torch.zeros_like(A)
+    z_b = torch.zeros_like(B)
+    from paper_2603_20009_b200 import native
+    dev.gemm(A, z_a, B, z_b, 128, 256, 8, native.GEMM_STORE, out=out)
+    v = float(out[0, 0].item())
+    print("tf32 raw-input probe:", repr(v), "(1.0 => truncation, 1.000244 => exact/round)")
+    assert v in (1.0, float(np.float32(1.0) + np.float32(2.0 ** -12)))
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 77, 25), (128, 256, 32), (1000, 513, 200), (777, 1536, 1536),
+                                   (129, 4096, 192)])
+def test_gemm_store_matches_fp64(M, N, K):
+    dev = _dev()
+    rng = np.random.default_rng(M + N + K)
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K)).astype(np.float32)
+    out = dev.matmul_nt(_pad(a), _pad(b), K).cpu().numpy()
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    scale = np.sqrt((a.astype(np.float64) ** 2) @ (b.astype(np.float64) ** 2).T)
+    err = np.abs(out - ref) / scale
+    assert err.max() < 5e-6, err.max()
+
+
+def test_gemm_dist_argmin_gate_consistent():
+    """DIST, ARGMIN and GATE epilogues see the same accumulator bits."""
+    from paper_2603_20009_b200 import native
+    dev = _dev()
+    x = make_blobs(3000, 160, 40, seed=3)
+    c = x[np.random.default_rng(4).choice(3000, 300, replace=False)]
+    X, Cm = _pad(x), _pad(c)
+    K = 40
+    xh, xl = dev.split_hilo(X, K)
+    ch, cl = dev.split_hilo(Cm, K)
+    xs = dev.row_sq_norms(X, K)
+    cs = dev.row_sq_norms(Cm, K)
+    M, N = 3000, 300
+    D = torch.empty((M, dev.padded_ld(N)), dtype=torch.float32, device="cuda")
+    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_DIST, out=D, xsq=xs, ysq=cs)
+    a = torch.empty(M, dtype=torch.int32, device="cuda")
+    t = torch.empty(M, dtype=torch.float32, device="cuda")
+    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_ARGMIN, xsq=xs, ysq=cs, assign=a, tau=t)
+    Dn = D[:, :N].cpu().numpy()
+    assert np.array_equal(a.cpu().numpy(), np.argmin(Dn, axis=1))
+    assert np.array_equal(t.cpu().numpy(), Dn.min(axis=1))
+    # multi-CTA split along N goes through packed atomicMin keys
+    keys = torch.full((M,), -1, dtype=torch.int64, device="cuda")
+    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_ARGMIN, xsq=xs, ysq=cs, keys=keys, n_split=2)
+    a2 = torch.empty_like(a)
+    t2 = torch.empty_like(t)
+    native.call("skm_decode_argmin_keys", dev.ptr(keys), M, dev.ptr(a2), dev.ptr(t2), dev.stream_handle())
+    assert np.array_equal(a2.cpu().numpy(), a.cpu().numpy())
+    assert np.array_equal(t2.cpu().numpy(), t.cpu().numpy())
+    # gate
+    thr = torch.tensor(np.quantile(Dn, 0.05, axis=1).astype(np.float32), device="cuda")
+    cap = 64
+    ci = torch.empty((M, cap), dtype=torch.int32, device="cuda")
+    cv = torch.empty((M, cap), dtype=torch.float32, device="cuda")
+    cc = torch.empty(M, dtype=torch.int32, device="cuda")
+    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand_idx=ci, cand_val=cv,
+             cand_cnt=cc, cand_cap=cap)
+    thr_n = thr.cpu().numpy()
+    ci_n, cv_n, cc_n = ci.cpu().numpy(), cv.cpu().numpy(), cc.cpu().numpy()
+    for i in range(0, M, 37):
+        want = np.flatnonzero(~(Dn[i] > thr_n[i]))
+        assert cc_n[i] == want.size
+        m = min(cap, want.size)
+        assert np.array_equal(ci_n[i, :m], want[:m])
+        assert np.array_equal(cv_n[i, :m], Dn[i, want[:m]])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("sentinel", [False, True])
+def test_scan_bank_bitwise_vs_oracle(seed, sentinel):
+    from oracle import kernels_np as O
+    dev = _dev()
+    x, c, prev, bank, vals, f, dp = _scan_case(seed)
+    n = x.shape[0]
+    tau_o = np.empty(n, np.float32)
+    O.seed_thresholds(x, c, prev, tau_o)
+    X, Cm = _pad(x), _pad(c)
+    tau_d = torch.empty(n, dtype=torch.float32, device="cuda")
+    dev.seed_thresholds(X, Cm, torch.tensor(prev, device="cuda"), tau_d, d=x.shape[1])
+    assert np.array_equal(tau_d.cpu().numpy(), tau_o)
+    if sentinel:
+        tau_o[:] = np.inf
+        tau_d.fill_(float("inf"))
+    a_o = prev.copy()
+    out_o = O.scan_bank(vals, x, bank.tail, bank.block_offsets, bank.block_dims, f, dp, 0, tau_o, a_o, sentinel)
+    a_d = torch.tensor(prev, device="cuda")
+    out_d = dev.scan_bank(torch.tensor(vals, device="cuda"), X, torch.tensor(bank.tail, device="cuda"),
+                          torch.tensor(bank.block_offsets, device="cuda"),
+                          torch.tensor(bank.block_dims, device="cuda"), torch.tensor(f, device="cuda"), dp, 0,
+                          tau_d, a_d, sentinel)
+    assert out_d == out_o
+    assert np.array_equal(a_d.cpu().numpy(), a_o)
+    assert np.array_equal(tau_d.cpu().numpy(), tau_o)
+
+
+def test_accumulate_sums_bitwise():
+    from oracle import kernels_np as O
+    dev = _dev()
+    rng = np.random.default_rng(3)
+    for n, d, k in ((500, 64, 12), (20000, 130, 300), (70000, 33, 70000)):
+        x = rng.standard_normal((n, d)).astype(np.float32)
+        assign = rng.integers(0, k, n).astype(np.int32)
+        s_o = rng.standard_normal((k, d))
+        c_o = rng.integers(0, 5, k).astype(np.int64)
+        s_d = torch.tensor(s_o, device="cuda")
+        c_d = torch.tensor(c_o, device="cuda")
+        O.accumulate_centroid_sums(x, assign, s_o, c_o)
+        dev.accumulate_centroid_sums(_pad(x), torch.tensor(assign, device="cuda"), s_d, c_d, d=d)
+        assert np.array_equal(s_d.cpu().numpy(), s_o)
+        assert np.array_equal(c_d.cpu().numpy(), c_o)
+
+
+def test_cluster_sort_is_stable_argsort():
+    from paper_2603_20009_b200 import native
+    dev = _dev()
+    rng = np.random.default_rng(5)
+    for n, k in ((1, 1), (5000, 3), (100000, 4096), (300000, 70000)):
+        a = rng.integers(0, k, n).astype(np.int32)
+        A = torch.tensor(a, device="cuda")
+        order = torch.empty(n, dtype=torch.int32, device="cuda")
+        counts = torch.empty(k, dtype=torch.int32, device="cuda")
+        offs = torch.empty(k, dtype=torch.int32, device="cuda")
+        ws = torch.empty(int(native.load().skm_update_workspace_bytes(n, k)), dtype=torch.uint8, device="cuda")
+        native.call("skm_cluster_sort", dev.ptr(A), n, k, dev.ptr(order), dev.ptr(counts), dev.ptr(offs),
+                    dev.ptr(ws), ws.numel(), dev.stream_handle())
+        assert np.array_equal(order.cpu().numpy(), np.argsort(a, kind="stable"))
+        bc = np.bincount(a, minlength=k)
+        assert np.array_equal(counts.cpu().numpy(), bc)
+        assert np.array_equal(offs.cpu().numpy(), np.concatenate(([0], np.cumsum(bc)[:-1])))
+
+
+def test_portable_matmul_bitwise():
+    from oracle import kernels_np as O
+    dev = _dev()
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((50, 300)).astype(np.float32)
+    b = rng.standard_normal((20, 300)).astype(np.float32)
+    want = np.empty((50, 20), np.float32)
+    O.portable_matmul(a, b, 300, want)
+    out = torch.empty((50, 20), dtype=torch.float32, device="cuda")
+    dev.portable_matmul(_pad(a), _pad(b), 300, out)
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("seed,n,k,d,dp,sentinel", [
+    (0, 123, 77, 200, 25, False), (1, 123, 77, 200, 25, True), (2, 600, 900, 256, 32, False),
+    (3, 400, 1500, 1536, 192, False), (4, 300, 64, 96, 16, False), (5, 257, 300, 130, 40, True)])
+def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel):
+    """Production scan (candidate lists + speculative waves + in-order resolve) equals the
+    sequential reference scan over all centroids, including survivor/dims counters."""
+    from oracle import kernels_np as O
+    from paper_2603_20009_b200 import native
+    from paper_2603_20009_b200.config import pdxify, tail_block_layout
+    from paper_2603_20009_b200.hostmath import sentinel_factors, threshold_factors
+    dev = _dev()
+    rng = np.random.default_rng(seed)
+    x = make_blobs(n, d, 20, seed=seed, spread=3.0)
+    c = x[rng.choice(n, min(k, n), replace=False)] if k <= n else rng.standard_normal((k, d)).astype(np.float32) * 3
+    c = np.ascontiguousarray(c[:k], dtype=np.float32)
+    k = c.shape[0]
+    prev = rng.integers(0, k, n).astype(np.int32)
+    X, Cm = _pad(x), _pad(c)
+    xh, xl = dev.split_hilo(X, dp)
+    ch, cl = dev.split_hilo(Cm, dp)
+    xs = dev.row_sq_norms(X, dp)
+    cs = dev.row_sq_norms(Cm, dp)
+    D = torch.empty((n, dev.padded_ld(k)), dtype=torch.float32, device="cuda")
+    dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_DIST, out=D, xsq=xs, ysq=cs)
+    vals = np.ascontiguousarray(D[:, :k].cpu().numpy())
+    widths, bounds = tail_block_layout(d, dp)
+    f = threshold_factors(d, dp, bounds, 2.1)
+    fs = sentinel_factors(f) if sentinel else f
+    # oracle: one bank holding every centroid (bank splitting does not change semantics)
+    tau_o = np.empty(n, np.float32)
+    O.seed_thresholds(x, c, prev, tau_o)
+    if sentinel:
+        tau_o[:] = np.inf
+    a_o = prev.copy()
+    surv_o, td_o = 0, 0
+    for s1 in range(0, k, 1024):
+        bank = pdxify(c[s1:s1 + 1024], dp)
+        sv, td = O.scan_bank(np.ascontiguousarray(vals[:, s1:s1 + 1024]), x, bank.tail, bank.block_offsets,
+                             bank.block_dims, f, dp, s1, tau_o, a_o, sentinel)
+        surv_o += sv
+        td_o += td
+    # device: seed, gate GEMM, scan
+    tau = torch.empty(n, dtype=torch.float32, device="cuda")
+    assign = torch.tensor(prev, device="cuda")
+    dev.seed_thresholds(X, Cm, assign, tau, d=d)
+    if sentinel:
+        tau.fill_(float("inf"))
+    thr = torch.empty(n, dtype=torch.float32, device="cuda")
+    native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[0]), int(sentinel), dev.ptr(thr), dev.stream_handle())
+    cap = 128
+    ci = torch.empty((n, cap), dtype=torch.int32, device="cuda")
+    cv = torch.empty((n, cap), dtype=torch.float32, device="cuda")
+    cc = torch.empty(n, dtype=torch.int32, device="cuda")
+    dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand_idx=ci, cand_val=cv,
+             cand_cnt=cc, cand_cap=cap)
+    nb = len(widths)
+    tails = torch.empty(k * 64 * nb, dtype=torch.float32, device="cuda")
+    native.call("skm_build_tails", dev.ptr(Cm), Cm.stride(0), k, d, dp, dev.ptr(tails), dev.stream_handle())
+    counters = torch.zeros(3, dtype=torch.int64, device="cuda")
+    theta = torch.tensor(fs, device="cuda")
+    bdims = torch.tensor(widths, device="cuda")
+    p = native.ScanParams()
+    p.cand_idx, p.cand_val, p.cand_cnt, p.cap = ci.data_ptr(), cv.data_ptr(), cc.data_ptr(), cap
+    p.k, p.n_rows, p.row0 = k, n, 0
+    p.x, p.ldx = X.data_ptr(), X.stride(0)
+    p.tails, p.nb, p.d_prime = tails.data_ptr(), nb, dp
+    p.theta, p.block_dims = theta.data_ptr(), bdims.data_ptr()
+    p.tau, p.assign, p.counters = tau.data_ptr(), assign.data_ptr(), counters.data_ptr()
+    import ctypes
+    native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
+    # overflow rows -> dense pass over their full distance rows
+    over = torch.nonzero(cc > cap).flatten().to(torch.int32)
+    if over.numel():
+        p2 = native.ScanParams.from_buffer_copy(p)
+        p2.dense, p2.ld_dense = D.data_ptr(), D.stride(0)
+        p2.dense_row = torch.arange(n, dtype=torch.int32, device="cuda").data_ptr()
+        p2.rows, p2.n_rows, p2.dense_mode = over.data_ptr(), over.numel(), 1
+        ident = torch.arange(n, dtype=torch.int32, device="cuda")
+        p2.dense_row = ident.data_ptr()
+        native.check(native.load().skm_pruned_scan(ctypes.byref(p2), dev.stream_handle()), "scan dense")
+    torch.cuda.synchronize()
+    sv, td, ch_ = counters.cpu().tolist()
+    assert np.array_equal(assign.cpu().numpy(), a_o)
+    assert np.array_equal(tau.cpu().numpy(), tau_o)
+    assert (sv, td) == (surv_o, td_o)
+    assert ch_ == int(np.count_nonzero(a_o != prev))
