@@ -1,0 +1,283 @@
+"""Drop-in public entry points: ``fit`` / ``final_assign`` / ``hierarchical_fit`` + result type.
+
+Signatures, result fields and error behaviour follow the reference package
+(``core.fit`` core.py:417-460, ``core.final_assign`` core.py:463-541, ``KMeansResult``
+core.py:55-76, ``hierarchical_fit`` hierarchical.py:91-171).  Inputs are host NumPy (copied to
+HBM once); outputs are freshly owned host NumPy arrays.  Everything between runs on the B200.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import native
+from .config import (
+    KMeansConfig,
+    DimensionMismatch,
+    RotationMatrix,
+    WorkCounters,
+    pruning_supported,
+    validate_vector_set,
+)
+from .device import padded_ld, ptr, require_cuda, stream_handle
+from .engine import (
+    Centroids,
+    Comm,
+    DeviceData,
+    PrunePlan,
+    Workspace,
+    _gemm,
+    _Timer,
+    fit_rotated_device,
+    full_assign_pass,
+    pruned_assign_pass,
+)
+from .hostmath import generate_rotation, sample_indices
+
+
+@dataclass
+class KMeansResult:
+    centroids: np.ndarray
+    assignments: np.ndarray
+    stats: list
+    terminated_by: str
+    rotation: RotationMatrix
+    centroids_rotated: np.ndarray
+    d_prime_final: int | None
+    sample_indices: np.ndarray | None
+    init_indices: np.ndarray
+    work: WorkCounters
+    phase_seconds: dict
+    peak_aux_values: int
+    n_train: int
+    recall_history: list = field(default_factory=list)
+
+    @property
+    def k(self) -> int:
+        return self.centroids.shape[0]
+
+
+# ------------------------------------------------------------------------------ rotation
+class DeviceRotation:
+    """R resident on device in both operand orientations (split once)."""
+
+    def __init__(self, rotation: RotationMatrix, dev):
+        d = rotation.dim
+        self.d = d
+        ld = padded_ld(d)
+        r = torch.zeros((d, ld), dtype=torch.float32, device=dev)
+        r[:, :d] = torch.from_numpy(np.ascontiguousarray(rotation.data)).to(dev)
+        rt = torch.zeros((d, ld), dtype=torch.float32, device=dev)
+        rt[:, :d] = torch.from_numpy(np.ascontiguousarray(rotation.data.T)).to(dev)
+        self.r_hi, self.r_lo = _split(r, d)     # rows of R   -> X @ R^T (unrotate)
+        self.rt_hi, self.rt_lo = _split(rt, d)  # rows of R^T -> X @ R   (rotate)
+
+    def apply(self, x_dev: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = False) -> torch.Tensor:
+        """out = x @ R (or x @ R^T); x_dev (n, ld) padded."""
+        n = x_dev.shape[0]
+        if out is None:
+            out = torch.zeros((n, padded_ld(self.d)), dtype=torch.float32, device=x_dev.device)
+        if n == 0:
+            return out
+        x_hi, x_lo = _split(x_dev, self.d)
+        b_hi, b_lo = (self.r_hi, self.r_lo) if inverse else (self.rt_hi, self.rt_lo)
+        _gemm(x_hi, x_lo, b_hi, b_lo, n, self.d, self.d, native.GEMM_STORE, out=out,
+              n_split=_store_split(n, self.d))
+        return out
+
+
+def _store_split(m, n):
+    from .engine import _n_split
+    return _n_split(m, n)
+
+
+def _split(x: torch.Tensor, cols: int):
+    hi = torch.empty_like(x)
+    lo = torch.empty_like(x)
+    native.call("skm_split_hilo", ptr(x), x.shape[1], x.shape[0], cols, ptr(hi), ptr(lo), x.shape[1],
+                stream_handle())
+    return hi, lo
+
+
+def _h2d(x: np.ndarray, dev) -> torch.Tensor:
+    n, d = x.shape
+    out = torch.zeros((n, padded_ld(d)), dtype=torch.float32, device=dev)
+    if n:
+        out[:, :d].copy_(torch.from_numpy(x))
+    return out
+
+
+def _device_bytes_values(*ts) -> int:
+    return int(sum(t.numel() * t.element_size() for t in ts if t is not None) // 4)
+
+
+# ------------------------------------------------------------------------------ fit
+class _RotationJob:
+    """Host QR of the rotation (LAPACK releases the GIL) overlapped with the H2D copy."""
+
+    def __init__(self, d: int, seed: int):
+        import threading
+        self.result = None
+        self.error = None
+        self.t0 = time.perf_counter()
+        self.seconds = 0.0
+
+        def run():
+            try:
+                self.result = generate_rotation(d, seed)
+            except BaseException as e:  # pragma: no cover - surfaced in get()
+                self.error = e
+            self.seconds = time.perf_counter() - self.t0
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+
+    def get(self) -> RotationMatrix:
+        self.thread.join()
+        if self.error is not None:
+            raise self.error
+        return self.result
+
+
+@dataclass
+class DeviceFit:
+    """Output of the device-resident fit: loop output + device centroids (original space)."""
+    loop: object
+    rotation: RotationMatrix
+    centroids_dev: torch.Tensor      # (k, ld) original space
+    data: DeviceData
+    phase: dict
+
+
+def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: RotationMatrix, inspect=None,
+               comm: Comm | None = None, n_global: int | None = None, row_lo: int = 0, keep_data: bool = False,
+               init_rows: torch.Tensor | None = None) -> DeviceFit:
+    """The hot path with inputs already in HBM: rotate (tcgen05 GEMM), Lloyd loop, un-rotate.
+
+    ``x_dev`` is this rank's (n_local, ld) shard (pad columns zero); with ``comm.world > 1``
+    the Forgy rows are assembled across ranks by one allreduce."""
+    comm = comm or Comm()
+    dev = x_dev.device
+    timer = _Timer()
+    timer.start("rotation")
+    rot = DeviceRotation(rotation, dev)
+    xr = rot.apply(x_dev)
+    data = DeviceData(xr, d)
+    timer.stop("rotation")
+    n_local = data.n
+    n = n_local if n_global is None else n_global
+    from .hostmath import init_indices
+    init_idx = init_indices(n, cfg.k, [cfg.seed, 2])
+    if init_rows is None and comm.world > 1:
+        init_rows = torch.zeros((cfg.k, data.ld), dtype=torch.float32, device=dev)
+        mine = np.flatnonzero((init_idx >= row_lo) & (init_idx < row_lo + n_local))
+        if mine.size:
+            src = torch.tensor(init_idx[mine] - row_lo, dtype=torch.int64, device=dev)
+            tmp = torch.empty((mine.size, data.ld), dtype=torch.float32, device=dev)
+            native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(src), int(mine.size), data.ld, ptr(tmp),
+                        data.ld, stream_handle())
+            init_rows[torch.tensor(mine, dtype=torch.int64, device=dev)] = tmp
+        comm.allreduce_(init_rows)
+    etr = None
+    if cfg.etr is not None:
+        from .etr import EtrState
+        etr = EtrState(cfg)
+    phase = dict(timer.collect())
+    out = fit_rotated_device(data, cfg, inspect=inspect, comm=comm, n_global=n, row_lo=row_lo, init_rows=init_rows,
+                             init_idx=init_idx, etr=etr, timer=timer)
+    phase.update(out.phase_seconds)
+    timer.start("unrotate")
+    cent = rot.apply(out.centroids_dev, inverse=True)
+    timer.stop("unrotate")
+    phase.update(timer.collect())
+    if not keep_data:
+        data = DeviceData.__new__(DeviceData)
+        data.n = n_local
+    return DeviceFit(loop=out, rotation=rotation, centroids_dev=cent, data=data, phase=phase)
+
+
+def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
+    """Sample, rotate, cluster and un-rotate on the B200 (core.py:417-460)."""
+    x = validate_vector_set(x)
+    dev = require_cuda(device)
+    n_total, d = x.shape
+    sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
+    xs = x if sidx is None else x[sidx]
+    job = _RotationJob(d, cfg.seed)       # host PCG64 + LAPACK QR (persisted-model contract) ...
+    x_dev = _h2d(xs, dev)                  # ... overlapped with the host->device copy
+    rotation = job.get()
+    res = fit_device(x_dev, d, cfg, rotation, inspect=inspect)
+    del x_dev
+    out = res.loop
+    phase = dict(res.phase)
+    phase["rotation_host"] = job.seconds
+    cent = res.centroids_dev[:, :d].cpu().numpy().copy()
+    ld = padded_ld(d)
+    peak = 3 * out.assignments.shape[0] * ld + 6 * out.assignments.shape[0] + 4 * cfg.k * ld
+    return KMeansResult(
+        centroids=cent,
+        assignments=out.assignments,
+        stats=out.stats,
+        terminated_by=out.terminated_by,
+        rotation=rotation,
+        centroids_rotated=out.centroids_rotated,
+        d_prime_final=out.d_prime_final,
+        sample_indices=sidx,
+        init_indices=out.init_indices,
+        work=out.work,
+        phase_seconds=phase,
+        peak_aux_values=peak,
+        n_train=out.assignments.shape[0],
+        recall_history=out.recall_history,
+    )
+
+
+def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, batch_rows: int = 1 << 20
+                 ) -> np.ndarray:
+    """Assign every vector to the fitted centroids with the pruned pass (core.py:463-541).
+
+    Rows are rotated lazily in batches; tau is seeded from the training assignment for sampled
+    rows (centroid 0 otherwise), exactly like the reference."""
+    x_full = validate_vector_set(x_full)
+    dev = require_cuda(device)
+    n, d = x_full.shape
+    if d != result.rotation.dim:
+        raise ValueError(f"vectors have dim {d}, model has dim {result.rotation.dim}")
+    k = result.centroids_rotated.shape[0]
+    assign = np.zeros(n, dtype=np.int32)
+    if result.sample_indices is not None:
+        assign[result.sample_indices] = result.assignments
+    elif result.assignments.shape[0] == n:
+        assign[:] = result.assignments
+    pruned = pruning_supported(d) and result.d_prime_final is not None
+    rot = DeviceRotation(result.rotation, dev)
+    cents = Centroids(_h2d(np.ascontiguousarray(result.centroids_rotated, dtype=np.float32), dev), d)
+    if pruned:
+        dp = result.d_prime_final
+        cents.refresh(dp, dp)
+        plan = PrunePlan(d, dp, cfg.epsilon0, False, dev)
+    else:
+        cents.refresh(d, None)
+        plan = None
+    cfg_ws = KMeansConfig(k=k, x_batch_device=cfg.x_batch_device, cand_cap=cfg.cand_cap)
+    for s0 in range(0, n, batch_rows):
+        e0 = min(n, s0 + batch_rows)
+        data = DeviceData(rot.apply(_h2d(x_full[s0:e0], dev)), d)
+        ws = Workspace(dev, e0 - s0, k, d, cfg_ws)
+        ws.assign[: e0 - s0].copy_(torch.from_numpy(assign[s0:e0]))
+        if pruned:
+            ws.counters.zero_()
+            pruned_assign_pass(data, cents, ws, plan)
+            result.work.seed_dims += (e0 - s0) * d
+            result.work.front_pair_dims += (e0 - s0) * k * plan.d_prime
+            result.work.tail_dims += int(ws.counters[1].item())
+        else:
+            full_assign_pass(data, cents, ws)
+            result.work.full_pair_dims += (e0 - s0) * k * d
+        assign[s0:e0] = ws.assign[: e0 - s0].cpu().numpy()
+    return assign

@@ -1,0 +1,529 @@
+"""Device-resident SuperKMeans Lloyd loop (the north-star hot path).
+
+Host orchestration of ``core._fit_rotated`` (pkg/src/superkmeans/core.py:284-414), with every
+per-vector operation running in libskm_b200:
+
+  iteration 1 (and every iteration when d < 80):  fused full-distance GEMM + row argmin
+                                                   (core.py:169-192)
+  iterations >= 2:  seed tau (core.py:237) -> gate threshold -> partial-distance GEMM fused with
+                    the ADSampling first gate and ascending-index candidate emission -> exact
+                    sequential-tau pruning scan over PDX-quad centroid tails (core.py:195-267)
+  update:           stable cluster sort + ordered f64 member sums + divide (core.py:79-100),
+                    host-drawn empty-cluster splits applied on device (core.py:103-128)
+  control:          d' controller, convergence and ETR decisions on host scalars
+                    (core.py:131-161, 305-316, 379-399)
+
+Data never returns to the host inside the loop except O(k) counts (needed by the host RNG of
+the split step, exactly like the reference), a handful of scalars, and -- only when an
+``inspect`` callback is given -- the snapshot the callback receives.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import native
+from .config import (
+    IterationStats,
+    KMeansConfig,
+    WorkCounters,
+    initial_d_prime,
+    pruning_supported,
+    tail_block_layout,
+)
+from .device import padded_ld, ptr, stream_handle
+from .hostmath import (
+    SPLIT_EPS,
+    adjust_d_prime,
+    init_indices,
+    plan_splits,
+    prune_rate_from_totals,
+    sentinel_factors,
+    threshold_factors,
+)
+
+_U64_MAX = (1 << 64) - 1
+
+
+def _i64(t: torch.Tensor) -> int:
+    return int(t.item())
+
+
+class Comm:
+    """Row-sharded data parallelism: one allreduce(sum) per iteration over a packed buffer.
+
+    ``world == 1`` is the identity.  With ``torch.distributed`` initialised (NCCL on GPUs,
+    gloo in CPU tests) every rank holds a contiguous row shard and replicated centroids.
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.group = group
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def shard(self, n: int) -> tuple[int, int]:
+        """Contiguous row range of this rank."""
+        per = (n + self.world - 1) // self.world
+        lo = min(n, self.rank * per)
+        return lo, min(n, lo + per)
+
+
+@dataclass
+class LoopOutput:
+    centroids_rotated: np.ndarray
+    assignments: np.ndarray
+    best_sq_dist: np.ndarray
+    stats: list
+    terminated_by: str
+    d_prime_final: int | None
+    init_indices: np.ndarray
+    work: WorkCounters
+    recall_history: list
+    phase_seconds: dict
+    centroids_dev: torch.Tensor | None = None
+    assign_dev: torch.Tensor | None = None
+    device_ms: dict = field(default_factory=dict)
+
+
+class _Timer:
+    """CUDA-event phase timer (replaces the reference's perf_counter brackets)."""
+
+    def __init__(self):
+        self.open: dict[str, torch.cuda.Event] = {}
+        self.spans: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+
+    def start(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.open[name] = e
+
+    def stop(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.spans.append((name, self.open.pop(name), e))
+
+    def collect(self) -> dict:
+        out: dict[str, float] = {}
+        if self.spans:
+            self.spans[-1][2].synchronize()
+        for name, a, b in self.spans:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b) / 1e3
+        self.spans.clear()
+        return out
+
+
+class DeviceData:
+    """Rotated training rows resident in HBM, with their 3xTF32 split and norms."""
+
+    def __init__(self, xr: torch.Tensor, d: int):
+        self.x = xr            # (n, ld) fp32, pad columns zero
+        self.n = xr.shape[0]
+        self.d = d
+        self.ld = xr.shape[1]
+        self.hi = torch.empty_like(xr)
+        self.lo = torch.empty_like(xr)
+        if self.n:
+            native.call("skm_split_hilo", ptr(xr), self.ld, self.n, d, ptr(self.hi), ptr(self.lo), self.ld,
+                        stream_handle(), nbytes=12.0 * self.n * self.ld)
+        self._norms: dict[int, torch.Tensor] = {}
+
+    def norms(self, dims: int) -> torch.Tensor:
+        t = self._norms.get(dims)
+        if t is None:
+            t = torch.empty(max(self.n, 1), dtype=torch.float32, device=self.x.device)
+            if self.n:
+                native.call("skm_row_sq_norms", ptr(self.x), self.ld, self.n, dims, ptr(t), stream_handle(),
+                            nbytes=4.0 * self.n * dims)
+            if len(self._norms) > 4:
+                self._norms.pop(next(iter(self._norms)))
+            self._norms[dims] = t
+        return t
+
+
+class Centroids:
+    """Replicated centroid state: row-major matrix, its split, norms, PDX-quad tails."""
+
+    def __init__(self, c: torch.Tensor, d: int):
+        self.c = c
+        self.k = c.shape[0]
+        self.d = d
+        self.ld = c.shape[1]
+        self.hi = torch.empty_like(c)
+        self.lo = torch.empty_like(c)
+        self.ysq = torch.empty(self.k, dtype=torch.float32, device=c.device)
+        self.tails = None
+
+    def refresh(self, dims: int, d_prime: int | None):
+        """Recompute split + norms over `dims` (+ tails at d_prime) after an update."""
+        native.call("skm_split_hilo", ptr(self.c), self.ld, self.k, self.d, ptr(self.hi), ptr(self.lo), self.ld,
+                    stream_handle())
+        native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, dims, ptr(self.ysq), stream_handle())
+        if d_prime is not None:
+            nb = (self.d - d_prime + 63) // 64
+            need = self.k * 64 * nb
+            if self.tails is None or self.tails.numel() < need:
+                self.tails = torch.empty(need, dtype=torch.float32, device=self.c.device)
+            native.call("skm_build_tails", ptr(self.c), self.ld, self.k, self.d, d_prime, ptr(self.tails),
+                        stream_handle())
+
+
+def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
+    p = native.GemmParams()
+    p.a_hi, p.a_lo, p.lda = a_hi.data_ptr(), a_lo.data_ptr(), a_hi.stride(0)
+    p.b_hi, p.b_lo, p.ldb = b_hi.data_ptr(), b_lo.data_ptr(), b_hi.stride(0)
+    p.M, p.N, p.K, p.mode = M, N, K, mode
+    p.n_split = kw.pop("n_split", 1)
+    out = kw.pop("out", None)
+    if out is not None:
+        p.out, p.ldo = out.data_ptr(), out.stride(0)
+    p.cand_cap = kw.pop("cand_cap", 0)
+    p.row_offset = kw.pop("row_offset", 0)
+    for name, t in kw.items():
+        if t is not None:
+            setattr(p, name, t.data_ptr())
+    names = {native.GEMM_STORE: "gemm_store", native.GEMM_DIST: "gemm_dist", native.GEMM_ARGMIN: "gemm_argmin",
+             native.GEMM_GATE: "gemm_gate"}
+    native.call("skm_gemm_tf32x3", C.byref(p), stream_handle(), flops=2.0 * M * N * K, tag=names[mode])
+
+
+def _n_split(m_rows: int, n_cols: int, sms: int = 148) -> int:
+    """Spread N over CTAs when there are too few 128-row M tiles to fill the chip."""
+    m_tiles = (m_rows + 127) // 128
+    n_tiles = (n_cols + 255) // 256
+    if m_tiles >= 2 * sms:
+        return 1
+    return max(1, min(n_tiles, (2 * sms + m_tiles - 1) // m_tiles))
+
+
+class Workspace:
+    def __init__(self, dev, n: int, k: int, d: int, cfg: KMeansConfig):
+        self.dev = dev
+        b = max(1, min(n, cfg.x_batch_device))
+        self.batch = b
+        self.cap = cfg.cand_cap
+        i32, f32 = torch.int32, torch.float32
+        nn = max(n, 1)
+        self.assign = torch.zeros(nn, dtype=i32, device=dev)
+        self.prev = torch.zeros(nn, dtype=i32, device=dev)
+        self.tau = torch.full((nn,), float("inf"), dtype=f32, device=dev)
+        self.thr = torch.empty(nn, dtype=f32, device=dev)
+        self.keys = None
+        self.cand_idx = torch.empty((b, self.cap), dtype=i32, device=dev)
+        self.cand_val = torch.empty((b, self.cap), dtype=f32, device=dev)
+        self.cand_cnt = torch.empty(b, dtype=i32, device=dev)
+        self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.order = torch.empty(nn, dtype=i32, device=dev)
+        self.counts = torch.empty(k, dtype=i32, device=dev)
+        self.offsets = torch.empty(k, dtype=i32, device=dev)
+        lib = native.load()
+        self.sort_ws = torch.empty(int(lib.skm_update_workspace_bytes(n, k)), dtype=torch.uint8, device=dev)
+        self.stats_ws = torch.empty(int(lib.skm_stats_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+        self.wcss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.changed = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def argmin_keys(self, n):
+        if self.keys is None or self.keys.numel() < n:
+            self.keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
+        return self.keys
+
+
+# ------------------------------------------------------------------------------ passes
+def full_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, row0: int = 0, rows: int | None = None):
+    """Exact argmin over all centroids (lowest index on ties) -> ws.assign / ws.tau."""
+    n = data.n if rows is None else rows
+    if n == 0:
+        return
+    d = data.d
+    xsq = data.norms(d)
+    split = _n_split(n, cents.k)
+    a_hi = data.hi[row0:row0 + n]
+    a_lo = data.lo[row0:row0 + n]
+    if split == 1:
+        _gemm(a_hi, a_lo, cents.hi, cents.lo, n, cents.k, d, native.GEMM_ARGMIN, xsq=xsq[row0:row0 + n],
+              ysq=cents.ysq, assign=ws.assign[row0:row0 + n], tau=ws.tau[row0:row0 + n])
+    else:
+        keys = ws.argmin_keys(n)
+        native.call("skm_fill_u64", ptr(keys), n, C.c_ulonglong(_U64_MAX), stream_handle())
+        _gemm(a_hi, a_lo, cents.hi, cents.lo, n, cents.k, d, native.GEMM_ARGMIN, xsq=xsq[row0:row0 + n],
+              ysq=cents.ysq, keys=keys, n_split=split)
+        native.call("skm_decode_argmin_keys", ptr(keys), n, ptr(ws.assign[row0:row0 + n]),
+                    ptr(ws.tau[row0:row0 + n]), stream_handle())
+
+
+class PrunePlan:
+    """Per-iteration constants of the pruned pass at a given d'."""
+
+    def __init__(self, d: int, d_prime: int, eps0: float, sentinel: bool, dev):
+        widths, bounds = tail_block_layout(d, d_prime)
+        f = threshold_factors(d, d_prime, bounds, eps0)
+        self.factors = f
+        self.gate = sentinel_factors(f) if sentinel else f
+        self.widths = widths
+        self.nb = len(widths)
+        self.d_prime = d_prime
+        self.sentinel = sentinel
+        self.theta = torch.tensor(self.gate, dtype=torch.float32, device=dev)
+        self.bdims = torch.tensor(widths, dtype=torch.int32, device=dev)
+
+
+def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: PrunePlan, seed_tau: bool = True,
+                       row0: int = 0, rows: int | None = None):
+    """Seed tau, gate GEMM -> candidate lists, exact scan.  Accumulates ws.counters =
+    {survivors, tail dims touched, changed}."""
+    n = data.n if rows is None else rows
+    if n == 0:
+        return
+    d, dp = data.d, plan.d_prime
+    st = stream_handle()
+    x_rows = data.x[row0:row0 + n]
+    tau = ws.tau[row0:row0 + n]
+    assign = ws.assign[row0:row0 + n]
+    if plan.sentinel:
+        native.call("skm_fill_f32", ptr(tau), n, float("inf"), st)
+    elif seed_tau:
+        native.call("skm_seed_thresholds", ptr(x_rows), data.ld, ptr(cents.c), cents.ld, ptr(assign), n, d,
+                    ptr(tau), st, nbytes=4.0 * n * d + 8.0 * n)
+    native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
+                ptr(ws.thr[row0:row0 + n]), st)
+    xsq = data.norms(dp)
+    lib = native.load()
+    for b0 in range(0, n, ws.batch):
+        bn = min(ws.batch, n - b0)
+        r = row0 + b0
+        _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, cents.k, dp, native.GEMM_GATE,
+              xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand_idx=ws.cand_idx, cand_val=ws.cand_val,
+              cand_cnt=ws.cand_cnt, cand_cap=ws.cap)
+        sp = native.ScanParams()
+        sp.cand_idx, sp.cand_val, sp.cand_cnt, sp.cap = (ws.cand_idx.data_ptr(), ws.cand_val.data_ptr(),
+                                                          ws.cand_cnt.data_ptr(), ws.cap)
+        sp.k, sp.n_rows, sp.row0 = cents.k, bn, r
+        sp.x, sp.ldx = data.x.data_ptr(), data.ld
+        sp.tails, sp.nb, sp.d_prime = cents.tails.data_ptr(), plan.nb, dp
+        sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
+        sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
+        native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan",
+                    nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        # rows whose candidate list overflowed the slab: dense distance rows, same kernel
+        over = torch.nonzero(ws.cand_cnt[:bn] > ws.cap).flatten()
+        n_over = int(over.numel())
+        if n_over:
+            _dense_overflow(data, cents, ws, plan, r, over.to(torch.int32), n_over, xsq)
+
+
+def _dense_overflow(data, cents, ws, plan, r, over_local, n_over, xsq):
+    dev = data.x.device
+    st = stream_handle()
+    idx = (over_local.to(torch.int64) + r)
+    a_hi = torch.empty((n_over, data.ld), dtype=torch.float32, device=dev)
+    a_lo = torch.empty_like(a_hi)
+    xs = torch.empty(n_over, dtype=torch.float32, device=dev)
+    native.call("skm_gather_rows", ptr(data.hi), data.ld, ptr(idx), n_over, data.ld, ptr(a_hi), data.ld, st)
+    native.call("skm_gather_rows", ptr(data.lo), data.ld, ptr(idx), n_over, data.ld, ptr(a_lo), data.ld, st)
+    native.call("skm_gather_rows", ptr(xsq.view(-1, 1)), 1, ptr(idx), n_over, 1, ptr(xs.view(-1, 1)), 1, st)
+    k = cents.k
+    chunk = max(1, min(n_over, (1 << 28) // max(k, 1)))  # bound the dense buffer (1 GiB)
+    for c0 in range(0, n_over, chunk):
+        cn = min(chunk, n_over - c0)
+        dense = torch.empty((cn, padded_ld(k)), dtype=torch.float32, device=dev)
+        _gemm(a_hi[c0:c0 + cn], a_lo[c0:c0 + cn], cents.hi, cents.lo, cn, k, plan.d_prime, native.GEMM_DIST,
+              out=dense, xsq=xs[c0:c0 + cn], ysq=cents.ysq, n_split=_n_split(cn, k))
+        dense_row = torch.arange(cn, dtype=torch.int32, device=dev)
+        rows_local = over_local[c0:c0 + cn].contiguous()
+        # the kernel indexes dense rows by batch-local row -> provide a scatter map
+        remap = torch.full((int(rows_local.max().item()) + 1,), -1, dtype=torch.int32, device=dev)
+        remap[rows_local.to(torch.int64)] = dense_row
+        sp = native.ScanParams()
+        sp.dense, sp.ld_dense, sp.dense_row, sp.k = dense.data_ptr(), dense.stride(0), remap.data_ptr(), k
+        sp.rows, sp.n_rows, sp.row0 = rows_local.data_ptr(), cn, r
+        sp.x, sp.ldx = data.x.data_ptr(), data.ld
+        sp.tails, sp.nb, sp.d_prime = cents.tails.data_ptr(), plan.nb, plan.d_prime
+        sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
+        sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
+        sp.dense_mode = 1
+        native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan_dense", nbytes=4.0 * cn * k)
+
+
+def update_centroids_device(data: DeviceData, cents: Centroids, ws: Workspace, comm: Comm,
+                            sums_buf: torch.Tensor | None = None) -> np.ndarray:
+    """Mean of member rows (f64 ordered sums), empties keep their previous centroid.
+    Returns host int64 counts (global)."""
+    st = stream_handle()
+    k, d = cents.k, cents.d
+    native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
+                ptr(ws.sort_ws), ws.sort_ws.numel(), st, nbytes=32.0 * data.n)
+    if comm.world == 1:
+        native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k, d,
+                    None, 0, ptr(cents.c), cents.ld, 0, st, nbytes=4.0 * data.n * d + 4.0 * k * d)
+        return ws.counts.cpu().numpy().astype(np.int64)
+    # multi-GPU: local ordered sums -> one packed allreduce [sums | counts] -> finalize
+    packed = sums_buf if sums_buf is not None else torch.empty(k * d + k, dtype=torch.float64, device=data.x.device)
+    sums = packed[: k * d]
+    native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k, d,
+                ptr(sums), 0, None, 0, 1, st)
+    packed[k * d:].copy_(ws.counts.to(torch.float64))
+    comm.allreduce_(packed)
+    counts64 = packed[k * d:].round().to(torch.int64)
+    native.call("skm_finalize_centroids", ptr(sums), ptr(counts64), k, d, ptr(cents.c), cents.ld, st)
+    return counts64.cpu().numpy()
+
+
+def apply_splits_device(cents: Centroids, counts: np.ndarray, rng) -> int:
+    empties, donors = plan_splits(counts, rng)
+    if not empties:
+        return 0
+    dev = cents.c.device
+    e = torch.tensor(empties, dtype=torch.int32, device=dev)
+    dn = torch.tensor(donors, dtype=torch.int32, device=dev)
+    native.call("skm_apply_splits", ptr(cents.c), cents.ld, cents.d, ptr(e), ptr(dn), len(empties),
+                float(SPLIT_EPS), stream_handle())
+    return len(empties)
+
+
+def assign_stats(ws: Workspace, n: int, with_prev: bool) -> None:
+    native.call("skm_assign_stats", ptr(ws.tau), ptr(ws.assign), ptr(ws.prev) if with_prev else None, n,
+                ptr(ws.wcss), ptr(ws.changed), ptr(ws.stats_ws), ws.stats_ws.numel(), stream_handle())
+
+
+# ------------------------------------------------------------------------------ the loop
+def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: Comm | None = None,
+                       n_global: int | None = None, row_lo: int = 0, init_rows: torch.Tensor | None = None,
+                       init_idx: np.ndarray | None = None, etr=None, timer: _Timer | None = None) -> LoopOutput:
+    """Device twin of core._fit_rotated.  ``data`` holds this rank's rows; ``n_global`` the
+    total across ranks.  ``init_rows`` (k, ld) are the Forgy rows gathered from all ranks."""
+    comm = comm or Comm()
+    dev = data.x.device
+    n_local, d = data.n, data.d
+    n = n_local if n_global is None else n_global
+    k = cfg.k
+    work = WorkCounters()
+    timer = timer or _Timer()
+    if init_idx is None:
+        init_idx = init_indices(n, k, [cfg.seed, 2])
+    if init_rows is None:
+        idx = torch.tensor(init_idx, dtype=torch.int64, device=dev)
+        init_rows = torch.zeros((k, data.ld), dtype=torch.float32, device=dev)
+        native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(idx), k, data.ld, ptr(init_rows), data.ld,
+                    stream_handle())
+    cents = Centroids(init_rows, d)
+    ws = Workspace(dev, n_local, k, d, cfg)
+    rng_split = np.random.default_rng([cfg.seed, 3])
+    pruned_mode = pruning_supported(d)
+    d_prime = initial_d_prime(d, cfg.d_prime_init_fraction) if pruned_mode else None
+    stats: list[IterationStats] = []
+    recall_history: list[float] = []
+    terminated = "max_iters"
+    phase: dict[str, float] = {}
+    if etr is not None:
+        timer.start("ground_truth")
+        etr.setup(data, comm)
+        timer.stop("ground_truth")
+    sums_buf = None
+    if comm.world > 1:
+        sums_buf = torch.empty(k * d + k, dtype=torch.float64, device=dev)
+    scal = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    for it in range(1, cfg.max_iters + 1):
+        pruned_iter = pruned_mode and it > 1
+        d_used = d_prime if pruned_iter else None
+        survivors = touched = 0
+        prune_rate = None
+        n_changed = None
+        if it > 1:
+            native.call("skm_copy_i32", ptr(ws.assign), ptr(ws.prev), n_local, stream_handle())
+        if not pruned_iter:
+            timer.start("gemm")
+            cents.refresh(d, None)
+            full_assign_pass(data, cents, ws)
+            timer.stop("gemm")
+            work.full_pair_dims += n * k * d
+        else:
+            plan = PrunePlan(d, d_prime, cfg.epsilon0, cfg.pruning_sentinel, dev)
+            timer.start("pruning")
+            cents.refresh(d_prime, d_prime)
+            ws.counters.zero_()
+            pruned_assign_pass(data, cents, ws, plan)
+            timer.stop("pruning")
+            work.front_pair_dims += n * k * d_prime
+            if not cfg.pruning_sentinel:
+                work.seed_dims += n * d
+        assign_stats(ws, n_local, it > 1)
+        # ---- one reduction of the iteration's scalars (packed) ----
+        scal[0] = ws.wcss[0]
+        scal[1] = ws.changed[0].to(torch.float64)
+        scal[2] = ws.counters[0].to(torch.float64)
+        scal[3] = ws.counters[1].to(torch.float64)
+        comm.allreduce_(scal)
+        wcss, ch, sv, td = scal.tolist()
+        if it > 1:
+            n_changed = int(round(ch))
+        if pruned_iter:
+            survivors, touched = int(round(sv)), int(round(td))
+            prune_rate = prune_rate_from_totals(survivors, n, k)
+            work.tail_dims += touched
+        if inspect is not None:
+            inspect(it, {
+                "assignments": ws.assign[:n_local].cpu().numpy().copy(),
+                "best_sq_dist": ws.tau[:n_local].cpu().numpy().copy(),
+                "centroids_rotated": cents.c[:, :d].cpu().numpy().copy(),
+                "d_prime": d_used,
+                "prune_rate": prune_rate,
+            })
+        if n_changed == 0:
+            stats.append(IterationStats(iter_index=it, wcss=wcss, n_empty_splits=0, prune_rate_after_gemm=prune_rate,
+                                        d_prime=d_used, survivors=survivors, tail_dims_touched=touched,
+                                        n_changed=n_changed, timings=timer.collect()))
+            terminated = "converged"
+            break
+        timer.start("update")
+        counts = update_centroids_device(data, cents, ws, comm, sums_buf)
+        n_splits = apply_splits_device(cents, counts, rng_split) if cfg.split_empty else 0
+        timer.stop("update")
+        if pruned_iter:
+            d_prime = adjust_d_prime(d_prime, prune_rate, cfg, d)
+        recall = None
+        if etr is not None:
+            timer.start("etr")
+            recall = etr.probe(data, cents, ws, comm)
+            timer.stop("etr")
+            recall_history.append(recall)
+        stats.append(IterationStats(iter_index=it, wcss=wcss, n_empty_splits=n_splits,
+                                    prune_rate_after_gemm=prune_rate, recall=recall, d_prime=d_used,
+                                    survivors=survivors, tail_dims_touched=touched, n_changed=n_changed,
+                                    timings=timer.collect()))
+        if etr is not None and etr.should_stop(recall_history):
+            terminated = "etr"
+            break
+
+    gt_time = 0.0
+    for s in stats:
+        gt_time += s.timings.pop("ground_truth", 0.0)
+    if etr is not None:
+        phase["ground_truth"] = gt_time
+    for key in ("gemm", "pruning", "update", "etr"):
+        phase[key] = sum(s.timings.get(key, 0.0) for s in stats)
+    return LoopOutput(
+        centroids_rotated=cents.c[:, :d].cpu().numpy().copy(),
+        assignments=ws.assign[:n_local].cpu().numpy().copy(),
+        best_sq_dist=ws.tau[:n_local].cpu().numpy().copy(),
+        stats=stats,
+        terminated_by=terminated,
+        d_prime_final=d_prime,
+        init_indices=np.asarray(init_idx),
+        work=work,
+        recall_history=recall_history,
+        phase_seconds=phase,
+        centroids_dev=cents.c,
+        assign_dev=ws.assign[:n_local],
+    )

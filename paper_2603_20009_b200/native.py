@@ -121,5 +121,15 @@ def check(rc: int, what: str) -> None:
         raise NativeError(f"{what} failed ({rc}): {msg}")
 
 
-def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+def call(name: str, *args, flops: float = 0.0, nbytes: float = 0.0, tag: str | None = None) -> None:
+    """Invoke an ABI entry point; raise NativeError on failure.  When a profiling.KernelTimer
+    is active the launch is bracketed by CUDA events and its algorithmic work recorded."""
+    from . import profiling
+    prof = profiling.current()
+    fn = getattr(load(), name)
+    if prof is None:
+        check(fn(*args), name)
+        return
+    e0 = prof.begin()
+    check(fn(*args), name)
+    prof.end(tag or name, e0, flops, nbytes)

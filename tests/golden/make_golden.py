@@ -1,0 +1,166 @@
+"""Generate the golden fixtures in tests/golden/ by running the REAL reference package.
+
+Run here (the container that has /root/reference):
+    PYTHONPATH=/root/reference/pkg/src SUPERKMEANS_KERNELS=python python tests/golden/make_golden.py
+
+The reference is imported read-only; nothing under /root/reference is copied.  The fixtures
+pin (a) the bit-exact kernel protocol outputs (scan/seed/accumulate/portable matmul) for
+fixed inputs, (b) whole-fit trajectories (assignments, centroids, d', survivors, wcss,
+prune rates, ETR recall, hierarchical plans) on seeded synthetic data, and (c) host math
+(rotation, factors, cutoff controller).  GPU runs compare against these with the
+north-star tolerances; CPU tests pin oracle/ against them bitwise where bits are
+CPU-independent.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))  # tests/ for conftest generators
+from conftest import make_blobs, make_skewed_blobs  # noqa: E402
+
+import superkmeans as skm  # noqa: E402  (the reference, from PYTHONPATH)
+from superkmeans import _kernels_py as RK  # noqa: E402
+from superkmeans.distance import expand_to_sq_l2, matmul  # noqa: E402
+from superkmeans.model import pdxify, tail_block_layout  # noqa: E402
+from superkmeans.preprocess import compute_norms  # noqa: E402
+from superkmeans.pruning import threshold_factors  # noqa: E402
+
+
+def kernels():
+    out = {}
+    for seed in range(3):
+        rng = np.random.default_rng(seed)
+        n, k, d, dp = 123, 77, 200, 25
+        x = rng.standard_normal((n, d)).astype(np.float32)
+        c = rng.standard_normal((k, d)).astype(np.float32)
+        prev = rng.integers(0, k, n).astype(np.int32)
+        bank = pdxify(c, dp)
+        vals = expand_to_sq_l2(matmul(x, c, dp), compute_norms(x, dp), compute_norms(c, dp), partial=True).values
+        dims, bounds = tail_block_layout(d, dp)
+        f = threshold_factors(d, dp, bounds, 2.1)
+        for sentinel in (False, True):
+            tau = np.empty(n, np.float32)
+            RK.seed_thresholds(x, c, prev, tau, 1)
+            seed_tau = tau.copy()
+            if sentinel:
+                tau[:] = np.inf
+            a = prev.copy()
+            sv, td = RK.scan_bank(vals, x, bank.tail, bank.block_offsets, bank.block_dims, f, dp, 0, tau, a,
+                                  sentinel, 1)
+            key = f"scan_s{seed}_{int(sentinel)}"
+            out[key + "_x"] = x
+            out[key + "_c"] = c
+            out[key + "_prev"] = prev
+            out[key + "_vals"] = vals
+            out[key + "_f"] = f
+            out[key + "_seedtau"] = seed_tau
+            out[key + "_tau"] = tau
+            out[key + "_assign"] = a
+            out[key + "_counts"] = np.array([sv, td], np.int64)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((500, 64)).astype(np.float32)
+    a = rng.integers(0, 12, 500).astype(np.int32)
+    sums = np.zeros((12, 64))
+    counts = np.zeros(12, np.int64)
+    RK.accumulate_centroid_sums(x, a, sums, counts)
+    out.update(acc_x=x, acc_a=a, acc_sums=sums, acc_counts=counts)
+    return out
+
+
+def fit_case(name, x, cfg, out):
+    snaps = []
+    res = skm.fit(x, cfg, inspect=lambda it, ctx: snaps.append(ctx))
+    out[f"{name}_centroids"] = res.centroids
+    out[f"{name}_centroids_rot"] = res.centroids_rotated
+    out[f"{name}_assign"] = res.assignments
+    out[f"{name}_init"] = res.init_indices
+    out[f"{name}_term"] = np.array(res.terminated_by)
+    out[f"{name}_dpf"] = np.array(-1 if res.d_prime_final is None else res.d_prime_final)
+    st = res.stats
+    out[f"{name}_wcss"] = np.array([s.wcss for s in st])
+    out[f"{name}_surv"] = np.array([s.survivors for s in st], np.int64)
+    out[f"{name}_tail"] = np.array([s.tail_dims_touched for s in st], np.int64)
+    out[f"{name}_dp"] = np.array([-1 if s.d_prime is None else s.d_prime for s in st], np.int64)
+    out[f"{name}_rate"] = np.array([np.nan if s.prune_rate_after_gemm is None else s.prune_rate_after_gemm for s in st])
+    out[f"{name}_changed"] = np.array([-1 if s.n_changed is None else s.n_changed for s in st], np.int64)
+    out[f"{name}_splits"] = np.array([s.n_empty_splits for s in st], np.int64)
+    out[f"{name}_recall"] = np.array(res.recall_history)
+    out[f"{name}_snap_assign"] = np.stack([s["assignments"] for s in snaps])
+    out[f"{name}_snap_cent"] = np.stack([s["centroids_rotated"] for s in snaps])
+    out[f"{name}_rotation"] = res.rotation.data
+    if res.sample_indices is not None:
+        out[f"{name}_sidx"] = res.sample_indices
+    fa = skm.final_assign(x, res, cfg)
+    out[f"{name}_final"] = fa
+    return res
+
+
+FIT_CASES = {
+    # name: (generator args, config kwargs)
+    "blobs": (("blobs", 3000, 128, 32, 4), dict(k=24, max_iters=6, seed=5)),
+    "sentinel": (("blobs", 2000, 96, 16, 6), dict(k=12, max_iters=5, seed=7, pruning_sentinel=True)),
+    "smalld": (("blobs", 1500, 48, 8, 3), dict(k=8, max_iters=6, seed=1)),
+    "skewed": (("skewed", 6000, 256, 128, 11), dict(k=64, max_iters=6, seed=5)),
+    "ragged": (("blobs", 2500, 200, 20, 9), dict(k=30, max_iters=6, seed=2)),
+    "sampled": (("blobs", 3000, 128, 24, 12), dict(k=16, max_iters=5, seed=3, sampling_fraction=0.5)),
+    "etr": (("blobs", 4000, 128, 60, 21), dict(k=40, max_iters=12, seed=1)),
+    "split": (("blobs", 1200, 96, 4, 13), dict(k=40, max_iters=5, seed=0)),
+}
+
+
+def make_x(spec):
+    kind, n, d, centers, seed = spec
+    if kind == "blobs":
+        return make_blobs(n, d, centers, seed=seed)
+    return make_skewed_blobs(n, d, centers, seed=seed)
+
+
+def fits():
+    out = {}
+    for name, (spec, kw) in FIT_CASES.items():
+        x = make_x(spec)
+        if name == "etr":
+            kw = dict(kw, etr=skm.EtrConfig(n_queries=300, top_k=10))
+        fit_case(name, x, skm.KMeansConfig(**kw), out)
+    # hierarchical
+    x = make_blobs(6000, 128, 50, seed=31, spread=5.0, noise=0.8)
+    h = skm.hierarchical_fit(x, skm.HierarchicalConfig(k_total=120, seed=2))
+    out["hier_centroids"] = h.centroids
+    out["hier_assign"] = h.assignments
+    out["hier_k"] = np.array(h.k)
+    out["hier_meso_assign_snap"] = np.array(0)
+    return out
+
+
+def hostmath():
+    out = {}
+    for d, s in ((64, 3), (200, 0), (96, 7)):
+        out[f"rot_{d}_{s}"] = skm.generate_rotation(d, s).data
+    from superkmeans.core import adjust_d_prime
+    cfg = skm.KMeansConfig(k=4)
+    cases = [(192, 0.96, 1536), (192, 0.99, 1536), (96, 0.90, 1536), (18, 0.999, 1536), (1400, 0.5, 1536),
+             (25, 0.90, 200), (24, 0.98, 128), (32, 0.9476, 128), (24, 0.9713, 128)]
+    out["adjust_in"] = np.array([[a, r, d] for a, r, d in cases])
+    out["adjust_out"] = np.array([adjust_d_prime(a, r, cfg, d) for a, r, d in cases])
+    dims, bounds = tail_block_layout(1536, 192)
+    out["factors_1536_192"] = threshold_factors(1536, 192, bounds, 2.1)
+    dims, bounds = tail_block_layout(200, 25)
+    out["factors_200_25"] = threshold_factors(200, 25, bounds, 2.1)
+    return out
+
+
+def main():
+    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels())
+    np.savez_compressed(os.path.join(HERE, "hostmath.npz"), **hostmath())
+    np.savez_compressed(os.path.join(HERE, "fits.npz"), **fits())
+    for f in ("kernels.npz", "hostmath.npz", "fits.npz"):
+        print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()
