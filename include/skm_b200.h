@@ -48,6 +48,8 @@ int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* o
 /* out[r,:cols] = in[idx[r],:cols] */
 int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
                     long long ldo, void* stream);
+int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
+                        long long ldo, void* stream);
 int skm_fill_f32(float* p, long long n, float v, void* stream);
 int skm_copy_i32(const int* src, int* dst, int n, void* stream);
 
@@ -114,13 +116,17 @@ typedef struct skm_scan_params {
   const int* cand_idx; const float* cand_val; const int* cand_cnt; int cap;  /* list mode */
   const float* dense; long long ld_dense; const int* dense_row; int k;       /* dense mode */
   const int* rows; int n_rows; long long row0;  /* batch-local rows to scan (NULL = 0..n_rows-1) */
+  const int* row_map;                          /* optional global row of each batch-local row */
+  void* work;                                  /* device u32[SKM_SCAN_MAX_QUEUES] scratch: per-SM row queues */
   const float* x; long long ldx;
   const float* tails; int nb; int d_prime;
   const float* theta; const int* block_dims;   /* nb+1 factors, nb block widths */
   float* tau; int* assign;                     /* global rows (row0 + local) */
   unsigned long long* counters;                /* += {survivors, dims touched, changed} */
   int dense_mode;
+  unsigned long long* counters_ext;            /* optional diagnostics: += {block sums computed} */
 } skm_scan_params;
+#define SKM_SCAN_MAX_QUEUES 256
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
 
 #ifdef __cplusplus

@@ -57,10 +57,22 @@ __global__ void gather_rows_kernel(const float* __restrict__ in, long long ldi, 
   }
 }
 
+__global__ void gather_rows_i32_kernel(const float* __restrict__ in, long long ldi, const int* __restrict__ idx,
+                                       int rows, int cols, float* __restrict__ out, long long ldo) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols;
+    const int c = static_cast<int>(e - r * cols);
+    out[r * ldo + c] = in[static_cast<long long>(idx[r]) * ldi + c];
+  }
+}
+
 // tau_i = sum_t (x_it - c_{a_i,t})^2, ascending t, separate mul/add (_kernels.pyx:85-103).
-// One thread per row; 32-column chunks staged through padded shared memory so the
-// global reads stay coalesced while each thread runs its own sequential chain.
+// One thread per row runs its own sequential chain; 32-column chunks of the CTA's 128 rows
+// (and of their assigned centroid rows) are loaded coalesced into registers one chunk ahead
+// (software pipelining), parked in padded shared memory, then consumed row-wise.
 constexpr int SEED_ROWS = 128;
+constexpr int SEED_PER = 32;  // elements per thread per chunk (128 rows x 32 cols / 128 threads)
 __global__ void __launch_bounds__(SEED_ROWS)
     seed_thresholds_kernel(const float* __restrict__ x, long long ldx, const float* __restrict__ cent, long long ldc,
                            const int* __restrict__ assign, int n, int d, float* __restrict__ out) {
@@ -69,28 +81,39 @@ __global__ void __launch_bounds__(SEED_ROWS)
   __shared__ int sa[SEED_ROWS];
   const int r0 = blockIdx.x * SEED_ROWS;
   const int tid = threadIdx.x;
-  if (r0 + tid < n) sa[tid] = assign[r0 + tid];
+  sa[tid] = (r0 + tid < n) ? assign[r0 + tid] : 0;
   __syncthreads();
+  // thread tid loads column (tid & 31) of rows (tid >> 5) + 4*m, m < 32
+  const int lc = tid & 31, lr = tid >> 5;
+  float px[SEED_PER], pc[SEED_PER];
+  auto load_chunk = [&](int t0) {
+    const int col = t0 + lc;
+#pragma unroll
+    for (int m = 0; m < SEED_PER; ++m) {
+      const int r = lr + 4 * m;
+      const int row = r0 + r;
+      const bool ok = row < n && col < d;
+      px[m] = ok ? __ldg(x + static_cast<long long>(row) * ldx + col) : 0.0f;
+      pc[m] = ok ? __ldg(cent + static_cast<long long>(sa[r]) * ldc + col) : 0.0f;
+    }
+  };
   float acc = 0.0f;
+  load_chunk(0);
   for (int t0 = 0; t0 < d; t0 += 32) {
-    for (int e = tid; e < SEED_ROWS * 32; e += SEED_ROWS) {
-      const int r = e >> 5, tt = e & 31;
-      const int row = r0 + r, col = t0 + tt;
-      float xv = 0.0f, cv = 0.0f;
-      if (row < n && col < d) {
-        xv = x[static_cast<long long>(row) * ldx + col];
-        cv = cent[static_cast<long long>(sa[r]) * ldc + col];
-      }
-      xs[r][tt] = xv;
-      cs[r][tt] = cv;
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < SEED_PER; ++m) {
+      xs[lr + 4 * m][lc] = px[m];
+      cs[lr + 4 * m][lc] = pc[m];
     }
     __syncthreads();
+    if (t0 + 32 < d) load_chunk(t0 + 32);  // next chunk in flight while this one is consumed
     const int lim = min(32, d - t0);
+#pragma unroll 8
     for (int tt = 0; tt < lim; ++tt) {
       const float diff = __fsub_rn(xs[tid][tt], cs[tid][tt]);
       acc = __fadd_rn(acc, __fmul_rn(diff, diff));
     }
-    __syncthreads();
   }
   if (r0 + tid < n) out[r0 + tid] = acc;
 }

@@ -12,7 +12,10 @@
 //    seed tau, and tau never increases) or, for overflow rows, from a dense distance row;
 //  * block sums are independent of tau, so 32 lanes compute them speculatively as
 //    8 candidate slots x 4 consecutive blocks per wave, recording every block sum;
-//  * a warp-parallel in-order resolver replays the exact sequential semantics from the
+//  * slot leaders decide each candidate's exact outcome incrementally, tagged with a tau
+//    version; a warp-parallel in-order resolver consumes decided outcomes in O(1) and
+//    re-walks (from the recorded sums) only those decided before tau last tightened.
+//    This replays the exact sequential semantics from the
 //    recorded sums: a speculative evaluation always ran under a tau >= the exact one,
 //    so it computed at least the blocks the exact walk needs (the exact walk prunes no
 //    later).  Survivor / dims-touched counters therefore match the reference bitwise.
@@ -25,11 +28,20 @@
 
 namespace skm {
 
-constexpr int SCAN_SLOTS = 8;
-constexpr int SCAN_DEPTH = 4;
-constexpr int SCAN_WINDOW = 64;   // in-flight queue positions per warp
-constexpr int SCAN_NB_MAX = 40;   // tail blocks supported (d - d' <= 2560)
-constexpr int SCAN_WARPS = 4;     // warps per CTA
+#ifndef SKM_SCAN_DEPTH
+#define SKM_SCAN_DEPTH 4
+#endif
+#ifndef SKM_SCAN_WARPS
+#define SKM_SCAN_WARPS 4
+#endif
+#ifndef SKM_SCAN_WINDOW
+#define SKM_SCAN_WINDOW 48
+#endif
+constexpr int SCAN_DEPTH = SKM_SCAN_DEPTH;     // consecutive blocks per candidate per wave
+constexpr int SCAN_SLOTS = 32 / SCAN_DEPTH;    // candidates in flight per wave
+constexpr int SCAN_WINDOW = SKM_SCAN_WINDOW;   // in-flight queue positions per warp
+constexpr int SCAN_NB_MAX = 40;                // tail blocks supported (d - d' <= 2560)
+constexpr int SCAN_WARPS = SKM_SCAN_WARPS;     // warps per CTA
 
 struct ScanArgs {
   // candidate source (list mode)
@@ -45,7 +57,10 @@ struct ScanArgs {
   // rows to process: rows[r] (batch-local index) for r < n_rows; nullptr = identity
   const int* rows;
   int n_rows;
-  long long row0;  // global row of batch-local row 0
+  long long row0;  // global row of batch-local row 0 (when row_map == nullptr)
+  const int* row_map;      // optional: global row of batch-local row (cluster-ordered batches)
+  unsigned int* work;      // per-SM row-queue counters [n_queues] (zeroed by the launcher)
+  int n_queues;
   const float* x;
   long long ldx;
   const float4* tails;  // [k][16][nb] float4
@@ -56,6 +71,7 @@ struct ScanArgs {
   float* tau;              // global rows, in/out
   int* assign;             // global rows, in/out
   unsigned long long* counters;  // [0] survivors, [1] dims touched, [2] changed
+  unsigned long long* counters_ext;  // optional diagnostics: [0] 64-dim block sums computed
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -83,19 +99,66 @@ __global__ void gate_threshold_kernel(const float* __restrict__ tau, int n, floa
 }
 
 struct ScanWarpSmem {
-  // sized at launch: xsm[64*nb] floats, rec[WINDOW*nb] floats
+  // per queue position (ring of SCAN_WINDOW)
   int qj[SCAN_WINDOW];
   float qp[SCAN_WINDOW];
-  int qdone[SCAN_WINDOW];
+  int qdone[SCAN_WINDOW];   // block sums recorded so far
+  int qstat[SCAN_WINDOW];   // 0 pending, 1 not a survivor, 2 pruned (at qpb), 3 complete (qrun)
+  int qpb[SCAN_WINDOW];
+  float qrun[SCAN_WINDOW];
+  int qver[SCAN_WINDOW];    // tau version the outcome was decided under
 };
 
+// (a - b)^2 for two lanes with sm_100 packed fp32 ops: sub.rn.f32x2 / mul.rn.f32x2.
+__device__ __forceinline__ float2 sq_diff2(float2 a, float2 b) {
+  unsigned long long ua, ub, d, q;
+  ua = (static_cast<unsigned long long>(__float_as_uint(a.y)) << 32) | __float_as_uint(a.x);
+  ub = (static_cast<unsigned long long>(__float_as_uint(b.y)) << 32) | __float_as_uint(b.x);
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(q) : "l"(d));
+  return make_float2(__uint_as_float(static_cast<unsigned>(q)), __uint_as_float(static_cast<unsigned>(q >> 32)));
+}
+
+enum : int { ST_PENDING = 0, ST_NOTSURV = 1, ST_PRUNED = 2, ST_COMPLETE = 3 };
+
+// Exact walk of one recorded candidate under threshold tcur (blocks < nd are available).
+// Returns the status; ST_PENDING if it needs a block that has not been computed yet.
+__device__ __forceinline__ int walk_exact(float p, const float* rec_row, int nd, int nb, float tcur, float f0,
+                                          const float* theta, int& pb, float& run) {
+  if (p > __fmul_rn(tcur, f0)) return ST_NOTSURV;
+  run = p;
+  for (int b = 0; b < nb; ++b) {
+    if (b >= nd) return ST_PENDING;
+    run = __fadd_rn(run, rec_row[b]);
+    if (run > __fmul_rn(tcur, theta[b + 1])) {
+      pb = b;
+      return ST_PRUNED;
+    }
+  }
+  return ST_COMPLETE;
+}
+
+__device__ __forceinline__ int next_row(const ScanArgs& a, int& qs, int& lo, int& hi) {
+  for (int tries = 0; tries <= a.n_queues; ++tries) {
+    const int r = lo + static_cast<int>(atomicAdd(a.work + qs, 1u));
+    if (r < hi) return r;
+    qs = (qs + 1) % a.n_queues;
+    lo = static_cast<int>((static_cast<long long>(a.n_rows) * qs) / a.n_queues);
+    hi = static_cast<int>((static_cast<long long>(a.n_rows) * (qs + 1)) / a.n_queues);
+  }
+  return a.n_rows;
+}
+
+#ifndef SKM_SCAN_MINB
+#define SKM_SCAN_MINB 1
+#endif
 template <bool DENSE>
-__global__ void __launch_bounds__(SCAN_WARPS * 32)
+__global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     pruned_scan_kernel(const ScanArgs a) {
   extern __shared__ float scan_smem[];
   __shared__ ScanWarpSmem wsm[SCAN_WARPS];
   __shared__ float s_theta[SCAN_NB_MAX + 1];
-  __shared__ int s_bdcum[SCAN_NB_MAX + 1];  // dims touched through block b (exclusive prefix at b+1)
+  __shared__ int s_bdcum[SCAN_NB_MAX + 1];  // dims touched through block b (prefix at b+1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = a.nb;
@@ -119,10 +182,29 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32)
   const unsigned FULL = 0xffffffffu;
   const int slot = lane / SCAN_DEPTH, dep = lane % SCAN_DEPTH;
   const bool slot_leader = dep == 0;
+  const unsigned leader_mask = (SCAN_DEPTH == 4) ? 0x11111111u : (SCAN_DEPTH == 8) ? 0x01010101u
+                              : (SCAN_DEPTH == 2) ? 0x55555555u : 0xffffffffu;  // slot leader lanes
 
-  unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0;
+  unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0;
+  // per-SM row queue: SM s owns the contiguous (cluster-sorted) row range [s*n/nq, (s+1)*n/nq),
+  // so the warps sharing an SM's L1 scan rows of the same cluster (shared candidates);
+  // exhausted queues steal from the following ones.
+  int q_sm = 0, q_lo = 0, q_hi = 0;
+  if (lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    q_sm = static_cast<int>(smid % static_cast<unsigned>(a.n_queues));
+    q_lo = static_cast<int>((static_cast<long long>(a.n_rows) * q_sm) / a.n_queues);
+    q_hi = static_cast<int>((static_cast<long long>(a.n_rows) * (q_sm + 1)) / a.n_queues);
+  }
 
-  for (int r = blockIdx.x * SCAN_WARPS + warp; r < a.n_rows; r += gridDim.x * SCAN_WARPS) {
+  while (true) {
+    // rows are handed out in order from a global counter: warps running concurrently work on
+    // neighbouring (cluster-sorted) rows, so their candidate centroids' tails stay L2-hot
+    int r = 0;
+    if (lane == 0) r = next_row(a, q_sm, q_lo, q_hi);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= a.n_rows) break;
     const int rl = a.rows ? a.rows[r] : r;
     int n_src;
     if constexpr (DENSE) {
@@ -131,7 +213,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32)
       n_src = a.cand_cnt[rl];
       if (n_src > a.cap) continue;  // overflow row: handled by the dense pass
     }
-    const long long row = a.row0 + rl;
+    const long long row = a.row_map ? static_cast<long long>(a.row_map[rl]) : a.row0 + rl;
     // ---- stage the x tail, quad layout (q, b, r)
     const float* xrow = a.x + row * a.ldx + a.d_prime;
     for (int u = lane; u < 64 * nb; u += 32) {
@@ -141,12 +223,10 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32)
     float tcur = a.tau[row];
     int best = a.assign[row];
     const int best0 = best;
-    int src = 0;        // next source entry to read
-    int F = 0;          // queue fill pointer
-    int D = 0;          // dispatch pointer
-    int R = 0;          // resolve pointer
-    // slot state (meaningful in all lanes of the slot; kept identical via shuffles)
-    int spos = -1, snxt = 0;
+    int ver = 0;  // bumped whenever tau tightens
+    int src = 0, F = 0, D = 0, R = 0;
+    // slot state: all lanes of a slot hold spos/snxt; the leader also walks (srun, sb, sver)
+    int spos = -1, snxt = 0, sb = 0, sver = -1;
     float srun = 0.0f;
     const float* dense_row = nullptr;
     const int* lidx = nullptr;
@@ -178,128 +258,182 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32)
         }
         const unsigned m = __ballot_sync(FULL, ok);
         if (ok) {
-          const int qpos = (F + __popc(m & ((1u << lane) - 1u))) % SCAN_WINDOW;
-          W.qj[qpos] = j;
-          W.qp[qpos] = p;
-          W.qdone[qpos] = 0;
+          const int qs = (F + __popc(m & ((1u << lane) - 1u))) % SCAN_WINDOW;
+          W.qj[qs] = j;
+          W.qp[qs] = p;
+          W.qdone[qs] = 0;
+          W.qstat[qs] = ST_PENDING;
+          W.qver[qs] = -1;
         }
         F += __popc(m);
         src += 32;
       }
       __syncwarp();
       if (R == F && src >= n_src) break;  // everything resolved
-      // ---- 2. dispatch free slots in order
+      // ---- 2. dispatch: free slots take the next positions that still pass the gate under
+      //         the current tau; positions failing it are decided (not survivors) on the spot
       {
-        const unsigned freem = __ballot_sync(FULL, slot_leader && spos < 0);
-        // slot s takes the rank-th free position
-        if (spos < 0) {
-          const unsigned my_leader_bit = 1u << (slot * SCAN_DEPTH);
-          const int rank = __popc(freem & (my_leader_bit - 1u));
-          const int p = D + rank;
-          if (p < F && p < R + SCAN_WINDOW) {
-            spos = p;
+        const unsigned freem = __ballot_sync(FULL, slot_leader && spos < 0) & leader_mask;
+        int nfree = __popc(freem);
+        unsigned free_left = freem;
+        while (nfree > 0 && D < F && D < R + SCAN_WINDOW) {
+          const int lim = min(min(F, R + SCAN_WINDOW) - D, 32);
+          const int pp = D + lane;
+          bool pass = false;
+          if (lane < lim) pass = !(W.qp[pp % SCAN_WINDOW] > __fmul_rn(tcur, f0));
+          const unsigned pm = __ballot_sync(FULL, pass);
+          // the first nfree passing positions get slots; cut = positions consumed this round
+          int cut = lim;
+          if (__popc(pm) >= nfree) cut = static_cast<int>(__fns(pm, 0, nfree)) + 1;  // past the nfree-th pass
+          if (lane < cut && !pass) {
+            const int qs = pp % SCAN_WINDOW;
+            W.qstat[qs] = ST_NOTSURV;
+            W.qver[qs] = ver;
+          }
+          const unsigned took = pm & ((cut >= 32) ? FULL : ((1u << cut) - 1u));
+          // taken positions (ascending) go to the remaining free slots (ascending)
+          int newpos = -1;
+          if (slot_leader && ((free_left >> lane) & 1u)) {
+            const int my_rank = __popc(free_left & ((1u << lane) - 1u));
+            if (my_rank < __popc(took)) newpos = D + static_cast<int>(__fns(took, 0, my_rank + 1));
+          }
+          newpos = __shfl_sync(FULL, newpos, slot * SCAN_DEPTH);
+          const unsigned assigned = __ballot_sync(FULL, slot_leader && newpos >= 0);
+          if (newpos >= 0) {
+            spos = newpos;
             snxt = 0;
-            srun = W.qp[p % SCAN_WINDOW];
+            sb = 0;
+            sver = -1;
           }
-        }
-        const int nfree = __popc(freem);
-        D = min(min(D + nfree, F), R + SCAN_WINDOW);
-      }
-      // ---- 3. one wave of speculative block sums
-      if (spos >= 0) {
-        const int b = snxt + dep;
-        if (b < nb) {
-          const int qs = spos % SCAN_WINDOW;
-          const int j = W.qj[qs];
-          const float4* cb = a.tails + static_cast<long long>(j) * 16 * nb + b;
-          const float4* xb = xsm4 + b;
-          float acc = 0.0f;
-#pragma unroll 4
-          for (int q = 0; q < 16; ++q) {
-            const float4 c4 = __ldg(cb + q * nb);
-            const float4 x4 = xb[q * nb];
-            float df = __fsub_rn(x4.x, c4.x);
-            acc = __fadd_rn(acc, __fmul_rn(df, df));
-            df = __fsub_rn(x4.y, c4.y);
-            acc = __fadd_rn(acc, __fmul_rn(df, df));
-            df = __fsub_rn(x4.z, c4.z);
-            acc = __fadd_rn(acc, __fmul_rn(df, df));
-            df = __fsub_rn(x4.w, c4.w);
-            acc = __fadd_rn(acc, __fmul_rn(df, df));
-          }
-          rec[qs * nb + b] = acc;
+          free_left &= ~assigned;
+          nfree -= __popc(took);
+          D += cut;
+          __syncwarp();
         }
       }
-      __syncwarp();
-      // ---- 4. slot leaders extend the running sum, mark done / speculatively dead
-      {
-        int fin_local = 0;
-        if (spos >= 0 && slot_leader) {
-          const int qs = spos % SCAN_WINDOW;
-          const int hi = min(nb, snxt + SCAN_DEPTH);
-          for (int b = snxt; b < hi; ++b) {
-            srun = __fadd_rn(srun, rec[qs * nb + b]);
-            if (srun > __fmul_rn(tcur, s_theta[b + 1])) { fin_local = 1; break; }
-          }
-          W.qdone[qs] = hi;
-          if (hi >= nb) fin_local = 1;
-        }
-        const int finished = __shfl_sync(FULL, fin_local, slot * SCAN_DEPTH);
-        if (spos >= 0) {
-          snxt += SCAN_DEPTH;
-          if (finished) spos = -1;
-        }
+      // ---- 3. issue this wave's tail loads (16 x 16 B per lane); their latency is hidden
+      //         behind the in-order resolution of the previous waves' outcomes (step 4)
+      ++waves_acc;
+      const int myb = snxt + dep;
+      const bool active = spos >= 0 && myb < nb;
+      float4 c4[16];
+      int my_qs = 0;
+      if (active) {
+        my_qs = spos % SCAN_WINDOW;
+        const float4* cb = a.tails + static_cast<long long>(W.qj[my_qs]) * 16 * nb + myb;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) c4[q] = __ldg(cb + q * nb);
       }
-      __syncwarp();
-      // ---- 5. in-order resolution, 32 positions per round
+      // ---- 4. in-order resolution, 32 positions per round; outcomes already decided under
+      //         the current tau version are O(1), older ones are re-walked from the records
       while (R < D) {
         const int p = R + lane;
-        int outcome = 0;  // 0 none(beyond D), 1 not survivor, 2 pruned, 3 complete, 4 incomplete
+        int st = ST_NOTSURV;  // lanes beyond D: neutral
         float run = 0.0f;
         int pb = 0, j = 0;
         if (p < D) {
           const int qs = p % SCAN_WINDOW;
-          const float pv = W.qp[qs];
+          st = W.qstat[qs];
           j = W.qj[qs];
-          if (pv > __fmul_rn(tcur, f0)) {
-            outcome = 1;
-          } else {
-            const int nd = W.qdone[qs];
-            run = pv;
-            outcome = 3;
-            for (int b = 0; b < nb; ++b) {
-              if (b >= nd) { outcome = 4; break; }
-              run = __fadd_rn(run, rec[qs * nb + b]);
-              if (run > __fmul_rn(tcur, s_theta[b + 1])) { outcome = 2; pb = b; break; }
+          if (st != ST_PENDING) {
+            if (W.qver[qs] != ver) {
+              st = walk_exact(W.qp[qs], rec + qs * nb, W.qdone[qs], nb, tcur, f0, s_theta, pb, run);
+              if (st != ST_PENDING) {
+                W.qstat[qs] = st;
+                W.qpb[qs] = pb;
+                W.qrun[qs] = run;
+                W.qver[qs] = ver;
+              }
+            } else {
+              pb = W.qpb[qs];
+              run = W.qrun[qs];
             }
           }
         }
-        const bool improve = outcome == 3 && (run < tcur || (run == tcur && j < best));
-        const unsigned ev = __ballot_sync(FULL, improve || outcome == 4);
+        const bool improve = st == ST_COMPLETE && (run < tcur || (run == tcur && j < best));
+        const unsigned ev = __ballot_sync(FULL, p < D && (improve || st == ST_PENDING));
         const int limit = ev ? (__ffs(ev) - 1) : 32;  // lanes < limit are final
-        const bool counted = lane < limit || (lane == limit && improve);
-        unsigned long long s_add = 0, t_add = 0;
-        if (counted && (outcome == 2 || outcome == 3)) {
-          s_add = 1;
-          t_add = (outcome == 2) ? s_bdcum[pb + 1] : tail_dims;
+        const bool counted = p < D && (lane < limit || (lane == limit && improve));
+        if (counted && (st == ST_PRUNED || st == ST_COMPLETE)) {
+          surv_acc += 1;
+          touched_acc += (st == ST_PRUNED) ? s_bdcum[pb + 1] : tail_dims;
         }
-        surv_acc += s_add;
-        touched_acc += t_add;
         const int src_lane = ev ? limit : 0;
         const int ev_improve = __shfl_sync(FULL, (int)improve, src_lane);
         const float ev_run = __shfl_sync(FULL, run, src_lane);
         const int ev_j = __shfl_sync(FULL, j, src_lane);
+        __syncwarp();
         if (!ev) {
           R += min(32, D - R);
         } else if (ev_improve) {
           tcur = ev_run;
           best = ev_j;
+          ++ver;
           R += limit + 1;
         } else {
           R += limit;
           break;  // stalled on a candidate whose blocks are still being computed
         }
       }
+      // ---- 5. the wave's speculative block sums: sequential fp32 chain per (candidate, block)
+      float acc = 0.0f;
+      if (active) {
+        const float4* xb = xsm4 + myb;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float4 x4 = xb[q * nb];
+          // squares of 4 dims with packed FADD2/FMUL2 (per-lane IEEE RN, identical bits),
+          // then the sequential fp32 chain in ascending dimension order
+          const float2 s01 = sq_diff2(make_float2(x4.x, x4.y), make_float2(c4[q].x, c4[q].y));
+          const float2 s23 = sq_diff2(make_float2(x4.z, x4.w), make_float2(c4[q].z, c4[q].w));
+          acc = __fadd_rn(acc, s01.x);
+          acc = __fadd_rn(acc, s01.y);
+          acc = __fadd_rn(acc, s23.x);
+          acc = __fadd_rn(acc, s23.y);
+        }
+        rec[my_qs * nb + myb] = acc;
+        ++blocks_acc;
+      }
+      // ---- 6. slot leaders walk their candidate exactly under the current tau version; the
+      //         wave's 4 block sums come from the slot lanes by shuffle
+      {
+        float blk[SCAN_DEPTH];
+#pragma unroll
+        for (int i = 0; i < SCAN_DEPTH; ++i) blk[i] = __shfl_sync(FULL, acc, slot * SCAN_DEPTH + i);
+        int fin = 0;
+        if (spos >= 0 && slot_leader) {
+          const int qs = spos % SCAN_WINDOW;
+          const int hi = min(nb, snxt + SCAN_DEPTH);
+          W.qdone[qs] = hi;
+          if (sver != ver) {  // tau tightened since this walk started: restart from the records
+            sver = ver;
+            sb = 0;
+            srun = W.qp[qs];
+            if (srun > __fmul_rn(tcur, f0)) fin = ST_NOTSURV;
+          }
+          while (!fin && sb < hi) {
+            const float v = (sb >= snxt) ? blk[(sb - snxt) & (SCAN_DEPTH - 1)] : rec[qs * nb + sb];
+            srun = __fadd_rn(srun, v);
+            if (srun > __fmul_rn(tcur, s_theta[sb + 1])) {
+              fin = ST_PRUNED;
+              W.qpb[qs] = sb;
+            }
+            ++sb;
+          }
+          if (!fin && sb >= nb) fin = ST_COMPLETE;
+          if (fin) {
+            W.qrun[qs] = srun;
+            W.qver[qs] = ver;
+            W.qstat[qs] = fin;
+          }
+        }
+        fin = __shfl_sync(FULL, fin, slot * SCAN_DEPTH);
+        if (spos >= 0) {
+          snxt += SCAN_DEPTH;
+          if (fin) spos = -1;
+        }
+      }
+      __syncwarp();
       // slots whose candidate got resolved are released
       if (spos >= 0 && spos < R) spos = -1;
       __syncwarp();
@@ -314,6 +448,10 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32)
   warp_add_u64(surv_acc, &a.counters[0]);
   warp_add_u64(touched_acc, &a.counters[1]);
   warp_add_u64(changed_acc, &a.counters[2]);
+  if (a.counters_ext) {
+    warp_add_u64(blocks_acc, &a.counters_ext[0]);  // speculative block sums computed
+    if (lane == 0 && waves_acc) atomicAdd(&a.counters_ext[1], waves_acc);  // warp waves executed
+  }
 }
 
 inline size_t scan_dyn_smem(int nb) { return static_cast<size_t>(SCAN_WARPS) * (64 * nb + SCAN_WINDOW * nb) * 4; }

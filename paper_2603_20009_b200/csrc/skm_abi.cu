@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -152,6 +153,15 @@ int skm_gather_rows(const float* in, long long ldi, const long long* idx, int ro
   skm::gather_rows_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
                                                                                               cols, out, ldo);
   SKM_LAUNCH_CHECK("gather_rows");
+  return SKM_OK;
+}
+
+int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
+                        long long ldo, void* stream) {
+  if (rows <= 0) return SKM_OK;
+  skm::gather_rows_i32_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
+                                                                                                  cols, out, ldo);
+  SKM_LAUNCH_CHECK("gather_rows_i32");
   return SKM_OK;
 }
 
@@ -390,6 +400,19 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.rows = p->rows;
   a.n_rows = p->n_rows;
   a.row0 = p->row0;
+  a.row_map = p->row_map;
+  a.work = reinterpret_cast<unsigned int*>(p->work);
+  if (!a.work) return fail(SKM_E_ARG, "pruned_scan: work counter required");
+  {
+    int dev0 = 0, nsm = 148;
+    cudaGetDevice(&dev0);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev0);
+    // one global queue measured fastest (per-SM queues: 3x slower); SKM_SCAN_QUEUES overrides
+    const char* qv = getenv("SKM_SCAN_QUEUES");
+    a.n_queues = std::max(1, std::min(qv ? atoi(qv) : 1, std::min(nsm, SKM_SCAN_MAX_QUEUES)));
+    cudaError_t e = cudaMemsetAsync(p->work, 0, sizeof(unsigned int) * a.n_queues, as_stream(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "pruned_scan work reset");
+  }
   a.x = p->x;
   a.ldx = p->ldx;
   a.tails = reinterpret_cast<const float4*>(p->tails);
@@ -400,8 +423,16 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.tau = p->tau;
   a.assign = p->assign;
   a.counters = p->counters;
+  a.counters_ext = p->counters_ext;
   const size_t smem = skm::scan_dyn_smem(p->nb);
-  const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, 148 * 16));
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (p->dense_mode)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skm::pruned_scan_kernel<true>, skm::SCAN_WARPS * 32, smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skm::pruned_scan_kernel<false>, skm::SCAN_WARPS * 32, smem);
+  const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms * std::max(per_sm, 1)));
   cudaStream_t st = as_stream(stream);
   if (p->dense_mode) {
     static bool set = false;
@@ -409,7 +440,12 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
     skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   } else {
     static bool set = false;
-    if (!set) { cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); set = true; }
+    if (!set) {
+      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      const char* cv = getenv("SKM_SCAN_CARVEOUT");
+      if (cv) cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+      set = true;
+    }
     skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   }
   SKM_LAUNCH_CHECK("pruned_scan");

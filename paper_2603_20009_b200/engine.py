@@ -95,6 +95,8 @@ class LoopOutput:
     centroids_dev: torch.Tensor | None = None
     assign_dev: torch.Tensor | None = None
     device_ms: dict = field(default_factory=dict)
+    scan_blocks: list = field(default_factory=list)  # speculative 64-dim block sums computed per pruned iter
+    scan_waves: list = field(default_factory=list)   # warp-waves of the scan per pruned iter
 
 
 class _Timer:
@@ -210,9 +212,10 @@ def _n_split(m_rows: int, n_cols: int, sms: int = 148) -> int:
 class Workspace:
     def __init__(self, dev, n: int, k: int, d: int, cfg: KMeansConfig):
         self.dev = dev
-        b = max(1, min(n, cfg.x_batch_device))
+        self.cap = min(cfg.cand_cap, (k + 31) // 32 * 32)
+        # candidate slab bounded to ~2 GiB (8 B per candidate)
+        b = max(128, min(max(n, 1), cfg.x_batch_device, (2 << 30) // (8 * self.cap)))
         self.batch = b
-        self.cap = cfg.cand_cap
         i32, f32 = torch.int32, torch.float32
         nn = max(n, 1)
         self.assign = torch.zeros(nn, dtype=i32, device=dev)
@@ -224,6 +227,11 @@ class Workspace:
         self.cand_val = torch.empty((b, self.cap), dtype=f32, device=dev)
         self.cand_cnt = torch.empty(b, dtype=i32, device=dev)
         self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.work = torch.zeros(256, dtype=torch.int32, device=dev)  # per-SM scan row queues
+        self.diag = torch.zeros(4, dtype=torch.int64, device=dev)  # scan diagnostics (blocks computed)
+        self.bx = torch.empty(b, dtype=f32, device=dev)
+        self.bthr = torch.empty(b, dtype=f32, device=dev)
+        self._front = None
         self.order = torch.empty(nn, dtype=i32, device=dev)
         self.counts = torch.empty(k, dtype=i32, device=dev)
         self.offsets = torch.empty(k, dtype=i32, device=dev)
@@ -232,6 +240,13 @@ class Workspace:
         self.stats_ws = torch.empty(int(lib.skm_stats_workspace_bytes(n)), dtype=torch.uint8, device=dev)
         self.wcss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.changed = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def front_buffers(self, fld: int):
+        """Gathered (hi, lo) front rows of one cluster-ordered batch."""
+        if self._front is None or self._front[0].shape[1] < fld:
+            self._front = (torch.empty((self.batch, fld), dtype=torch.float32, device=self.dev),
+                           torch.empty((self.batch, fld), dtype=torch.float32, device=self.dev))
+        return self._front[0][:, :fld], self._front[1][:, :fld]
 
     def argmin_keys(self, n):
         if self.keys is None or self.keys.numel() < n:
@@ -279,9 +294,14 @@ class PrunePlan:
 
 
 def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: PrunePlan, seed_tau: bool = True,
-                       row0: int = 0, rows: int | None = None):
+                       row0: int = 0, rows: int | None = None, order: torch.Tensor | None = None):
     """Seed tau, gate GEMM -> candidate lists, exact scan.  Accumulates ws.counters =
-    {survivors, tail dims touched, changed}."""
+    {survivors, tail dims touched, changed}.
+
+    With ``order`` (rows sorted by their previous assignment, from the last update) batches
+    follow that order: the gate GEMM reads gathered front rows, and concurrently running scan
+    warps then work on rows of the same/neighbouring clusters, whose candidate centroid tails
+    are shared in L1/L2.  Results do not depend on the order (rows are independent)."""
     n = data.n if rows is None else rows
     if n == 0:
         return
@@ -298,34 +318,58 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
                 ptr(ws.thr[row0:row0 + n]), st)
     xsq = data.norms(dp)
-    lib = native.load()
+    k = cents.k
+    ordered = order is not None and row0 == 0 and n == data.n
+    if ordered:
+        fld = padded_ld(dp)
+        ga_hi, ga_lo = ws.front_buffers(fld)
     for b0 in range(0, n, ws.batch):
         bn = min(ws.batch, n - b0)
         r = row0 + b0
-        _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, cents.k, dp, native.GEMM_GATE,
-              xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand_idx=ws.cand_idx, cand_val=ws.cand_val,
-              cand_cnt=ws.cand_cnt, cand_cap=ws.cap)
         sp = native.ScanParams()
+        if ordered:
+            rmap = order[b0:b0 + bn]
+            native.call("skm_gather_rows_i32", ptr(data.hi), data.ld, ptr(rmap), bn, dp, ptr(ga_hi), fld, st,
+                        nbytes=8.0 * bn * dp)
+            native.call("skm_gather_rows_i32", ptr(data.lo), data.ld, ptr(rmap), bn, dp, ptr(ga_lo), fld, st,
+                        nbytes=8.0 * bn * dp)
+            native.call("skm_gather_rows_i32", ptr(xsq.view(-1, 1)), 1, ptr(rmap), bn, 1, ptr(ws.bx.view(-1, 1)), 1,
+                        st)
+            native.call("skm_gather_rows_i32", ptr(ws.thr.view(-1, 1)), 1, ptr(rmap), bn, 1,
+                        ptr(ws.bthr.view(-1, 1)), 1, st)
+            _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
+                  ysq=cents.ysq, thr=ws.bthr[:bn], cand_idx=ws.cand_idx, cand_val=ws.cand_val, cand_cnt=ws.cand_cnt,
+                  cand_cap=ws.cap)
+            sp.row_map = rmap.data_ptr()
+        else:
+            _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE,
+                  xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand_idx=ws.cand_idx,
+                  cand_val=ws.cand_val, cand_cnt=ws.cand_cnt, cand_cap=ws.cap)
         sp.cand_idx, sp.cand_val, sp.cand_cnt, sp.cap = (ws.cand_idx.data_ptr(), ws.cand_val.data_ptr(),
                                                           ws.cand_cnt.data_ptr(), ws.cap)
-        sp.k, sp.n_rows, sp.row0 = cents.k, bn, r
+        sp.k, sp.n_rows, sp.row0 = k, bn, r
+        sp.work = ws.work.data_ptr()
         sp.x, sp.ldx = data.x.data_ptr(), data.ld
         sp.tails, sp.nb, sp.d_prime = cents.tails.data_ptr(), plan.nb, dp
         sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
         sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
-        native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan",
-                    nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
-        # rows whose candidate list overflowed the slab: dense distance rows, same kernel
-        over = torch.nonzero(ws.cand_cnt[:bn] > ws.cap).flatten()
-        n_over = int(over.numel())
-        if n_over:
-            _dense_overflow(data, cents, ws, plan, r, over.to(torch.int32), n_over, xsq)
+        sp.counters_ext = ws.diag.data_ptr()
+        native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        if ws.cap < k:
+            # rows whose candidate list overflowed the slab: dense distance rows, same kernel
+            over = torch.nonzero(ws.cand_cnt[:bn] > ws.cap).flatten()
+            n_over = int(over.numel())
+            if n_over:
+                gl = (order[b0:b0 + bn][over] if ordered else over + r).to(torch.int64)
+                _dense_overflow(data, cents, ws, plan, gl, n_over, xsq)
 
 
-def _dense_overflow(data, cents, ws, plan, r, over_local, n_over, xsq):
+def _dense_overflow(data, cents, ws, plan, glob_rows, n_over, xsq):
+    """Rows with more gate candidates than the slab holds: full partial-distance rows from the
+    same GEMM (bit-identical values), then the scan in dense mode."""
     dev = data.x.device
     st = stream_handle()
-    idx = (over_local.to(torch.int64) + r)
+    idx = glob_rows.to(torch.int64).contiguous()
     a_hi = torch.empty((n_over, data.ld), dtype=torch.float32, device=dev)
     a_lo = torch.empty_like(a_hi)
     xs = torch.empty(n_over, dtype=torch.float32, device=dev)
@@ -334,19 +378,18 @@ def _dense_overflow(data, cents, ws, plan, r, over_local, n_over, xsq):
     native.call("skm_gather_rows", ptr(xsq.view(-1, 1)), 1, ptr(idx), n_over, 1, ptr(xs.view(-1, 1)), 1, st)
     k = cents.k
     chunk = max(1, min(n_over, (1 << 28) // max(k, 1)))  # bound the dense buffer (1 GiB)
+    rmap_all = idx.to(torch.int32)
     for c0 in range(0, n_over, chunk):
         cn = min(chunk, n_over - c0)
         dense = torch.empty((cn, padded_ld(k)), dtype=torch.float32, device=dev)
         _gemm(a_hi[c0:c0 + cn], a_lo[c0:c0 + cn], cents.hi, cents.lo, cn, k, plan.d_prime, native.GEMM_DIST,
               out=dense, xsq=xs[c0:c0 + cn], ysq=cents.ysq, n_split=_n_split(cn, k))
-        dense_row = torch.arange(cn, dtype=torch.int32, device=dev)
-        rows_local = over_local[c0:c0 + cn].contiguous()
-        # the kernel indexes dense rows by batch-local row -> provide a scatter map
-        remap = torch.full((int(rows_local.max().item()) + 1,), -1, dtype=torch.int32, device=dev)
-        remap[rows_local.to(torch.int64)] = dense_row
+        ident = torch.arange(cn, dtype=torch.int32, device=dev)
         sp = native.ScanParams()
-        sp.dense, sp.ld_dense, sp.dense_row, sp.k = dense.data_ptr(), dense.stride(0), remap.data_ptr(), k
-        sp.rows, sp.n_rows, sp.row0 = rows_local.data_ptr(), cn, r
+        sp.dense, sp.ld_dense, sp.dense_row, sp.k = dense.data_ptr(), dense.stride(0), ident.data_ptr(), k
+        sp.n_rows, sp.row0 = cn, 0
+        sp.row_map = rmap_all[c0:c0 + cn].data_ptr()
+        sp.work = ws.work.data_ptr()
         sp.x, sp.ldx = data.x.data_ptr(), data.ld
         sp.tails, sp.nb, sp.d_prime = cents.tails.data_ptr(), plan.nb, plan.d_prime
         sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
@@ -433,6 +476,9 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
     if comm.world > 1:
         sums_buf = torch.empty(k * d + k, dtype=torch.float64, device=dev)
     scal = torch.zeros(4, dtype=torch.float64, device=dev)
+    have_order = False
+    scan_blocks: list[int] = []
+    scan_waves: list[int] = []
 
     for it in range(1, cfg.max_iters + 1):
         pruned_iter = pruned_mode and it > 1
@@ -453,7 +499,8 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             timer.start("pruning")
             cents.refresh(d_prime, d_prime)
             ws.counters.zero_()
-            pruned_assign_pass(data, cents, ws, plan)
+            ws.diag.zero_()
+            pruned_assign_pass(data, cents, ws, plan, order=ws.order[:n_local] if have_order else None)
             timer.stop("pruning")
             work.front_pair_dims += n * k * d_prime
             if not cfg.pruning_sentinel:
@@ -469,6 +516,8 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         if it > 1:
             n_changed = int(round(ch))
         if pruned_iter:
+            scan_blocks.append(int(ws.diag[0].item()))
+            scan_waves.append(int(ws.diag[1].item()))
             survivors, touched = int(round(sv)), int(round(td))
             prune_rate = prune_rate_from_totals(survivors, n, k)
             work.tail_dims += touched
@@ -488,6 +537,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             break
         timer.start("update")
         counts = update_centroids_device(data, cents, ws, comm, sums_buf)
+        have_order = True  # ws.order now lists rows grouped by their current assignment
         n_splits = apply_splits_device(cents, counts, rng_split) if cfg.split_empty else 0
         timer.stop("update")
         if pruned_iter:
@@ -526,4 +576,6 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         phase_seconds=phase,
         centroids_dev=cents.c,
         assign_dev=ws.assign[:n_local],
+        scan_blocks=scan_blocks,
+        scan_waves=scan_waves,
     )

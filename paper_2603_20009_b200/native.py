@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libskm_b200.so")
+LIB_PATH = os.environ.get("SKM_LIB", os.path.join(_HERE, "libskm_b200.so"))
 
 
 class NativeUnavailable(RuntimeError):
@@ -49,12 +49,14 @@ class ScanParams(C.Structure):
         ("cand_idx", _vp), ("cand_val", _vp), ("cand_cnt", _vp), ("cap", _i),
         ("dense", _vp), ("ld_dense", _ll), ("dense_row", _vp), ("k", _i),
         ("rows", _vp), ("n_rows", _i), ("row0", _ll),
+        ("row_map", _vp), ("work", _vp),
         ("x", _vp), ("ldx", _ll),
         ("tails", _vp), ("nb", _i), ("d_prime", _i),
         ("theta", _vp), ("block_dims", _vp),
         ("tau", _vp), ("assign", _vp),
         ("counters", _vp),
         ("dense_mode", _i),
+        ("counters_ext", _vp),
     ]
 
 
@@ -66,6 +68,7 @@ _SIGS = {
     "skm_split_hilo": ([_vp, _ll, _i, _i, _vp, _vp, _ll, _vp], _i),
     "skm_row_sq_norms": ([_vp, _ll, _i, _i, _vp, _vp], _i),
     "skm_gather_rows": ([_vp, _ll, _vp, _i, _i, _vp, _ll, _vp], _i),
+    "skm_gather_rows_i32": ([_vp, _ll, _vp, _i, _i, _vp, _ll, _vp], _i),
     "skm_fill_f32": ([_vp, _ll, _f, _vp], _i),
     "skm_copy_i32": ([_vp, _vp, _i, _vp], _i),
     "skm_seed_thresholds": ([_vp, _ll, _vp, _ll, _vp, _i, _i, _vp, _vp], _i),

@@ -268,6 +268,8 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel):
     p.tails, p.nb, p.d_prime = tails.data_ptr(), nb, dp
     p.theta, p.block_dims = theta.data_ptr(), bdims.data_ptr()
     p.tau, p.assign, p.counters = tau.data_ptr(), assign.data_ptr(), counters.data_ptr()
+    work = torch.zeros(256, dtype=torch.int32, device="cuda")
+    p.work = work.data_ptr()
     import ctypes
     native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
     # overflow rows -> dense pass over their full distance rows

@@ -1,0 +1,41 @@
+"""Small fit driver for ncu captures: c2 shape (d=1536, k=4096) on fewer rows.
+   ncu ... python tools/profile_fit.py --n 200000 --iters 4"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200 import api  # noqa: E402
+from paper_2603_20009_b200.config import KMeansConfig  # noqa: E402
+from paper_2603_20009_b200.hostmath import generate_rotation  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=200000)
+ap.add_argument("--d", type=int, default=1536)
+ap.add_argument("--k", type=int, default=4096)
+ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+x = make_shard_device(a.n, a.d, 8192, 0, a.n, 0, dev)
+cfg = KMeansConfig(k=a.k, max_iters=a.iters, seed=0)
+rot = generate_rotation(a.d, 0)
+from paper_2603_20009_b200 import profiling  # noqa: E402
+prof = profiling.KernelTimer()
+for i in range(a.reps):
+    if i == a.reps - 1:
+        with profiling.active(prof):
+            r = api.fit_device(x, a.d, cfg, rot)
+    else:
+        r = api.fit_device(x, a.d, cfg, rot)
+torch.cuda.synchronize()
+print("kernels ms:", {k: round(v["ms"], 2) for k, v in sorted(prof.summary().items(), key=lambda kv: -kv[1]["ms"])})
+st = r.loop.stats
+print("d'", [s.d_prime for s in st], "surv/vec", [round(s.survivors / a.n, 1) for s in st],
+      "tail/vec", [round(s.tail_dims_touched / a.n) for s in st],
+      "computed blocks/vec", [round(b / a.n) for b in r.loop.scan_blocks],
+      "waves/vec", [round(w / a.n, 1) for w in r.loop.scan_waves], "phase", {k: round(v * 1e3, 1) for k, v in r.phase.items()})
