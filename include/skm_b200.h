@@ -117,7 +117,7 @@ typedef struct skm_scan_params {
   const float* dense; long long ld_dense; const int* dense_row; int k;       /* dense mode */
   const int* rows; int n_rows; long long row0;  /* batch-local rows to scan (NULL = 0..n_rows-1) */
   const int* row_map;                          /* optional global row of each batch-local row */
-  void* work;                                  /* device u32[SKM_SCAN_MAX_QUEUES] scratch: per-SM row queues */
+  void* work;                                  /* device u32 scratch: dynamic row-queue counter */
   const float* x; long long ldx;
   const float* tails; int nb; int d_prime;
   const float* theta; const int* block_dims;   /* nb+1 factors, nb block widths */
@@ -126,8 +126,19 @@ typedef struct skm_scan_params {
   int dense_mode;
   unsigned long long* counters_ext;            /* optional diagnostics: += {block sums computed} */
 } skm_scan_params;
-#define SKM_SCAN_MAX_QUEUES 256
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
+
+/* ---- exact top-k + ETR tally ------------------------------------------------------- */
+/* k smallest of each row by (value, column) ascending, ties to the lower column (stable
+ * argsort semantics); out_idx = column + col_offset.  k <= 2048. */
+int skm_topk_rows(const float* d, long long ld, int rows, int cols, int k, int* out_idx, float* out_val,
+                  long long out_ld, int col_offset, void* stream);
+/* merge `shards` sorted per-shard top-k lists laid out [shard][row][k] */
+int skm_topk_merge(const int* in_idx, const float* in_val, int shards, int k, int rows, int* out_idx, float* out_val,
+                   void* stream);
+/* hits[q] = #{g in gt[q][:top_k], row_lo <= g < row_hi : assign[g-row_lo] in probe[q][:nprobe]} */
+int skm_etr_hits(const int* gt, int gt_ld, int top_k, const int* probe, int probe_ld, int nprobe, const int* assign,
+                 long long row_lo, long long row_hi, int k, int nq, int* hits, void* stream);
 
 #ifdef __cplusplus
 }

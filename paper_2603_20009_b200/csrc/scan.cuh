@@ -59,8 +59,7 @@ struct ScanArgs {
   int n_rows;
   long long row0;  // global row of batch-local row 0 (when row_map == nullptr)
   const int* row_map;      // optional: global row of batch-local row (cluster-ordered batches)
-  unsigned int* work;      // per-SM row-queue counters [n_queues] (zeroed by the launcher)
-  int n_queues;
+  unsigned int* work;      // global row-queue counter (zeroed by the launcher)
   const float* x;
   long long ldx;
   const float4* tails;  // [k][16][nb] float4
@@ -138,17 +137,6 @@ __device__ __forceinline__ int walk_exact(float p, const float* rec_row, int nd,
   return ST_COMPLETE;
 }
 
-__device__ __forceinline__ int next_row(const ScanArgs& a, int& qs, int& lo, int& hi) {
-  for (int tries = 0; tries <= a.n_queues; ++tries) {
-    const int r = lo + static_cast<int>(atomicAdd(a.work + qs, 1u));
-    if (r < hi) return r;
-    qs = (qs + 1) % a.n_queues;
-    lo = static_cast<int>((static_cast<long long>(a.n_rows) * qs) / a.n_queues);
-    hi = static_cast<int>((static_cast<long long>(a.n_rows) * (qs + 1)) / a.n_queues);
-  }
-  return a.n_rows;
-}
-
 #ifndef SKM_SCAN_MINB
 #define SKM_SCAN_MINB 1
 #endif
@@ -186,23 +174,11 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
                               : (SCAN_DEPTH == 2) ? 0x55555555u : 0xffffffffu;  // slot leader lanes
 
   unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0;
-  // per-SM row queue: SM s owns the contiguous (cluster-sorted) row range [s*n/nq, (s+1)*n/nq),
-  // so the warps sharing an SM's L1 scan rows of the same cluster (shared candidates);
-  // exhausted queues steal from the following ones.
-  int q_sm = 0, q_lo = 0, q_hi = 0;
-  if (lane == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    q_sm = static_cast<int>(smid % static_cast<unsigned>(a.n_queues));
-    q_lo = static_cast<int>((static_cast<long long>(a.n_rows) * q_sm) / a.n_queues);
-    q_hi = static_cast<int>((static_cast<long long>(a.n_rows) * (q_sm + 1)) / a.n_queues);
-  }
-
   while (true) {
     // rows are handed out in order from a global counter: warps running concurrently work on
     // neighbouring (cluster-sorted) rows, so their candidate centroids' tails stay L2-hot
     int r = 0;
-    if (lane == 0) r = next_row(a, q_sm, q_lo, q_hi);
+    if (lane == 0) r = static_cast<int>(atomicAdd(a.work, 1u));
     r = __shfl_sync(FULL, r, 0);
     if (r >= a.n_rows) break;
     const int rl = a.rows ? a.rows[r] : r;

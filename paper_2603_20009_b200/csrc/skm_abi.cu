@@ -13,6 +13,7 @@
 #include "gemm_tf32x3.cuh"
 #include "update.cuh"
 #include "scan.cuh"
+#include "topk.cuh"
 
 namespace {
 
@@ -404,13 +405,9 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.work = reinterpret_cast<unsigned int*>(p->work);
   if (!a.work) return fail(SKM_E_ARG, "pruned_scan: work counter required");
   {
-    int dev0 = 0, nsm = 148;
-    cudaGetDevice(&dev0);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev0);
-    // one global queue measured fastest (per-SM queues: 3x slower); SKM_SCAN_QUEUES overrides
-    const char* qv = getenv("SKM_SCAN_QUEUES");
-    a.n_queues = std::max(1, std::min(qv ? atoi(qv) : 1, std::min(nsm, SKM_SCAN_MAX_QUEUES)));
-    cudaError_t e = cudaMemsetAsync(p->work, 0, sizeof(unsigned int) * a.n_queues, as_stream(stream));
+    // one global row queue: concurrently running warps then scan neighbouring cluster-sorted
+    // rows (per-SM queues over contiguous ranges measured 3x slower)
+    cudaError_t e = cudaMemsetAsync(p->work, 0, sizeof(unsigned int), as_stream(stream));
     if (e != cudaSuccess) return cuda_fail(e, "pruned_scan work reset");
   }
   a.x = p->x;
@@ -449,6 +446,43 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
     skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   }
   SKM_LAUNCH_CHECK("pruned_scan");
+  return SKM_OK;
+}
+
+// ---------------------------------------------------------------- top-k / ETR
+int skm_topk_rows(const float* d, long long ld, int rows, int cols, int k, int* out_idx, float* out_val,
+                  long long out_ld, int col_offset, void* stream) {
+  if (rows <= 0 || k <= 0) return SKM_OK;
+  if (k > skm::TOPK_MAX) return fail(SKM_E_ARG, "topk_rows: k too large (max 2048)");
+  skm::topk_rows_kernel<<<rows, skm::TOPK_THREADS, 0, as_stream(stream)>>>(d, ld, cols, k, out_idx, out_val, out_ld,
+                                                                           col_offset);
+  SKM_LAUNCH_CHECK("topk_rows");
+  return SKM_OK;
+}
+
+int skm_topk_merge(const int* in_idx, const float* in_val, int shards, int k, int rows, int* out_idx, float* out_val,
+                   void* stream) {
+  if (rows <= 0) return SKM_OK;
+  if (shards > 8) return fail(SKM_E_ARG, "topk_merge: at most 8 shards");
+  skm::topk_merge_kernel<<<(rows + 127) / 128, 128, 0, as_stream(stream)>>>(in_idx, in_val, shards, k, rows, out_idx,
+                                                                            out_val);
+  SKM_LAUNCH_CHECK("topk_merge");
+  return SKM_OK;
+}
+
+int skm_etr_hits(const int* gt, int gt_ld, int top_k, const int* probe, int probe_ld, int nprobe, const int* assign,
+                 long long row_lo, long long row_hi, int k, int nq, int* hits, void* stream) {
+  if (nq <= 0) return SKM_OK;
+  const size_t smem = sizeof(unsigned) * ((k + 31) / 32);
+  if (smem > 200 * 1024) return fail(SKM_E_ARG, "etr_hits: k too large for the shared bitmap");
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(skm::etr_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    set = true;
+  }
+  skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, row_lo,
+                                                             row_hi, k, hits);
+  SKM_LAUNCH_CHECK("etr_hits");
   return SKM_OK;
 }
 

@@ -470,7 +470,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
     phase: dict[str, float] = {}
     if etr is not None:
         timer.start("ground_truth")
-        etr.setup(data, comm)
+        etr.setup(data, comm, n_global=n, row_lo=row_lo)
         timer.stop("ground_truth")
     sums_buf = None
     if comm.world > 1:

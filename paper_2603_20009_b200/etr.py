@@ -1,0 +1,220 @@
+"""Early Termination by Recall on the device.
+
+Setup (once per fit, core.py:305-316):
+  q_idx = default_rng([seed, 4]).choice(n, nq)   (host RNG -> device gather)
+  GT    = exact top_k of every query over all rows: distance GEMM (tcgen05 3xTF32, DIST
+          epilogue) + exact per-row radix top-k with lowest-index ties
+          (brute_force_topk, evaluation.py:53-75).  Row-sharded: per-rank top-k + merge.
+Per iteration (after update + split, core.py:380-387):
+  probe = top-nprobe post-update centroids per query (GEMM + top-k, stable ties)
+  hits_q = #{g in GT_q : assign[g] in probe_q}        (integer tally, allreduced)
+  recall = (sum_q hits_q / top_k) / nq               (host f64, query order)
+The tally equals the reference's per-query recall (evaluation.py:142-170): a GT member that
+is a candidate always ranks within top_k among the candidates.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import native
+from .device import padded_ld, ptr, require_cuda, stream_handle
+from .hostmath import etr_should_stop
+
+
+@dataclass
+class GroundTruth:
+    indices: np.ndarray   # (n_queries, k_gt) int64
+    distances: np.ndarray  # (n_queries, k_gt) float32
+    k_gt: int
+    metric: str = "l2"
+
+
+@dataclass
+class RecallHistory:
+    values: list = field(default_factory=list)
+    tolerance: float = 0.005
+    patience: int = 2
+
+    def append(self, value: float) -> None:
+        self.values.append(float(value))
+
+    def should_stop(self) -> bool:
+        return etr_should_stop(self.values, self.tolerance, self.patience)
+
+
+def _split(x: torch.Tensor, cols: int):
+    hi = torch.empty_like(x)
+    lo = torch.empty_like(x)
+    if x.shape[0]:
+        native.call("skm_split_hilo", ptr(x), x.shape[1], x.shape[0], cols, ptr(hi), ptr(lo), x.shape[1],
+                    stream_handle())
+    return hi, lo
+
+
+def _norms(x: torch.Tensor, dims: int) -> torch.Tensor:
+    out = torch.empty(max(x.shape[0], 1), dtype=torch.float32, device=x.device)
+    if x.shape[0]:
+        native.call("skm_row_sq_norms", ptr(x), x.shape[1], x.shape[0], dims, ptr(out), stream_handle())
+    return out
+
+
+def device_topk_distances(q: torch.Tensor, q_hi, q_lo, q_sq, x: torch.Tensor, x_hi, x_lo, x_sq, d: int, k: int,
+                          col_offset: int = 0, max_bytes: int = 1 << 30) -> tuple[torch.Tensor, torch.Tensor]:
+    """Exact top-k rows of x for each query (squared L2 via the expansion identity, stable
+    ties).  Returns (idx int32 (nq, k) with col_offset added, dist float32 (nq, k))."""
+    from .engine import _gemm, _n_split
+    nq, n = q.shape[0], x.shape[0]
+    dev = q.device
+    kk = min(k, n)
+    out_i = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+    out_v = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+    if nq == 0 or n == 0:
+        return out_i, out_v
+    qb = max(1, min(nq, max_bytes // (4 * padded_ld(n))))
+    for s in range(0, nq, qb):
+        e = min(nq, s + qb)
+        D = torch.empty((e - s, padded_ld(n)), dtype=torch.float32, device=dev)
+        _gemm(q_hi[s:e], q_lo[s:e], x_hi, x_lo, e - s, n, d, native.GEMM_DIST, out=D, xsq=q_sq[s:e], ysq=x_sq,
+              n_split=_n_split(e - s, n))
+        native.call("skm_topk_rows", ptr(D), D.stride(0), e - s, n, kk, ptr(out_i[s:e]), ptr(out_v[s:e]), kk,
+                    col_offset, stream_handle(), nbytes=5.0 * 4 * (e - s) * n)
+    return out_i, out_v
+
+
+class EtrState:
+    """Ground truth + probe state for one fit (replicated across ranks)."""
+
+    def __init__(self, cfg):
+        self.etr = cfg.etr
+        self.k = cfg.k
+        self.seed = cfg.seed
+        self.top_k = cfg.etr.top_k
+        self.nprobe = int(np.ceil(cfg.etr.nprobe_fraction * cfg.k))
+
+    def setup(self, data, comm, n_global: int | None = None, row_lo: int = 0):
+        dev = data.x.device
+        n = data.n if n_global is None else n_global
+        self.row_lo, self.row_hi = row_lo, row_lo + data.n
+        nq = min(self.etr.n_queries, n)
+        q_idx = np.random.default_rng([self.seed, 4]).choice(n, size=nq, replace=False)
+        self.q_idx = q_idx
+        q = torch.zeros((nq, data.ld), dtype=torch.float32, device=dev)
+        mine = np.flatnonzero((q_idx >= row_lo) & (q_idx < row_lo + data.n))
+        if mine.size:
+            src = torch.tensor(q_idx[mine] - row_lo, dtype=torch.int64, device=dev)
+            tmp = torch.empty((mine.size, data.ld), dtype=torch.float32, device=dev)
+            native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(src), int(mine.size), data.ld, ptr(tmp),
+                        data.ld, stream_handle())
+            q[torch.tensor(mine, dtype=torch.int64, device=dev)] = tmp
+        comm.allreduce_(q)
+        self.q = q
+        self.q_hi, self.q_lo = _split(q, data.d)
+        self.q_sq = _norms(q, data.d)
+        top_k = self.top_k
+        if top_k > n:
+            raise ValueError(f"k_gt={top_k} exceeds collection size {n}")
+        gi, gv = device_topk_distances(q, self.q_hi, self.q_lo, self.q_sq, data.x, data.hi, data.lo,
+                                       data.norms(data.d), data.d, top_k, col_offset=row_lo)
+        if comm.world > 1:
+            # per-rank top-k -> allgather -> stable (dist, index) merge
+            kk = gi.shape[1]
+            ai = [torch.empty_like(gi) for _ in range(comm.world)]
+            av = [torch.empty_like(gv) for _ in range(comm.world)]
+            comm.dist.all_gather(ai, gi.contiguous(), group=comm.group)
+            comm.dist.all_gather(av, gv.contiguous(), group=comm.group)
+            all_i = torch.stack(ai).contiguous()
+            all_v = torch.stack(av).contiguous()
+            gi = torch.empty((nq, top_k), dtype=torch.int32, device=dev)
+            gv = torch.empty((nq, top_k), dtype=torch.float32, device=dev)
+            native.call("skm_topk_merge", ptr(all_i), ptr(all_v), comm.world, kk, nq, ptr(gi), ptr(gv),
+                        stream_handle())
+        self.gt_idx, self.gt_val = gi.contiguous(), gv.contiguous()
+        self.hits = torch.zeros(nq, dtype=torch.int32, device=dev)
+
+    def probe(self, data, cents, ws, comm) -> float:
+        nq = self.q.shape[0]
+        c_hi, c_lo = _split(cents.c, cents.d)
+        c_sq = _norms(cents.c, cents.d)
+        pi, _ = device_topk_distances(self.q, self.q_hi, self.q_lo, self.q_sq, cents.c, c_hi, c_lo, c_sq, cents.d,
+                                      self.nprobe)
+        native.call("skm_etr_hits", ptr(self.gt_idx), self.gt_idx.shape[1], self.top_k, ptr(pi), pi.shape[1],
+                    pi.shape[1], ptr(ws.assign), self.row_lo, self.row_hi, cents.k, nq, ptr(self.hits),
+                    stream_handle())
+        h = comm.allreduce_(self.hits.to(torch.int64)) if comm.world > 1 else self.hits
+        hits = h.cpu().numpy()
+        total = 0.0
+        for v in hits:  # the reference's accumulation order (evaluation.py:169-170)
+            total += int(v) / self.top_k
+        return total / nq
+
+    def should_stop(self, history) -> bool:
+        return etr_should_stop(history, self.etr.tolerance, self.etr.patience_iters)
+
+
+# ------------------------------------------------------------------ host-array entry points
+def brute_force_topk(x, queries, k_gt: int, query_batch: int = 128, device=None) -> GroundTruth:
+    """Exact top-k by squared L2 over the collection, ties to the lower index
+    (evaluation.py:53-75), computed on the B200."""
+    from .config import DimensionMismatch
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    queries = np.ascontiguousarray(queries, dtype=np.float32)
+    if x.shape[1] != queries.shape[1]:
+        raise DimensionMismatch(f"data dim {x.shape[1]} != query dim {queries.shape[1]}")
+    if k_gt > x.shape[0]:
+        raise ValueError(f"k_gt={k_gt} exceeds collection size {x.shape[0]}")
+    dev = require_cuda(device)
+    from .api import _h2d
+    d = x.shape[1]
+    X = _h2d(x, dev)
+    Q = _h2d(queries, dev)
+    xh, xl = _split(X, d)
+    qh, ql = _split(Q, d)
+    gi, gv = device_topk_distances(Q, qh, ql, _norms(Q, d), X, xh, xl, _norms(X, d), d, k_gt)
+    return GroundTruth(indices=gi.cpu().numpy().astype(np.int64), distances=gv.cpu().numpy(), k_gt=k_gt)
+
+
+def build_cluster_lists(assignments, k: int, device=None) -> list:
+    """Per-cluster row lists in ascending row order (evaluation.py:78-83) from the device
+    stable cluster sort."""
+    a = np.ascontiguousarray(assignments, dtype=np.int32)
+    dev = require_cuda(device)
+    n = a.shape[0]
+    A = torch.from_numpy(a).to(dev)
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    counts = torch.empty(k, dtype=torch.int32, device=dev)
+    offs = torch.empty(k, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(native.load().skm_update_workspace_bytes(n, k)), dtype=torch.uint8, device=dev)
+    native.call("skm_cluster_sort", ptr(A), n, k, ptr(order), ptr(counts), ptr(offs), ptr(ws), ws.numel(),
+                stream_handle())
+    o = order[:n].cpu().numpy().astype(np.int64)
+    bounds = np.cumsum(counts.cpu().numpy().astype(np.int64))[:-1]
+    return np.split(o, bounds)
+
+
+def etr_probe(centroids, train_x, assignments, queries, gt: GroundTruth, nprobe: int, top_k: int,
+              device=None) -> float:
+    """Mean probe recall of the current state (evaluation.py:142-170), device tally."""
+    dev = require_cuda(device)
+    from .api import _h2d
+    c = np.ascontiguousarray(centroids, dtype=np.float32)
+    q = np.ascontiguousarray(queries, dtype=np.float32)
+    k, d = c.shape
+    nprobe = min(max(1, nprobe), k)
+    Cd, Qd = _h2d(c, dev), _h2d(q, dev)
+    ch, cl = _split(Cd, d)
+    qh, ql = _split(Qd, d)
+    pi, _ = device_topk_distances(Qd, qh, ql, _norms(Qd, d), Cd, ch, cl, _norms(Cd, d), d, nprobe)
+    gt_i = torch.from_numpy(np.ascontiguousarray(gt.indices[:, :top_k], dtype=np.int32)).to(dev)
+    A = torch.from_numpy(np.ascontiguousarray(assignments, dtype=np.int32)).to(dev)
+    hits = torch.zeros(q.shape[0], dtype=torch.int32, device=dev)
+    native.call("skm_etr_hits", ptr(gt_i), gt_i.shape[1], top_k, ptr(pi), pi.shape[1], nprobe, ptr(A), 0,
+                A.shape[0], k, q.shape[0], ptr(hits), stream_handle())
+    total = 0.0
+    for v in hits.cpu().numpy():
+        total += int(v) / top_k
+    return total / q.shape[0]

@@ -110,13 +110,16 @@ FIT_CASES = {
     "sampled": (("blobs", 3000, 128, 24, 12), dict(k=16, max_iters=5, seed=3, sampling_fraction=0.5)),
     "etr": (("blobs", 4000, 128, 60, 21), dict(k=40, max_iters=12, seed=1)),
     "split": (("blobs", 1200, 96, 4, 13), dict(k=40, max_iters=5, seed=0)),
+    "etr2": (("blobs", 12000, 128, 200, 3, 4.0), dict(k=100, max_iters=25, seed=1)),
 }
 
 
 def make_x(spec):
-    kind, n, d, centers, seed = spec
+    kind, n, d, centers, seed = spec[:5]
+    spread = spec[5] if len(spec) > 5 else None
     if kind == "blobs":
-        return make_blobs(n, d, centers, seed=seed)
+        return make_blobs(n, d, centers, seed=seed) if spread is None else \
+            make_blobs(n, d, centers, seed=seed, spread=spread)
     return make_skewed_blobs(n, d, centers, seed=seed)
 
 
@@ -124,7 +127,7 @@ def fits():
     out = {}
     for name, (spec, kw) in FIT_CASES.items():
         x = make_x(spec)
-        if name == "etr":
+        if name.startswith("etr"):
             kw = dict(kw, etr=skm.EtrConfig(n_queries=300, top_k=10))
         fit_case(name, x, skm.KMeansConfig(**kw), out)
     # hierarchical
