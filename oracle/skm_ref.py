@@ -23,7 +23,16 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import kernels_np as K
+from . import kernels_c as _KC
+from . import kernels_np as _KN
+
+# the C/OpenMP restatement when built (same bits, reference-compiled speed), else NumPy
+K = _KC if _KC.available() else _KN
+
+
+def use_numpy_kernels(flag: bool = True) -> None:
+    global K
+    K = _KN if flag or not _KC.available() else _KC
 
 PDX_BLOCK, MAX_BANK, D_MIN, D_ALIGN = 64, 1024, 16, 8
 SPLIT_EPS = np.float32(1.0 / 1024.0)
@@ -197,7 +206,7 @@ def pruned_pass(xr, c, dp, p: Params, tau, assign):
         front = np.ascontiguousarray(xb[:, :dp])
         for s1, (bf, tail, bw, boff) in banks:
             v = expand(front @ bf.T, xs[s0:e0], ys[s1:s1 + bf.shape[0]])
-            sv, td = K.scan_bank(v, xb, tail, boff, bw, f, dp, s1, tb, ab, p.pruning_sentinel)
+            sv, td = K.scan_bank(np.ascontiguousarray(v), xb, tail, boff, bw, f, dp, s1, tb, ab, p.pruning_sentinel)
             surv += sv
             touched += td
         changed += int(np.count_nonzero(prev != ab))
