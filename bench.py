@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=8192, help="rows in the bounded CPU sample")
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="rows in the bounded CPU sample (default n/16: ~10-30 s of CPU work)")
     return ap.parse_args()
 
 
@@ -117,7 +118,7 @@ def make_shard_device(n, d, centers, lo, hi, seed, dev):
 
 
 # ----------------------------------------------------------------------------- reference arm
-def cpu_reference_sample(args, sample_rows, iters=3):
+def cpu_reference_sample(args, sample_rows, iters=10):
     """Reference CPU path (oracle/ restatement of core.fit) on a bounded sample of the same
     workload: returns (iterations/s scaled to the full n, seconds, description)."""
     from oracle import skm_ref
@@ -144,14 +145,15 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     per_step = []
     desc = ""
-    for i in range(args.warmup + args.steps):
-        v, dt, desc = cpu_reference_sample(args, args.cpu_sample, iters=2)
-        if i >= args.warmup:
+    n_warm, n_steps = min(args.warmup, 1), min(args.steps, 2)  # each sample is ~10-30 s of CPU work
+    for i in range(n_warm + n_steps):
+        v, dt, desc = cpu_reference_sample(args, args.cpu_sample or args.n // 16, iters=args.iters)
+        if i >= n_warm:
             per_step.append(v)
     value = float(np.median(per_step))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * args.iters / value,
+        "steps": n_steps, "warmup": n_warm, "ms_per_step": 1e3 * args.iters / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"c2: {args.n}x{args.d} fp32 skewed blobs, k={args.k}, {args.iters} fixed iterations",
                    "sample": f"bounded CPU sample per step: {desc}"},
@@ -229,7 +231,13 @@ def main():
     value = iters_done / elapsed
     ms_per_step = 1e3 * elapsed / args.steps
     launches = prof.launches
-    roof = prof.roofline(args.steps)
+    # algorithmic bytes of the pruning scan per timed region: the x tail rows it streams from HBM
+    # plus the centroid tail values it evaluates (4 B per touched (vector, centroid, dim), from
+    # the exact dims-touched counter; these are served from the L2-resident PDX tails)
+    st_last = res.loop.stats
+    scan_bytes = args.steps * sum(4.0 * args.n * (args.d - s.d_prime) + 4.0 * s.tail_dims_touched
+                                  for s in st_last if s.d_prime is not None)
+    roof = prof.roofline(args.steps, bytes_override={"pruned_scan": scan_bytes})
 
     # ---- end to end through the public entry with host (pinned) input ----
     e2e = None
@@ -257,7 +265,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc = cpu_reference_sample(args, args.cpu_sample, iters=2)
+        v, dt, desc = cpu_reference_sample(args, args.cpu_sample or args.n // 16, iters=args.iters)
         cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": desc}
 
     if rank == 0:

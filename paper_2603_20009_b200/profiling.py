@@ -61,8 +61,11 @@ class KernelTimer:
             s["bytes"] += by
         return agg
 
-    def roofline(self, steps: int) -> dict:
+    def roofline(self, steps: int, bytes_override: dict | None = None) -> dict:
         agg = self.summary()
+        for k_, v_ in (bytes_override or {}).items():
+            if k_ in agg:
+                agg[k_]["bytes"] = v_
         if not agg:
             return {}
         pk = peaks()
@@ -84,7 +87,10 @@ class KernelTimer:
         else:
             gbs = top["bytes"] / (top["ms"] * 1e-3) / 1e9
             out.update({"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": gbs / pk["hbm_gbs"]})
+                        "frac": gbs / pk["hbm_gbs"],
+                        "note": "achieved = algorithmic bytes / time; for pruned_scan the bytes are the x tail "
+                                "rows (HBM) + 4 B per touched (vector, centroid, dim) of the L2-resident "
+                                "centroid tails (exact dims-touched counter)"})
         out["per_kernel_ms_per_step"] = {k: round(v["ms"] / steps, 3) for k, v in agg.items()}
         return out
 
