@@ -329,10 +329,11 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         sp = native.ScanParams()
         if ordered:
             rmap = order[b0:b0 + bn]
-            native.call("skm_gather_rows_i32", ptr(data.hi), data.ld, ptr(rmap), bn, dp, ptr(ga_hi), fld, st,
-                        nbytes=8.0 * bn * dp)
-            native.call("skm_gather_rows_i32", ptr(data.lo), data.ld, ptr(rmap), bn, dp, ptr(ga_lo), fld, st,
-                        nbytes=8.0 * bn * dp)
+            # the front buffers may be wider than fld (allocated at a larger d'): use their stride
+            native.call("skm_gather_rows_i32", ptr(data.hi), data.ld, ptr(rmap), bn, dp, ptr(ga_hi),
+                        ga_hi.stride(0), st, nbytes=8.0 * bn * dp)
+            native.call("skm_gather_rows_i32", ptr(data.lo), data.ld, ptr(rmap), bn, dp, ptr(ga_lo),
+                        ga_lo.stride(0), st, nbytes=8.0 * bn * dp)
             native.call("skm_gather_rows_i32", ptr(xsq.view(-1, 1)), 1, ptr(rmap), bn, 1, ptr(ws.bx.view(-1, 1)), 1,
                         st)
             native.call("skm_gather_rows_i32", ptr(ws.thr.view(-1, 1)), 1, ptr(rmap), bn, 1,

@@ -1,0 +1,79 @@
+"""Row-sharded data-parallel fit on the real device path with world size 2.
+
+Only one GPU is available to this build, so both ranks share cuda:0 and talk over gloo
+(which accepts CUDA tensors); the device kernels, the sharded update (ordered partial sums ->
+packed allreduce -> finalize), the Forgy-row / ETR-query assembly, the sharded ETR ground
+truth (per-rank top-k -> allgather -> stable merge) and the integer hit tally all run exactly
+as under NCCL.  Result must match the single-process fit: integer outputs equal, centroids
+equal up to the f64 summation order of the cross-rank reduction."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import make_blobs
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rank, world, port, q, etr):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_20009_b200 import api
+        from paper_2603_20009_b200.config import EtrConfig, KMeansConfig
+        from paper_2603_20009_b200.engine import Comm
+        from paper_2603_20009_b200.hostmath import generate_rotation
+        torch.cuda.set_device(0)
+        x = make_blobs(12000, 128, 200, seed=3, spread=4.0)
+        n, d = x.shape
+        comm = Comm()
+        lo, hi = comm.shard(n)
+        cfg = KMeansConfig(k=100, max_iters=8, seed=1,
+                           etr=EtrConfig(n_queries=300, top_k=10) if etr else None)
+        xd = api._h2d(x[lo:hi], torch.device("cuda", 0))
+        res = api.fit_device(xd, d, cfg, generate_rotation(d, 1), comm=comm, n_global=n, row_lo=lo)
+        st = res.loop.stats
+        q.put((rank, {"assign": res.loop.assignments, "lo": lo,
+                      "cent": res.centroids_dev[:, :d].cpu().numpy(),
+                      "dp": [s.d_prime for s in st], "changed": [s.n_changed for s in st],
+                      "surv": [s.survivors for s in st], "recall": res.loop.recall_history,
+                      "term": res.loop.terminated_by}))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("etr", [False, True])
+def test_two_ranks_match_single_rank(etr):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    outs = {}
+    for world in (1, 2):
+        q = ctx.Queue()
+        port = 29600 + world + (os.getpid() % 500) + (100 if etr else 0)
+        ps = [ctx.Process(target=_run, args=(r, world, port, q, etr)) for r in range(world)]
+        for p in ps:
+            p.start()
+        res = dict(q.get(timeout=600) for _ in range(world))
+        for p in ps:
+            p.join(timeout=120)
+        for r, v in res.items():
+            assert isinstance(v, dict), v
+        outs[world] = res
+    one = outs[1][0]
+    two = outs[2]
+    a2 = np.concatenate([two[r]["assign"] for r in sorted(two, key=lambda r: two[r]["lo"])])
+    assert np.array_equal(a2, one["assign"])
+    for r in two:
+        for key in ("dp", "changed", "surv", "recall", "term"):
+            assert two[r][key] == one[key], key
+        rel = np.linalg.norm(two[r]["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
+        assert rel <= 1e-6, rel
+    assert np.array_equal(two[0]["cent"], two[1]["cent"])  # replicas stay identical
