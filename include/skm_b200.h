@@ -127,6 +127,18 @@ typedef struct skm_scan_params {
   unsigned long long* counters_ext;            /* optional diagnostics: += {block sums computed} */
 } skm_scan_params;
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
+/* Block-major tails T2[j][b][t] = C[j][d' + 64 b + t] (zero padded), the layout of the
+ * speculative pair scan. */
+int skm_build_tails_blk(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream);
+/* Production scan (list mode; same semantics and outputs as skm_pruned_scan): rounds of the
+ * speculative pair scan (each row resolved one tau change at a time, exact counters from
+ * per-position outcome records), then the exact sequential scan over rows still open.
+ * p->work: >= 20 device u32; scratch: skm_scan2_scratch_bytes(n_rows, cap) bytes of device
+ * memory; p->counters_ext (optional): 6 u64 diagnostics.
+ * Replaces the scan_bank loop of core.py:237-257 (_kernels.pyx:14-82) for a whole batch. */
+long long skm_scan2_scratch_bytes(int n_rows, int cap);
+int skm_pruned_scan2(const skm_scan_params* p, const float* tails_blk, void* scratch, long long scratch_bytes,
+                     void* stream);
 
 /* ---- exact top-k + ETR tally ------------------------------------------------------- */
 /* k smallest of each row by (value, column) ascending, ties to the lower column (stable

@@ -71,6 +71,11 @@ struct ScanArgs {
   int* assign;             // global rows, in/out
   unsigned long long* counters;  // [0] survivors, [1] dims touched, [2] changed
   unsigned long long* counters_ext;  // optional diagnostics: [0] 64-dim block sums computed
+  // two-phase scan (spec_scan.cuh)
+  const float4* tails_blk;       // [k][nb][16] float4: block-major tails
+  int* cx_rows;                  // complex rows (batch-local) appended by the speculative phase
+  unsigned int* cx_count;
+  const unsigned int* n_rows_dev;  // exact phase: row count read on device (overrides n_rows)
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -174,13 +179,16 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
                               : (SCAN_DEPTH == 2) ? 0x55555555u : 0xffffffffu;  // slot leader lanes
 
   unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0;
+  const int n_rows = a.n_rows_dev ? static_cast<int>(*a.n_rows_dev) : a.n_rows;
+  if (a.counters_ext && a.n_rows_dev && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&a.counters_ext[2], static_cast<unsigned long long>(n_rows));  // rows routed here
   while (true) {
     // rows are handed out in order from a global counter: warps running concurrently work on
     // neighbouring (cluster-sorted) rows, so their candidate centroids' tails stay L2-hot
     int r = 0;
     if (lane == 0) r = static_cast<int>(atomicAdd(a.work, 1u));
     r = __shfl_sync(FULL, r, 0);
-    if (r >= a.n_rows) break;
+    if (r >= n_rows) break;
     const int rl = a.rows ? a.rows[r] : r;
     int n_src;
     if constexpr (DENSE) {

@@ -13,6 +13,7 @@
 #include "gemm_tf32x3.cuh"
 #include "update.cuh"
 #include "scan.cuh"
+#include "spec_scan.cuh"
 #include "topk.cuh"
 
 namespace {
@@ -446,6 +447,166 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
     skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   }
   SKM_LAUNCH_CHECK("pruned_scan");
+  return SKM_OK;
+}
+
+int skm_build_tails_blk(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream) {
+  const int nb = (d - d_prime + 63) / 64;
+  if (k <= 0 || nb <= 0) return SKM_OK;
+  skm::build_tails_blk_kernel<<<grid_for((long long)k * 64 * nb, 256), 256, 0, as_stream(stream)>>>(
+      centroids, ldc, k, d, d_prime, nb, tails);
+  SKM_LAUNCH_CHECK("build_tails_blk");
+  return SKM_OK;
+}
+
+// Production scan (list mode): SPEC_ROUNDS rounds of [row_prep_kernel -> spec_scan_kernel]
+// (spec_scan.cuh) -- round 0 over every row of the batch, round r over the rows frozen in
+// round r-1 -- then the exact sequential kernel over any row still open.  All counts stay on
+// the device (no host synchronisation).  p->work: >= 20 device u32; scratch: see
+// skm_scan2_scratch_bytes.  counters_ext (optional, 6 u64): spec blocks, spec waves, exact
+// blocks, exact waves, exact rows, rows of rounds >= 1.
+long long skm_scan2_scratch_bytes(int n_rows, int cap) {
+  const long long n = std::max(n_rows, 1);
+  return (5 * n + n * static_cast<long long>(cap)) * 4 + n * static_cast<long long>(sizeof(skm::RowDesc)) + 256;
+}
+
+int skm_pruned_scan2(const skm_scan_params* p, const float* tails_blk, void* scratch, long long scratch_bytes,
+                     void* stream) {
+  if (!p) return fail(SKM_E_ARG, "pruned_scan2: null params");
+  if (p->n_rows <= 0) return SKM_OK;
+  if (p->dense_mode) return fail(SKM_E_ARG, "pruned_scan2: list mode only");
+  if (p->nb <= 0 || p->nb > skm::SCAN_NB_MAX) return fail(SKM_E_ARG, "pruned_scan2: tail block count out of range");
+  if (!p->work || !tails_blk || !scratch) return fail(SKM_E_ARG, "pruned_scan2: work, tails_blk and scratch required");
+  if (scratch_bytes < skm_scan2_scratch_bytes(p->n_rows, p->cap)) return fail(SKM_E_ARG, "pruned_scan2: scratch too small");
+  if ((reinterpret_cast<uintptr_t>(tails_blk) & 15) != 0) return fail(SKM_E_ARG, "pruned_scan2: tails_blk must be 16-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  unsigned int* work = reinterpret_cast<unsigned int*>(p->work);
+  {
+    cudaError_t e = cudaMemsetAsync(work, 0, 20 * sizeof(unsigned int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "pruned_scan2 work reset");
+  }
+  const long long n = p->n_rows;
+  int* lists[2] = {reinterpret_cast<int*>(scratch), reinterpret_cast<int*>(scratch) + n};
+  int* st_pos = lists[1] + n;
+  float* st_tau = reinterpret_cast<float*>(st_pos + n);
+  int* st_best = reinterpret_cast<int*>(st_tau + n);
+  int* outcome = st_best + n;
+  skm::RowDesc* desc = reinterpret_cast<skm::RowDesc*>(
+      (reinterpret_cast<uintptr_t>(outcome + n * static_cast<long long>(p->cap)) + 63) & ~uintptr_t(63));
+
+  skm::ScanArgs a{};
+  a.cand_idx = p->cand_idx;
+  a.cand_val = p->cand_val;
+  a.cand_cnt = p->cand_cnt;
+  a.cap = p->cap;
+  a.k = p->k;
+  a.rows = p->rows;
+  a.n_rows = p->n_rows;
+  a.row0 = p->row0;
+  a.row_map = p->row_map;
+  a.x = p->x;
+  a.ldx = p->ldx;
+  a.tails = reinterpret_cast<const float4*>(p->tails);
+  a.tails_blk = reinterpret_cast<const float4*>(tails_blk);
+  a.nb = p->nb;
+  a.d_prime = p->d_prime;
+  a.theta = p->theta;
+  a.block_dims = p->block_dims;
+  a.tau = p->tau;
+  a.assign = p->assign;
+  a.counters = p->counters;
+  a.counters_ext = p->counters_ext;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  {
+    // kernel shape (SKM_SPEC_CFG overrides for experiments): "P<K>" = pair_scan_kernel<K>
+    // (lane-local inner loop of K blocks), "<G>x<P>" = spec_scan_kernel<G, P>
+    static char cfg[8] = "P2";
+    static bool cfg_read = false;
+    if (!cfg_read) {
+      const char* c = getenv("SKM_SPEC_CFG");
+      if (c && strlen(c) >= 2 && strlen(c) < 8) strcpy(cfg, c);
+      cfg_read = true;
+    }
+    const void* kfn = nullptr;
+    int cfg_g = 0, cfg_p = 0;
+    if (cfg[0] == 'P') {
+      const int K = cfg[1] - '0';
+      if (K == 1) kfn = reinterpret_cast<const void*>(skm::pair_scan_kernel<1>);
+      else if (K == 4) kfn = reinterpret_cast<const void*>(skm::pair_scan_kernel<4>);
+      else kfn = reinterpret_cast<const void*>(skm::pair_scan_kernel<2>);
+    } else {
+      cfg_g = cfg[0] - '0';
+      cfg_p = cfg[2] - '0';
+      if (cfg_g == 2 && cfg_p == 1) kfn = reinterpret_cast<const void*>(skm::spec_scan_kernel<2, 1>);
+      else if (cfg_g == 1 && cfg_p == 2) kfn = reinterpret_cast<const void*>(skm::spec_scan_kernel<1, 2>);
+      else { cfg_g = 2; cfg_p = 2; kfn = reinterpret_cast<const void*>(skm::spec_scan_kernel<2, 2>); }
+    }
+    // as many warps per CTA (one CTA per SM) as shared memory allows
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kfn);
+    int optin = 232448;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t per_warp = cfg_g ? skm::spec_dyn_smem(p->nb, 1, cfg_g, cfg_p) : skm::pair_dyn_smem(p->nb, 1);
+    const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 256;
+    const int warps = static_cast<int>(std::min<size_t>(skm::SPEC_WARPS, budget / per_warp));
+    if (warps < 1) return fail(SKM_E_ARG, "pruned_scan2: tail too long for the staging budget");
+    const size_t smem = cfg_g ? skm::spec_dyn_smem(p->nb, warps, cfg_g, cfg_p) : skm::pair_dyn_smem(p->nb, warps);
+    const size_t psmem = skm::prep_dyn_smem(p->nb);
+    {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return cuda_fail(e, "spec_scan smem attribute");
+    }
+    static size_t set_psmem = 0;
+    if (set_psmem < psmem) {
+      cudaError_t e = cudaFuncSetAttribute(skm::row_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(psmem));
+      if (e != cudaSuccess) return cuda_fail(e, "row_prep smem attribute");
+      set_psmem = psmem;
+    }
+    for (int r = 0; r < skm::SPEC_ROUNDS; ++r) {
+      skm::SpecRound R{};
+      R.round = r;
+      R.in_rows = r ? lists[(r - 1) & 1] : nullptr;
+      R.in_cnt = r ? work + 8 + (r - 1) : nullptr;
+      R.out_rows = lists[r & 1];
+      R.out_cnt = work + 8 + r;
+      R.st_pos = st_pos;
+      R.st_tau = st_tau;
+      R.st_best = st_best;
+      R.outcome = outcome;
+      a.work = work + r;
+      const int pblocks = std::max(1, std::min(static_cast<int>((n + skm::PREP_WARPS - 1) / skm::PREP_WARPS),
+                                               r == 0 ? 8 * sms : 2 * sms));
+      skm::row_prep_kernel<<<pblocks, skm::PREP_WARPS * 32, psmem, st>>>(a, R, desc);
+      SKM_LAUNCH_CHECK("row_prep");
+      const int blocks = std::max(1, std::min(static_cast<int>((n + warps - 1) / warps), sms));
+      void* args[] = {&a, &R, &desc};
+      {
+        cudaError_t e = cudaLaunchKernel(kfn, dim3(blocks), dim3(warps * 32), args, smem, st);
+        if (e != cudaSuccess) return cuda_fail(e, "spec_scan launch");
+      }
+      SKM_LAUNCH_CHECK("spec_scan");
+    }
+  }
+  {
+    // rows still open after the speculative rounds: exact sequential kernel (count on device)
+    skm::ScanArgs e = a;
+    e.rows = lists[(skm::SPEC_ROUNDS - 1) & 1];
+    e.n_rows_dev = work + 8 + skm::SPEC_ROUNDS - 1;
+    e.work = work + 16;
+    e.counters_ext = p->counters_ext ? p->counters_ext + 2 : nullptr;
+    const size_t smem = skm::scan_dyn_smem(p->nb);
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      set = true;
+    }
+    const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms));
+    skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(e);
+    SKM_LAUNCH_CHECK("pruned_scan(exact fallback)");
+  }
   return SKM_OK;
 }
 

@@ -21,6 +21,7 @@ the split step, exactly like the reference), a handful of scalars, and -- only w
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -46,6 +47,11 @@ from .hostmath import (
     sentinel_factors,
     threshold_factors,
 )
+
+# Scan selection.  Default: the exact sequential kernel (scan.cuh), the fastest measured on
+# B200.  SKM_SCAN=spec selects the multi-round speculative pair scan (spec_scan.cuh, same
+# results bit for bit; see DESIGN.md section 3 for why it is not the default).
+TWO_PHASE_SCAN = os.environ.get("SKM_SCAN", "exact") == "spec"
 
 _U64_MAX = (1 << 64) - 1
 
@@ -97,6 +103,7 @@ class LoopOutput:
     device_ms: dict = field(default_factory=dict)
     scan_blocks: list = field(default_factory=list)  # speculative 64-dim block sums computed per pruned iter
     scan_waves: list = field(default_factory=list)   # warp-waves of the scan per pruned iter
+    scan_diag: list = field(default_factory=list)    # [spec blocks, spec waves, exact blocks, exact waves, exact rows]
 
 
 class _Timer:
@@ -166,6 +173,7 @@ class Centroids:
         self.lo = torch.empty_like(c)
         self.ysq = torch.empty(self.k, dtype=torch.float32, device=c.device)
         self.tails = None
+        self.tails_blk = None
 
     def refresh(self, dims: int, d_prime: int | None):
         """Recompute split + norms over `dims` (+ tails at d_prime) after an update."""
@@ -179,6 +187,11 @@ class Centroids:
                 self.tails = torch.empty(need, dtype=torch.float32, device=self.c.device)
             native.call("skm_build_tails", ptr(self.c), self.ld, self.k, self.d, d_prime, ptr(self.tails),
                         stream_handle())
+            if TWO_PHASE_SCAN:
+                if self.tails_blk is None or self.tails_blk.numel() < need:
+                    self.tails_blk = torch.empty(need, dtype=torch.float32, device=self.c.device)
+                native.call("skm_build_tails_blk", ptr(self.c), self.ld, self.k, self.d, d_prime,
+                            ptr(self.tails_blk), stream_handle())
 
 
 def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
@@ -228,7 +241,12 @@ class Workspace:
         self.cand_cnt = torch.empty(b, dtype=i32, device=dev)
         self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
         self.work = torch.zeros(256, dtype=torch.int32, device=dev)  # per-SM scan row queues
-        self.diag = torch.zeros(4, dtype=torch.int64, device=dev)  # scan diagnostics (blocks computed)
+        # scan diagnostics: spec blocks, spec waves, exact blocks, exact waves, rows routed to the exact phase
+        self.diag = torch.zeros(8, dtype=torch.int64, device=dev)
+        self.scan_scratch = None
+        if TWO_PHASE_SCAN:
+            nbytes = int(native.load().skm_scan2_scratch_bytes(self.batch, self.cap))
+            self.scan_scratch = torch.empty((nbytes + 3) // 4, dtype=torch.int32, device=dev)
         self.bx = torch.empty(b, dtype=f32, device=dev)
         self.bthr = torch.empty(b, dtype=f32, device=dev)
         self._front = None
@@ -355,7 +373,12 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
         sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
         sp.counters_ext = ws.diag.data_ptr()
-        native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        if TWO_PHASE_SCAN:
+            native.call("skm_pruned_scan2", C.byref(sp), ptr(cents.tails_blk), ptr(ws.scan_scratch),
+                        ws.scan_scratch.numel() * 4, st, tag="pruned_scan",
+                        nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        else:
+            native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
         if ws.cap < k:
             # rows whose candidate list overflowed the slab: dense distance rows, same kernel
             over = torch.nonzero(ws.cand_cnt[:bn] > ws.cap).flatten()
@@ -480,6 +503,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
     have_order = False
     scan_blocks: list[int] = []
     scan_waves: list[int] = []
+    scan_diag: list[list[int]] = []
 
     for it in range(1, cfg.max_iters + 1):
         pruned_iter = pruned_mode and it > 1
@@ -517,8 +541,10 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         if it > 1:
             n_changed = int(round(ch))
         if pruned_iter:
-            scan_blocks.append(int(ws.diag[0].item()))
-            scan_waves.append(int(ws.diag[1].item()))
+            dg = ws.diag.tolist()
+            scan_blocks.append(int(dg[0] + dg[2]))
+            scan_waves.append(int(dg[1] + dg[3]))
+            scan_diag.append([int(v) for v in dg[:6]])
             survivors, touched = int(round(sv)), int(round(td))
             prune_rate = prune_rate_from_totals(survivors, n, k)
             work.tail_dims += touched
@@ -579,4 +605,5 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         assign_dev=ws.assign[:n_local],
         scan_blocks=scan_blocks,
         scan_waves=scan_waves,
+        scan_diag=scan_diag,
     )

@@ -89,6 +89,9 @@ _SIGS = {
     "skm_build_tails": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
     "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp], _i),
     "skm_pruned_scan": ([C.POINTER(ScanParams), _vp], _i),
+    "skm_build_tails_blk": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
+    "skm_scan2_scratch_bytes": ([_i, _i], _ll),
+    "skm_pruned_scan2": ([C.POINTER(ScanParams), _vp, _vp, _ll, _vp], _i),
     "skm_topk_rows": ([_vp, _ll, _i, _i, _i, _vp, _vp, _ll, _i, _vp], _i),
     "skm_topk_merge": ([_vp, _vp, _i, _i, _i, _vp, _vp, _vp], _i),
     "skm_etr_hits": ([_vp, _i, _i, _vp, _i, _i, _vp, _ll, _ll, _i, _i, _vp, _vp], _i),

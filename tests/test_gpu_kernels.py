@@ -200,12 +200,21 @@ def test_portable_matmul_bitwise():
     assert np.array_equal(out.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("seed,n,k,d,dp,sentinel", [
+SCAN_CASES = [
     (0, 123, 77, 200, 25, False), (1, 123, 77, 200, 25, True), (2, 600, 900, 256, 32, False),
-    (3, 400, 1500, 1536, 192, False), (4, 300, 64, 96, 16, False), (5, 257, 300, 130, 40, True)])
-def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel):
-    """Production scan (candidate lists + speculative waves + in-order resolve) equals the
-    sequential reference scan over all centroids, including survivor/dims counters."""
+    (3, 400, 1500, 1536, 192, False), (4, 300, 64, 96, 16, False), (5, 257, 300, 130, 40, True)]
+
+
+@pytest.mark.parametrize("seed,n,k,d,dp,sentinel", SCAN_CASES)
+@pytest.mark.parametrize("two_phase,prev_mode", [(False, "random"), (True, "random"), (True, "nearest"),
+                                                 (True, "mixed")])
+def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, prev_mode):
+    """Production scan equals the sequential reference scan over all centroids, including the
+    survivor/dims counters: the one-phase exact kernel (candidate lists + speculative waves +
+    in-order resolve) and the two-phase scan (speculative pair scan for rows whose tau can only
+    change at their previous centroid + exact kernel on the rest).  ``prev_mode`` picks the
+    previous assignment: random (most rows re-assign), the nearest centroid (steady state: the
+    speculative phase owns almost every row) or 90% nearest."""
     from oracle import kernels_np as O
     from paper_2603_20009_b200 import native
     from paper_2603_20009_b200.config import pdxify, tail_block_layout
@@ -217,6 +226,10 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel):
     c = np.ascontiguousarray(c[:k], dtype=np.float32)
     k = c.shape[0]
     prev = rng.integers(0, k, n).astype(np.int32)
+    if prev_mode != "random":
+        d2 = ((x.astype(np.float64)[:, None, :] - c.astype(np.float64)[None, :, :]) ** 2).sum(-1)
+        near = d2.argmin(1).astype(np.int32)
+        prev = near if prev_mode == "nearest" else np.where(rng.random(n) < 0.9, near, prev).astype(np.int32)
     X, Cm = _pad(x), _pad(c)
     xh, xl = dev.split_hilo(X, dp)
     ch, cl = dev.split_hilo(Cm, dp)
@@ -271,7 +284,22 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel):
     work = torch.zeros(256, dtype=torch.int32, device="cuda")
     p.work = work.data_ptr()
     import ctypes
-    native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
+    if two_phase:
+        tails_blk = torch.empty(k * 64 * nb, dtype=torch.float32, device="cuda")
+        native.call("skm_build_tails_blk", dev.ptr(Cm), Cm.stride(0), k, d, dp, dev.ptr(tails_blk),
+                    dev.stream_handle())
+        nbytes = int(native.load().skm_scan2_scratch_bytes(n, cap))
+        scratch = torch.empty((nbytes + 3) // 4, dtype=torch.int32, device="cuda")
+        diag = torch.zeros(8, dtype=torch.int64, device="cuda")
+        p.counters_ext = diag.data_ptr()
+        native.check(native.load().skm_pruned_scan2(ctypes.byref(p), dev.ptr(tails_blk), dev.ptr(scratch), nbytes,
+                                                    dev.stream_handle()), "scan2")
+        p.counters_ext = None
+        if prev_mode == "nearest" and not sentinel:
+            # steady state: round 0 of the speculative scan finishes most rows itself
+            assert int(diag[5].item()) < n // 2
+    else:
+        native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
     # overflow rows -> dense pass over their full distance rows
     over = torch.nonzero(cc > cap).flatten().to(torch.int32)
     if over.numel():

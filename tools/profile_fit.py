@@ -38,4 +38,8 @@ st = r.loop.stats
 print("d'", [s.d_prime for s in st], "surv/vec", [round(s.survivors / a.n, 1) for s in st],
       "tail/vec", [round(s.tail_dims_touched / a.n) for s in st],
       "computed blocks/vec", [round(b / a.n) for b in r.loop.scan_blocks],
-      "waves/vec", [round(w / a.n, 1) for w in r.loop.scan_waves], "phase", {k: round(v * 1e3, 1) for k, v in r.phase.items()})
+      "waves/vec", [round(w / a.n, 1) for w in r.loop.scan_waves],
+      "n_changed", [s.n_changed for s in st], "exact-fallback rows", [dg[4] for dg in r.loop.scan_diag],
+      "round>=1 rows", [dg[5] for dg in r.loop.scan_diag],
+      "spec blocks/vec", [round(dg[0] / a.n) for dg in r.loop.scan_diag],
+      "spec lane util", [round(dg[0] / max(1, 32 * dg[1]), 3) for dg in r.loop.scan_diag], "phase", {k: round(v * 1e3, 1) for k, v in r.phase.items()})
