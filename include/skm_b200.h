@@ -48,6 +48,11 @@ int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* o
 /* out[r,:cols] = in[idx[r],:cols] */
 int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
                     long long ldo, void* stream);
+/* Gate-batch gather: ohi/olo[r, :cols] = hi/lo[idx[r], :cols], oxsq[r] = xsq[idx[r]],
+ * othr[r] = thr[idx[r]] (rows in cluster order for the gate GEMM). */
+int skm_gather_front(const float* hi, const float* lo, long long ldi, const int* idx, int rows, int cols, float* ohi,
+                     float* olo, long long ldo, const float* xsq, const float* thr, float* oxsq, float* othr,
+                     void* stream);
 int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
                         long long ldo, void* stream);
 int skm_fill_f32(float* p, long long n, float v, void* stream);

@@ -26,6 +26,68 @@ __global__ void split_hilo_kernel(const float* __restrict__ x, long long ldx, in
   }
 }
 
+// Vectorised split (16-byte aligned rows, ld multiple of 4): 2-D grid, x over float4 columns,
+// y strides over rows -- no per-element integer division.
+__global__ void split_hilo_vec_kernel(const float4* __restrict__ x, long long ldx4, int rows, int cols,
+                                      float4* __restrict__ hi, float4* __restrict__ lo, long long ldo4) {
+  const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c4 >= ldo4) return;
+  for (long long r = blockIdx.y; r < rows; r += gridDim.y) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * c4 < cols) v = x[r * ldx4 + c4];
+    if (4 * c4 + 3 >= cols) {  // ragged end: zero the padding columns
+      if (4 * c4 + 0 >= cols) v.x = 0.f;
+      if (4 * c4 + 1 >= cols) v.y = 0.f;
+      if (4 * c4 + 2 >= cols) v.z = 0.f;
+      if (4 * c4 + 3 >= cols) v.w = 0.f;
+    }
+    float4 h;
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    hi[r * ldo4 + c4] = h;
+    lo[r * ldo4 + c4] = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z), __fsub_rn(v.w, h.w));
+  }
+}
+
+// Gate batch gather, one warp per output row: front columns [0, cols) of hi and lo (float4
+// when both strides are multiples of 4), plus the row's norm term and gate threshold.
+__global__ void gather_front_kernel(const float* __restrict__ hi, const float* __restrict__ lo, long long ldi,
+                                    const int* __restrict__ idx, int rows, int cols, float* __restrict__ ohi,
+                                    float* __restrict__ olo, long long ldo, const float* __restrict__ xsq,
+                                    const float* __restrict__ thr, float* __restrict__ oxsq, float* __restrict__ othr) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const bool vec = ((ldi & 3) == 0) && ((ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(hi) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(lo) & 15) == 0) && ((reinterpret_cast<uintptr_t>(ohi) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(olo) & 15) == 0);
+  for (long long r = blockIdx.x * (long long)wpb + (threadIdx.x >> 5); r < rows; r += (long long)gridDim.x * wpb) {
+    const long long src = idx[r];
+    const float* sh = hi + src * ldi;
+    const float* sl = lo + src * ldi;
+    float* dh = ohi + r * ldo;
+    float* dl = olo + r * ldo;
+    int c0 = 0;
+    if (vec) {
+      const int c4n = cols >> 2;
+      for (int c = lane; c < c4n; c += 32) {
+        reinterpret_cast<float4*>(dh)[c] = __ldg(reinterpret_cast<const float4*>(sh) + c);
+        reinterpret_cast<float4*>(dl)[c] = __ldg(reinterpret_cast<const float4*>(sl) + c);
+      }
+      c0 = c4n << 2;
+    }
+    for (int c = c0 + lane; c < cols; c += 32) {
+      dh[c] = sh[c];
+      dl[c] = sl[c];
+    }
+    if (lane == 0) {
+      oxsq[r] = xsq[src];
+      othr[r] = thr[src];
+    }
+  }
+}
+
 // Squared row norms over the leading `dims` columns, double accumulation rounded to
 // fp32 (preprocess.py:95-101).  One warp per row.
 __global__ void row_sq_norms_kernel(const float* __restrict__ x, long long ldx, int rows, int dims,

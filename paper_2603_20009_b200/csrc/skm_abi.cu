@@ -135,6 +135,16 @@ int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi,
                    void* stream) {
   if (rows <= 0) return SKM_OK;
   if (cols > ldo) return fail(SKM_E_ARG, "split_hilo: cols > ldo");
+  if ((ldx & 3) == 0 && (ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(hi) & 15) == 0 && (reinterpret_cast<uintptr_t>(lo) & 15) == 0) {
+    const long long ldo4 = ldo / 4;
+    dim3 grid(static_cast<unsigned>((ldo4 + 127) / 128), static_cast<unsigned>(std::min(rows, 16384)));
+    skm::split_hilo_vec_kernel<<<grid, 128, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(x), ldx / 4, rows,
+                                                                     cols, reinterpret_cast<float4*>(hi),
+                                                                     reinterpret_cast<float4*>(lo), ldo4);
+    SKM_LAUNCH_CHECK("split_hilo");
+    return SKM_OK;
+  }
   skm::split_hilo_kernel<<<grid_for((long long)rows * ldo, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, hi,
                                                                                              lo, ldo);
   SKM_LAUNCH_CHECK("split_hilo");
@@ -155,6 +165,17 @@ int skm_gather_rows(const float* in, long long ldi, const long long* idx, int ro
   skm::gather_rows_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
                                                                                               cols, out, ldo);
   SKM_LAUNCH_CHECK("gather_rows");
+  return SKM_OK;
+}
+
+int skm_gather_front(const float* hi, const float* lo, long long ldi, const int* idx, int rows, int cols, float* ohi,
+                     float* olo, long long ldo, const float* xsq, const float* thr, float* oxsq, float* othr,
+                     void* stream) {
+  if (rows <= 0) return SKM_OK;
+  if (cols > ldo || cols > ldi) return fail(SKM_E_ARG, "gather_front: cols exceeds a stride");
+  skm::gather_front_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(
+      hi, lo, ldi, idx, rows, cols, ohi, olo, ldo, xsq, thr, oxsq, othr);
+  SKM_LAUNCH_CHECK("gather_front");
   return SKM_OK;
 }
 

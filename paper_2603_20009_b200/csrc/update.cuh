@@ -127,16 +127,13 @@ __global__ void __launch_bounds__(SUM_THREADS)
   double s = accumulate_sums ? sums_io[static_cast<long long>(c) * d + col] : 0.0;
   const int* ord = order + beg;
   int m = 0;
-  for (; m + 4 <= cnt; m += 4) {
-    const int i0 = ord[m], i1 = ord[m + 1], i2 = ord[m + 2], i3 = ord[m + 3];
-    const float v0 = x[static_cast<long long>(i0) * ldx + col];
-    const float v1 = x[static_cast<long long>(i1) * ldx + col];
-    const float v2 = x[static_cast<long long>(i2) * ldx + col];
-    const float v3 = x[static_cast<long long>(i3) * ldx + col];
-    s = __dadd_rn(s, static_cast<double>(v0));
-    s = __dadd_rn(s, static_cast<double>(v1));
-    s = __dadd_rn(s, static_cast<double>(v2));
-    s = __dadd_rn(s, static_cast<double>(v3));
+  // 8 member rows in flight per thread (the f64 chain itself stays in member order)
+  for (; m + 8 <= cnt; m += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(x + static_cast<long long>(__ldg(ord + m + u)) * ldx + col);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, static_cast<double>(v[u]));
   }
   for (; m < cnt; ++m) s = __dadd_rn(s, static_cast<double>(x[static_cast<long long>(ord[m]) * ldx + col]));
   if (mode == 1) {

@@ -348,14 +348,9 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         if ordered:
             rmap = order[b0:b0 + bn]
             # the front buffers may be wider than fld (allocated at a larger d'): use their stride
-            native.call("skm_gather_rows_i32", ptr(data.hi), data.ld, ptr(rmap), bn, dp, ptr(ga_hi),
-                        ga_hi.stride(0), st, nbytes=8.0 * bn * dp)
-            native.call("skm_gather_rows_i32", ptr(data.lo), data.ld, ptr(rmap), bn, dp, ptr(ga_lo),
-                        ga_lo.stride(0), st, nbytes=8.0 * bn * dp)
-            native.call("skm_gather_rows_i32", ptr(xsq.view(-1, 1)), 1, ptr(rmap), bn, 1, ptr(ws.bx.view(-1, 1)), 1,
-                        st)
-            native.call("skm_gather_rows_i32", ptr(ws.thr.view(-1, 1)), 1, ptr(rmap), bn, 1,
-                        ptr(ws.bthr.view(-1, 1)), 1, st)
+            native.call("skm_gather_front", ptr(data.hi), ptr(data.lo), data.ld, ptr(rmap), bn, dp, ptr(ga_hi),
+                        ptr(ga_lo), ga_hi.stride(0), ptr(xsq), ptr(ws.thr), ptr(ws.bx), ptr(ws.bthr), st,
+                        nbytes=16.0 * bn * dp + 16.0 * bn)
             _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
                   ysq=cents.ysq, thr=ws.bthr[:bn], cand_idx=ws.cand_idx, cand_val=ws.cand_val, cand_cnt=ws.cand_cnt,
                   cand_cap=ws.cap)
