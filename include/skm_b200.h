@@ -157,6 +157,11 @@ int skm_topk_merge(const int* in_idx, const float* in_val, int shards, int k, in
 int skm_etr_hits(const int* gt, int gt_ld, int top_k, const int* probe, int probe_ld, int nprobe, const int* assign,
                  long long row_lo, long long row_hi, int k, int nq, int* hits, void* stream);
 
+/* probe_eval tally (evaluation.py:173-203): hits[q] as skm_etr_hits over rows 0..n-1
+ * (assign[g] < 0: row in no cluster list) and explored[q] += sum_{c in probe[q]} sizes[c]. */
+int skm_probe_tally(const int* gt, int gt_ld, int top_k, const int* probe, int probe_ld, int nprobe, const int* assign,
+                    long long n, int k, int nq, const int* sizes, int* hits, long long* explored, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

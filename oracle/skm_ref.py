@@ -11,6 +11,7 @@ arithmetic exactly given the same GEMM (NumPy/OpenBLAS sgemm):
   update/split/adjust  core.py:79-154
   final_assign         core.py:463-541
   ETR                  evaluation.py:53-75, 116-170
+  IVF probe evaluation evaluation.py:78-105, 173-203
   hierarchical_fit     hierarchical.py:91-171
 
 It is pinned against the real reference (tests/test_oracle_*.py compare it with the imported
@@ -246,6 +247,49 @@ def etr_hits(c, xr, assign, q, gt_idx, nprobe, top_k):
             top = cand[np.lexsort((cand, d2))[:take]]
             hits[s + qi] = int(np.isin(top, gt_idx[s + qi, :top_k], assume_unique=True).sum())
     return hits
+
+
+def cluster_lists(assign, k):
+    """build_cluster_lists (evaluation.py:78-83)."""
+    order = np.argsort(assign, kind="stable")
+    return np.split(order, np.cumsum(np.bincount(assign, minlength=k))[:-1])
+
+
+def ivf_probe_search(c, lists, x, q, nprobe, top_k):
+    """evaluation.py:86-105."""
+    nprobe = min(nprobe, c.shape[0])
+    q2 = q.reshape(1, -1).astype(np.float32)
+    probe = np.argsort(expand(q2 @ c.T, sq_norms(q2), sq_norms(c))[0], kind="stable")[:nprobe]
+    cand = np.concatenate([lists[j] for j in probe])
+    if cand.size == 0:
+        return np.empty(0, np.int64), np.empty(0, np.float32), 0
+    d2 = expand(q2 @ x[cand].T, sq_norms(q2), sq_norms(x[cand]))[0]
+    o = np.lexsort((cand, d2))[:top_k]
+    return cand[o].astype(np.int64), d2[o], int(cand.size)
+
+
+def probe_eval(c, lists, x, q, gt_idx, k_gt, nprobe, top_ks=(10, 100)):
+    """evaluation.py:173-203: recall@t per t <= k_gt and mean vectors explored."""
+    nprobe = min(max(1, nprobe), c.shape[0])
+    top_ks = sorted({t for t in top_ks if t <= k_gt})
+    cs, xs = sq_norms(c), sq_norms(x)
+    nq = q.shape[0]
+    rec = {t: 0.0 for t in top_ks}
+    explored = 0
+    for s in range(0, nq, 256):
+        e = min(nq, s + 256)
+        probe = np.argsort(expand(q[s:e] @ c.T, sq_norms(q[s:e]), cs), axis=1, kind="stable")[:, :nprobe]
+        for qi in range(e - s):
+            cand = np.concatenate([lists[j] for j in probe[qi]])
+            explored += cand.size
+            d2 = expand(q[s + qi:s + qi + 1] @ x[cand].T, sq_norms(q[s + qi:s + qi + 1]), xs[cand])[0]
+            found = cand[np.lexsort((cand, d2))]
+            for t in top_ks:
+                take = min(t, found.size)
+                rec[t] += int(np.isin(found[:take], gt_idx[s + qi, :t], assume_unique=True).sum()) / t
+    out = {f"recall_at_{t}": rec[t] / nq for t in top_ks}
+    out["vectors_explored_mean"] = explored / nq
+    return out
 
 
 def recall_from_hits(hits, top_k):

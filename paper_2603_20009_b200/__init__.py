@@ -66,7 +66,8 @@ def __getattr__(name):
     if name in ("hierarchical_fit", "HierarchicalConfig", "reconcile_k"):
         from . import hierarchical
         return getattr(hierarchical, name)
-    if name in ("brute_force_topk", "etr_probe", "build_cluster_lists", "GroundTruth", "RecallHistory"):
+    if name in ("brute_force_topk", "etr_probe", "build_cluster_lists", "GroundTruth", "RecallHistory",
+                "probe_eval", "ivf_probe_search", "recall_at_k"):
         from . import etr
         return getattr(etr, name)
     if name in ("apply_rotation", "unapply_rotation", "sample_training_set", "init_centroids", "compute_norms",

@@ -668,4 +668,22 @@ int skm_etr_hits(const int* gt, int gt_ld, int top_k, const int* probe, int prob
   return SKM_OK;
 }
 
+// probe_eval tally (evaluation.py:173-203): hits[q] = #{g in gt[q][:top_k] : assign[g] in
+// probe[q][:nprobe]} and explored[q] += sum of sizes[c] over the probed clusters.
+int skm_probe_tally(const int* gt, int gt_ld, int top_k, const int* probe, int probe_ld, int nprobe, const int* assign,
+                    long long n, int k, int nq, const int* sizes, int* hits, long long* explored, void* stream) {
+  if (nq <= 0) return SKM_OK;
+  const size_t smem = sizeof(unsigned) * ((k + 31) / 32);
+  if (smem > 200 * 1024) return fail(SKM_E_ARG, "probe_tally: k too large for the shared bitmap");
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(skm::etr_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    set = true;
+  }
+  skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, 0, n,
+                                                             k, hits, sizes, explored);
+  SKM_LAUNCH_CHECK("probe_tally");
+  return SKM_OK;
+}
+
 }  // extern "C"

@@ -152,24 +152,33 @@ __global__ void topk_merge_kernel(const int* __restrict__ in_idx, const float* _
 // (the reference's per-query recall numerator, evaluation.py:163-169, as an integer tally).
 __global__ void etr_hits_kernel(const int* __restrict__ gt, int gt_ld, int top_k, const int* __restrict__ probe,
                                 int probe_ld, int nprobe, const int* __restrict__ assign, long long row_lo,
-                                long long row_hi, int k, int* __restrict__ hits) {
+                                long long row_hi, int k, int* __restrict__ hits,
+                                const int* __restrict__ sizes = nullptr, long long* __restrict__ explored = nullptr) {
   extern __shared__ unsigned bitmap[];
   const int q = blockIdx.x;
   const int words = (k + 31) / 32;
   for (int i = threadIdx.x; i < words; i += blockDim.x) bitmap[i] = 0;
   __syncthreads();
+  long long ex = 0;  // vectors in the probed clusters (probe_eval's vectors_explored)
   for (int i = threadIdx.x; i < nprobe; i += blockDim.x) {
     const int c = probe[static_cast<long long>(q) * probe_ld + i];
     atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+    if (sizes) ex += sizes[c];
   }
   __syncthreads();
   int h = 0;
   for (int i = threadIdx.x; i < top_k; i += blockDim.x) {
     const long long g = gt[static_cast<long long>(q) * gt_ld + i];
     if (g >= row_lo && g < row_hi) {
-      const int a = assign[g - row_lo];
-      h += (bitmap[a >> 5] >> (a & 31)) & 1u;
+      const int a = assign[g - row_lo];  // < 0: the row is in no cluster list
+      if (a >= 0 && a < k) h += (bitmap[a >> 5] >> (a & 31)) & 1u;
     }
+  }
+  if (explored) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
+    if ((threadIdx.x & 31) == 0 && ex) atomicAdd(reinterpret_cast<unsigned long long*>(explored + q),
+                                                 static_cast<unsigned long long>(ex));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);

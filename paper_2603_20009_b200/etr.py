@@ -218,3 +218,122 @@ def etr_probe(centroids, train_x, assignments, queries, gt: GroundTruth, nprobe:
     for v in hits.cpu().numpy():
         total += int(v) / top_k
     return total / q.shape[0]
+
+
+# ------------------------------------------------------------------ IVF probe evaluation
+def _lists_to_assign(cluster_lists, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """Invert cluster lists into a row -> cluster array (-1: in no list) and list sizes."""
+    assign = np.full(n, -1, dtype=np.int32)
+    sizes = np.empty(len(cluster_lists), dtype=np.int32)
+    for c, lst in enumerate(cluster_lists):
+        lst = np.asarray(lst, dtype=np.int64)
+        assign[lst] = c
+        sizes[c] = lst.size
+    return assign, sizes
+
+
+def _probe_ranking(centroids: np.ndarray, queries: np.ndarray, nprobe: int, dev) -> torch.Tensor:
+    """Top-nprobe centroids per query by squared L2, ties to the lower index (the stable
+    argsort of evaluation.py:97,196): distance GEMM + exact device top-k."""
+    from .api import _h2d
+    k, d = centroids.shape
+    Cd, Qd = _h2d(np.ascontiguousarray(centroids, dtype=np.float32), dev), _h2d(
+        np.ascontiguousarray(queries, dtype=np.float32), dev)
+    ch, cl = _split(Cd, d)
+    qh, ql = _split(Qd, d)
+    pi, _ = device_topk_distances(Qd, qh, ql, _norms(Qd, d), Cd, ch, cl, _norms(Cd, d), d, nprobe)
+    return pi
+
+
+def probe_eval(centroids, cluster_lists, x, queries, gt: GroundTruth, nprobe: int, top_ks=(10, 100),
+               device=None) -> dict:
+    """IVF probe-search quality (evaluation.py:173-203): recall@t for each t <= gt.k_gt and the
+    mean number of vectors scanned per query, on the B200.
+
+    A query's candidates are the members of its nprobe nearest clusters.  Its top-t by
+    (distance, index) among them contains exactly the ground-truth members GT[:t] that are
+    candidates (every row closer than such a member is itself in GT[:t]), so recall@t is the
+    integer tally #{g in GT[:t] : cluster(g) in probe} / t -- the reference's value up to
+    distance near-ties between its two GEMM calls.  Sums run in query order in
+    f64 like the reference."""
+    from .config import DimensionMismatch
+    dev = require_cuda(device)
+    c = np.ascontiguousarray(centroids, dtype=np.float32)
+    q = np.ascontiguousarray(queries, dtype=np.float32)
+    n = np.asarray(x).shape[0]
+    if np.asarray(x).shape[1] != q.shape[1] or c.shape[1] != q.shape[1]:
+        raise DimensionMismatch("dim mismatch between vectors, centroids and queries")
+    k = c.shape[0]
+    nprobe = min(max(1, nprobe), k)
+    top_ks = sorted({t for t in top_ks if t <= gt.k_gt})
+    nq = q.shape[0]
+    assign, sizes = _lists_to_assign(cluster_lists, n)
+    pi = _probe_ranking(c, q, nprobe, dev)
+    A = torch.from_numpy(assign).to(dev)
+    S = torch.from_numpy(sizes).to(dev)
+    gt_i = torch.from_numpy(np.ascontiguousarray(gt.indices, dtype=np.int32)).to(dev)
+    explored = torch.zeros(max(nq, 1), dtype=torch.int64, device=dev)
+    out = {}
+    hits_by_t = {}
+    for n_t, t in enumerate(top_ks):
+        hits = torch.zeros(max(nq, 1), dtype=torch.int32, device=dev)
+        native.call("skm_probe_tally", ptr(gt_i), gt_i.shape[1], t, ptr(pi), pi.shape[1], nprobe, ptr(A), n, k, nq,
+                    ptr(S) if n_t == 0 else None, ptr(hits), ptr(explored) if n_t == 0 else None, stream_handle())
+        hits_by_t[t] = hits[:nq].cpu().numpy()
+    if not top_ks:  # still count the explored vectors
+        hits = torch.zeros(max(nq, 1), dtype=torch.int32, device=dev)
+        native.call("skm_probe_tally", ptr(gt_i), gt_i.shape[1], 0, ptr(pi), pi.shape[1], nprobe, ptr(A), n, k, nq,
+                    ptr(S), ptr(hits), ptr(explored), stream_handle())
+    for t in top_ks:
+        total = 0.0
+        for v in hits_by_t[t]:
+            total += int(v) / t
+        out[f"recall_at_{t}"] = total / nq
+    out["vectors_explored_mean"] = int(explored[:nq].sum().item()) / nq
+    return out
+
+
+def ivf_probe_search(centroids, cluster_lists, x, q, nprobe: int, top_k: int, device=None):
+    """Scan the nprobe clusters nearest to one query (evaluation.py:86-105).  Returns
+    (indices int64, squared distances float32, vectors_explored); ties resolve to the lower
+    row index.  Probe ranking, candidate distances (3xTF32 GEMM, the reference's expansion
+    op order) and the top-k run on the B200."""
+    dev = require_cuda(device)
+    from .api import _h2d
+    from .engine import _gemm
+    c = np.ascontiguousarray(centroids, dtype=np.float32)
+    k = c.shape[0]
+    nprobe = min(nprobe, k)
+    q2 = np.ascontiguousarray(np.asarray(q, dtype=np.float32).reshape(1, -1))
+    probe = _probe_ranking(c, q2, max(nprobe, 1), dev)[0, :nprobe].cpu().numpy()
+    cand = np.concatenate([np.asarray(cluster_lists[int(p)], dtype=np.int64) for p in probe])
+    if cand.size == 0:
+        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float32), 0
+    take = min(top_k, cand.size)
+    if take > 2048:
+        raise NotImplementedError("ivf_probe_search: top_k > 2048 is not supported by the device top-k")
+    # candidates in ascending row order: column ties in the device top-k then resolve to the
+    # lower row index, as the reference's lexsort((cand, d2)) does
+    srt = np.sort(cand)
+    xs = np.ascontiguousarray(np.asarray(x, dtype=np.float32)[srt])
+    d = xs.shape[1]
+    X = _h2d(xs, dev)
+    Q = _h2d(q2, dev)
+    xh, xl = _split(X, d)
+    qh, ql = _split(Q, d)
+    m = X.shape[0]
+    D = torch.empty((1, padded_ld(m)), dtype=torch.float32, device=dev)
+    _gemm(qh, ql, xh, xl, 1, m, d, native.GEMM_DIST, out=D, xsq=_norms(Q, d), ysq=_norms(X, d))
+    oi = torch.empty((1, take), dtype=torch.int32, device=dev)
+    ov = torch.empty((1, take), dtype=torch.float32, device=dev)
+    native.call("skm_topk_rows", ptr(D), D.stride(0), 1, m, take, ptr(oi), ptr(ov), take, 0, stream_handle())
+    cols = oi[0].cpu().numpy().astype(np.int64)
+    return srt[cols], ov[0].cpu().numpy(), int(cand.size)
+
+
+def recall_at_k(result_ids, gt_row, k: int) -> float:
+    """|result[:k] & gt[:k]| / k (evaluation.py:108-113)."""
+    result_ids, gt_row = np.asarray(result_ids), np.asarray(gt_row)
+    if len(result_ids) < k or len(gt_row) < k:
+        raise ValueError(f"need at least {k} entries on both sides")
+    return np.intersect1d(result_ids[:k], gt_row[:k]).size / k

@@ -96,6 +96,7 @@ _SIGS = {
     "skm_topk_rows": ([_vp, _ll, _i, _i, _i, _vp, _vp, _ll, _i, _vp], _i),
     "skm_topk_merge": ([_vp, _vp, _i, _i, _i, _vp, _vp, _vp], _i),
     "skm_etr_hits": ([_vp, _i, _i, _vp, _i, _i, _vp, _ll, _ll, _i, _i, _vp, _vp], _i),
+    "skm_probe_tally": ([_vp, _i, _i, _vp, _i, _i, _vp, _ll, _i, _i, _vp, _vp, _vp, _vp], _i),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

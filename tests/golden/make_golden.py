@@ -157,7 +157,44 @@ def hostmath():
     return out
 
 
+def probes():
+    """IVF probe evaluation (evaluation.py:86-105, 173-203) on a reference fit: inputs are
+    regenerated from seeds by the tests; centroids, lists, GT and outputs are stored."""
+    from superkmeans.evaluation import build_cluster_lists, ivf_probe_search, probe_eval
+    out = {}
+    for case, (n, d, centers, k, seed) in enumerate([(12000, 48, 40, 64, 3), (6000, 130, 25, 37, 4)]):
+        x = make_blobs(n, d, centers, seed=seed)
+        res = skm.fit(x, skm.KMeansConfig(k=k, max_iters=6, seed=seed))
+        rng = np.random.default_rng([seed, 99])
+        q_idx = rng.choice(n, size=150, replace=False)
+        queries = (x[q_idx] + rng.standard_normal((150, d)).astype(np.float32) * 0.3).astype(np.float32)
+        gt = skm.brute_force_topk(x, queries, 100)
+        lists = build_cluster_lists(res.assignments, k)
+        key = f"p{case}"
+        out[key + "_centroids"] = res.centroids
+        out[key + "_assign"] = res.assignments
+        out[key + "_q_idx"] = q_idx
+        out[key + "_queries"] = queries
+        out[key + "_gt_idx"] = gt.indices
+        out[key + "_gt_dist"] = gt.distances
+        for nprobe in (1, 3, 8):
+            r = probe_eval(res.centroids, lists, x, queries, gt, nprobe, top_ks=(10, 100))
+            out[f"{key}_np{nprobe}_r10"] = np.float64(r["recall_at_10"])
+            out[f"{key}_np{nprobe}_r100"] = np.float64(r["recall_at_100"])
+            out[f"{key}_np{nprobe}_explored"] = np.float64(r["vectors_explored_mean"])
+        for qi in range(5):
+            ids, dist, ex = ivf_probe_search(res.centroids, lists, x, queries[qi], 3, 20)
+            out[f"{key}_s{qi}_ids"] = ids
+            out[f"{key}_s{qi}_dist"] = dist
+            out[f"{key}_s{qi}_ex"] = np.int64(ex)
+    return out
+
+
 def main():
+    if "--only-probes" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "probes.npz"), **probes())
+        return
+    np.savez_compressed(os.path.join(HERE, "probes.npz"), **probes())
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels())
     np.savez_compressed(os.path.join(HERE, "hostmath.npz"), **hostmath())
     np.savez_compressed(os.path.join(HERE, "fits.npz"), **fits())

@@ -135,3 +135,30 @@ def test_c_oracle_kernels_bitwise_equal_numpy_oracle():
     counts = np.zeros(12, np.int64)
     kernels_c.accumulate_centroid_sums(K["acc_x"], K["acc_a"], sums, counts)
     assert np.array_equal(sums, K["acc_sums"]) and np.array_equal(counts, K["acc_counts"])
+
+
+PROBE_CASES = [(0, 12000, 48, 40, 64, 3), (1, 6000, 130, 25, 37, 4)]
+
+
+@pytest.mark.parametrize("case,n,d,centers,k,seed", PROBE_CASES)
+def test_oracle_probe_eval_matches_reference(case, n, d, centers, k, seed):
+    """Oracle IVF probe evaluation == the reference's probe_eval / ivf_probe_search outputs
+    (golden fixture), bitwise on this container's OpenBLAS."""
+    P = np.load(os.path.join(HERE, "golden", "probes.npz"))
+    key = f"p{case}"
+    x = make_blobs(n, d, centers, seed=seed)
+    lists = skm_ref.cluster_lists(P[key + "_assign"], k)
+    for nprobe in (1, 3, 8):
+        r = skm_ref.probe_eval(P[key + "_centroids"], lists, x, P[key + "_queries"], P[key + "_gt_idx"], 100, nprobe)
+        assert r["recall_at_10"] == float(P[f"{key}_np{nprobe}_r10"])
+        assert r["recall_at_100"] == float(P[f"{key}_np{nprobe}_r100"])
+        assert r["vectors_explored_mean"] == float(P[f"{key}_np{nprobe}_explored"])
+    for qi in range(5):
+        ids, dist, ex = skm_ref.ivf_probe_search(P[key + "_centroids"], lists, x, P[key + "_queries"][qi], 3, 20)
+        assert np.array_equal(ids, P[f"{key}_s{qi}_ids"])
+        assert np.array_equal(dist, P[f"{key}_s{qi}_dist"])
+        assert ex == int(P[f"{key}_s{qi}_ex"])
+    # the tally formulation used on the device gives the same recall here
+    hits = skm_ref.etr_hits(P[key + "_centroids"], x, P[key + "_assign"], P[key + "_queries"],
+                            P[key + "_gt_idx"], 3, 10)
+    assert skm_ref.recall_from_hits(hits, 10) == float(P[f"{key}_np3_r10"])

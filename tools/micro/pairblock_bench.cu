@@ -26,6 +26,26 @@ __device__ __forceinline__ float chain(const float4* xq, int nb, const float4 (&
   return acc;
 }
 
+// G rows share each candidate block: one cooperative load, G independent chains per lane
+template <int G>
+__device__ __forceinline__ void chains(const float* xs, int nb, int slotf, int b, const float4* cq, float (&acc)[G]) {
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float4 cv = cq[q];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4 xv = reinterpret_cast<const float4*>(xs + g * slotf)[q * nb + b];
+      const float2 d01 = __fadd2_rn(make_float2(xv.x, xv.y), make_float2(-cv.x, -cv.y));
+      const float2 d23 = __fadd2_rn(make_float2(xv.z, xv.w), make_float2(-cv.z, -cv.w));
+      const float2 s01 = __fmul2_rn(d01, d01), s23 = __fmul2_rn(d23, d23);
+      acc[g] = __fadd_rn(acc[g], s01.x); acc[g] = __fadd_rn(acc[g], s01.y);
+      acc[g] = __fadd_rn(acc[g], s23.x); acc[g] = __fadd_rn(acc[g], s23.y);
+    }
+  }
+}
+
 template <int MODE>
 __global__ void bench(const float4* __restrict__ tails, int nblk, int nb, int iters, float* out) {
   extern __shared__ __align__(16) float sm[];
@@ -33,7 +53,7 @@ __global__ void bench(const float4* __restrict__ tails, int nblk, int nb, int it
   float* xs = sm + warp * (64 * nb);
   float4* stg = reinterpret_cast<float4*>(sm + nw * 64 * nb) + warp * (MODE == 1 ? 2 : 1) * 32 * 17;
   __shared__ uint64_t bars[32][2][32];
-  for (int i = lane; i < 64 * nb; i += 32) xs[i] = 0.001f * i;
+  for (int i = lane; i < 64 * nb * ((MODE == 6 || MODE == 8) ? 4 : (MODE == 5 || MODE == 7) ? 2 : 1); i += 32) (MODE >= 5 ? sm + warp * 64 * nb * ((MODE == 6 || MODE == 8) ? 4 : (MODE == 5 || MODE == 7) ? 2 : 1) : xs)[i] = 0.001f * i;
   if (MODE == 1) { mbar_init(&bars[warp][0][lane], 1); mbar_init(&bars[warp][1][lane], 1); fence_mbar_init(); }
   __syncthreads();
   const float4* xq = reinterpret_cast<const float4*>(xs);
@@ -73,6 +93,37 @@ __global__ void bench(const float4* __restrict__ tails, int nblk, int nb, int it
 #pragma unroll
       for (int q = 0; q < 16; ++q) c[q] = stg[(cur * 32 + lane) * 17 + q];
       tot += chain(xq + (blk % nb), nb, c);
+    }
+  } else if (MODE >= 5) {
+    constexpr int G = (MODE == 5 || MODE == 7) ? 2 : (MODE == 9 ? 1 : 4);
+    const int half = lane >> 4, part = lane & 15;
+    float* xg = sm + warp * (G * 64 * nb);
+    float4* st = reinterpret_cast<float4*>(sm + nw * G * 64 * nb) + warp * 32 * 17;
+    float4 v[16];
+    unsigned myblk = hsh(seed) % nblk;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const unsigned blk = __shfl_sync(0xffffffffu, myblk, 2 * i + half);
+      v[i] = __ldg(tails + (size_t)blk * 16 + part);
+    }
+    for (int it = 0; it < iters; ++it) {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) st[(2 * i + half) * 17 + part] = v[i];
+      __syncwarp();
+      const unsigned cur = myblk;
+      if (it + 1 < iters) {
+        myblk = hsh(seed + (it + 1) * 7919u) % nblk;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const unsigned blk = __shfl_sync(0xffffffffu, myblk, 2 * i + half);
+          v[i] = __ldg(tails + (size_t)blk * 16 + part);
+        }
+      }
+      float acc[G];
+      chains<G>(xg, nb, 64 * nb, (MODE >= 7 ? it : cur) % nb, st + lane * 17, acc);
+#pragma unroll
+      for (int g = 0; g < G; ++g) tot += acc[g];
     }
   } else if (MODE == 4) {
     const int half = lane >> 4, part = lane & 15;
@@ -133,11 +184,12 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int iters = 512;
-  for (int mode : {2, 4}) {
-    for (int warps : {4, 8, 12, 14}) {
-      const size_t smem = (size_t)warps * 64 * nb * 4 + (mode == 1 ? (size_t)warps * 2 * 32 * 17 * 16 : (mode == 2 || mode == 4) ? (size_t)warps * 32 * 17 * 16 : 0);
+  for (int mode : {9, 7, 8}) {
+    for (int warps : {4, 6, 8, 10, 12, 14}) {
+      const int G = (mode == 5 || mode == 7) ? 2 : (mode == 6 || mode == 8) ? 4 : 1;
+      const size_t smem = (size_t)warps * G * 64 * nb * 4 + (mode == 1 ? (size_t)warps * 2 * 32 * 17 * 16 : (mode == 2 || mode >= 4) ? (size_t)warps * 32 * 17 * 16 : 0);
       if (smem > 220 * 1024) continue;
-      void (*fn)(const float4*, int, int, int, float*) = mode == 0 ? bench<0> : mode == 1 ? bench<1> : mode == 2 ? bench<2> : mode == 3 ? bench<3> : bench<4>;
+      void (*fn)(const float4*, int, int, int, float*) = mode == 0 ? bench<0> : mode == 1 ? bench<1> : mode == 2 ? bench<2> : mode == 3 ? bench<3> : mode == 4 ? bench<4> : mode == 5 ? bench<5> : mode == 6 ? bench<6> : mode == 7 ? bench<7> : mode == 8 ? bench<8> : bench<9>;
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       fn<<<sms, warps * 32, smem>>>(tails, nblk, nb, iters, out);
       cudaEventRecord(e0);
@@ -145,7 +197,7 @@ int main() {
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
       cudaError_t err = cudaGetLastError();
-      const double pbs = (double)sms * warps * 32 * iters;
+      const double pbs = (double)sms * warps * 32 * iters * G;
       printf("mode %d warps/SM %2d: %.3f ms  %.2f Gpb/s  %.1f clk/pb/SM  %s\n", mode, warps, ms, pbs / ms / 1e6,
              (double)sms * 1.965e9 * ms * 1e-3 / pbs, cudaGetErrorString(err));
     }

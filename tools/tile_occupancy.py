@@ -44,6 +44,15 @@ for it, (cnt, idx, cap, k, dp) in enumerate(captured["it"], start=2):
     r, c = rows[valid], idx[valid].long()
     occ[r // 128, c // 256] = True
     uni[r // 128, c] = True
+    geff = []
+    for G in (2, 4, 8, 16):
+        ng = n // G
+        ug = torch.zeros(ng, k, dtype=torch.bool, device=dev)
+        rr = r // G
+        keep = rr < ng
+        ug[rr[keep], c[keep]] = True
+        geff.append(f"G{G}:{(cnt[:ng * G].clamp(max=cap).sum() / ug.sum()).item():.2f}")
+    print(f"iter {it} sharing (pairs per union column) " + " ".join(geff))
     print(f"iter {it} d'={dp}: surv/row {cnt.float().mean():.1f}  alive N-tiles per M-tile "
           f"{occ.float().sum(1).mean():.2f}/{nt} ({100 * occ.float().mean():.1f}%)  union cols per M-tile "
           f"{uni.float().sum(1).mean():.0f}/{k}")
