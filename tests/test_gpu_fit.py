@@ -103,6 +103,17 @@ def test_fit_matches_reference_trajectory(name):
         np.testing.assert_allclose([s.wcss for s in st], g[f"{name}_wcss"], rtol=1e-4)
     fa = skb.final_assign(x, res, cfg)
     assert float(np.mean(fa == g[f"{name}_final"])) >= 0.999
+    # north star: final IVF recall@10 within 0.5 points of the reference's clustering
+    from oracle import skm_ref
+    xt = x if res.sample_indices is None else x[res.sample_indices]
+    q = xt[np.random.default_rng(7).choice(xt.shape[0], 200, replace=False)]
+    gi, gd = skm_ref.brute_force_topk(xt, q, 10)
+    nprobe = max(1, int(np.ceil(0.05 * cfg.k)))
+    ours = skb.probe_eval(res.centroids, skb.build_cluster_lists(res.assignments, cfg.k), xt, q,
+                          skb.GroundTruth(indices=gi, distances=gd, k_gt=10), nprobe, top_ks=(10,))
+    ref = skm_ref.probe_eval(g[f"{name}_centroids"], skm_ref.cluster_lists(g[f"{name}_assign"], cfg.k), xt, q, gi, 10,
+                             nprobe, top_ks=(10,))
+    assert abs(ours["recall_at_10"] - ref["recall_at_10"]) <= 0.005, (ours, ref)
 
 
 def test_fit_c1_shape_vs_oracle():
