@@ -35,7 +35,7 @@ namespace skm {
 #define SKM_SCAN_WARPS 4
 #endif
 #ifndef SKM_SCAN_WINDOW
-#define SKM_SCAN_WINDOW 48
+#define SKM_SCAN_WINDOW 64
 #endif
 constexpr int SCAN_DEPTH = SKM_SCAN_DEPTH;     // consecutive blocks per candidate per wave
 constexpr int SCAN_SLOTS = 32 / SCAN_DEPTH;    // candidates in flight per wave
@@ -111,6 +111,7 @@ struct ScanWarpSmem {
   int qpb[SCAN_WINDOW];
   float qrun[SCAN_WINDOW];
   int qver[SCAN_WINDOW];    // tau version the outcome was decided under
+  int sel[32];              // dispatch: lane of the r-th taken position
 };
 
 // (a - b)^2 for two lanes with sm_100 packed fp32 ops: sub.rn.f32x2 / mul.rn.f32x2.
@@ -268,7 +269,10 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           const unsigned pm = __ballot_sync(FULL, pass);
           // the first nfree passing positions get slots; cut = positions consumed this round
           int cut = lim;
-          if (__popc(pm) >= nfree) cut = static_cast<int>(__fns(pm, 0, nfree)) + 1;  // past the nfree-th pass
+          if (__popc(pm) >= nfree) {  // past the nfree-th pass (rank by prefix popcount)
+            const bool nth = pass && __popc(pm & ((1u << lane) - 1u)) == nfree - 1;
+            cut = __ffs(__ballot_sync(FULL, nth));
+          }
           if (lane < cut && !pass) {
             const int qs = pp % SCAN_WINDOW;
             W.qstat[qs] = ST_NOTSURV;
@@ -276,10 +280,12 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           }
           const unsigned took = pm & ((cut >= 32) ? FULL : ((1u << cut) - 1u));
           // taken positions (ascending) go to the remaining free slots (ascending)
+          if ((took >> lane) & 1u) W.sel[__popc(took & ((1u << lane) - 1u))] = lane;
+          __syncwarp();
           int newpos = -1;
           if (slot_leader && ((free_left >> lane) & 1u)) {
             const int my_rank = __popc(free_left & ((1u << lane) - 1u));
-            if (my_rank < __popc(took)) newpos = D + static_cast<int>(__fns(took, 0, my_rank + 1));
+            if (my_rank < __popc(took)) newpos = D + W.sel[my_rank];
           }
           newpos = __shfl_sync(FULL, newpos, slot * SCAN_DEPTH);
           const unsigned assigned = __ballot_sync(FULL, slot_leader && newpos >= 0);
