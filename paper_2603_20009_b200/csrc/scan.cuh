@@ -26,6 +26,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "ptx.cuh"
+
 namespace skm {
 
 #ifndef SKM_SCAN_DEPTH
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
   const int tail_dims = s_bdcum[nb];
   const float f0 = s_theta[0];
   const unsigned FULL = 0xffffffffu;
+  const bool x_aligned = ((a.ldx & 3) == 0) && ((a.d_prime & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
   const int slot = lane / SCAN_DEPTH, dep = lane % SCAN_DEPTH;
   const bool slot_leader = dep == 0;
   const unsigned leader_mask = (SCAN_DEPTH == 4) ? 0x11111111u : (SCAN_DEPTH == 8) ? 0x01010101u
@@ -199,11 +202,20 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
       if (n_src > a.cap) continue;  // overflow row: handled by the dense pass
     }
     const long long row = a.row_map ? static_cast<long long>(a.row_map[rl]) : a.row0 + rl;
-    // ---- stage the x tail, quad layout (q, b, r)
+    // ---- stage the x tail, quad layout (q, b, r): 16-byte async copies (zero-filled past the
+    //      tail) whose latency overlaps the row's scalar loads and first queue fill
     const float* xrow = a.x + row * a.ldx + a.d_prime;
-    for (int u = lane; u < 64 * nb; u += 32) {
-      const int b = u >> 6, t = u & 63;
-      xsm[((t >> 2) * nb + b) * 4 + (t & 3)] = (u < tail_dims) ? xrow[u] : 0.0f;
+    if (x_aligned) {
+      for (int c = lane; c < 16 * nb; c += 32) {
+        const int b = c >> 4, q = c & 15;
+        const int valid = min(4, max(0, tail_dims - 4 * c));
+        cp_async_16_zfill(xsm + (q * nb + b) * 4, valid ? xrow + 4 * c : xrow, 4 * valid);
+      }
+    } else {
+      for (int u = lane; u < 64 * nb; u += 32) {
+        const int b = u >> 6, t = u & 63;
+        xsm[((t >> 2) * nb + b) * 4 + (t & 3)] = (u < tail_dims) ? xrow[u] : 0.0f;
+      }
     }
     float tcur = a.tau[row];
     int best = a.assign[row];
@@ -222,6 +234,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
       lidx = a.cand_idx + static_cast<long long>(rl) * a.cap;
       lval = a.cand_val + static_cast<long long>(rl) * a.cap;
     }
+    cp_async_wait_all();
     __syncwarp();
 
     while (true) {
@@ -401,14 +414,26 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             srun = W.qp[qs];
             if (srun > __fmul_rn(tcur, f0)) fin = ST_NOTSURV;
           }
-          while (!fin && sb < hi) {
-            const float v = (sb >= snxt) ? blk[(sb - snxt) & (SCAN_DEPTH - 1)] : rec[qs * nb + sb];
-            srun = __fadd_rn(srun, v);
+          // blocks recorded in earlier waves (only after a restart), then this wave's
+          // blocks straight from registers (static indices)
+          while (!fin && sb < snxt) {
+            srun = __fadd_rn(srun, rec[qs * nb + sb]);
             if (srun > __fmul_rn(tcur, s_theta[sb + 1])) {
               fin = ST_PRUNED;
               W.qpb[qs] = sb;
             }
             ++sb;
+          }
+#pragma unroll
+          for (int i = 0; i < SCAN_DEPTH; ++i) {
+            if (!fin && snxt + i < hi) {
+              srun = __fadd_rn(srun, blk[i]);
+              if (srun > __fmul_rn(tcur, s_theta[snxt + i + 1])) {
+                fin = ST_PRUNED;
+                W.qpb[qs] = snxt + i;
+              }
+              ++sb;
+            }
           }
           if (!fin && sb >= nb) fin = ST_COMPLETE;
           if (fin) {
