@@ -295,16 +295,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float* cv = args.cand_val + out_row * args.cand_cap;
 #pragma unroll
           for (int c = 0; c < GEMM_HALF / 32; ++c) {
+            // skip empty 4-column groups (about a tenth of the columns pass the gate); static
+            // register indices keep acc[] out of local memory
             const uint32_t m = mask[c];
             if (m == 0) continue;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if ((m >> j) & 1u) {
-                if (pos < args.cand_cap) {
-                  ci[pos] = col0 + c * 32 + j;
-                  cv[pos] = acc[c * 32 + j];
+            for (int g = 0; g < 8; ++g) {
+              if (((m >> (4 * g)) & 15u) == 0) continue;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const int j = 4 * g + jj;
+                if ((m >> j) & 1u) {
+                  if (pos < args.cand_cap) {
+                    ci[pos] = col0 + c * 32 + j;
+                    cv[pos] = acc[c * 32 + j];
+                  }
+                  ++pos;
                 }
-                ++pos;
               }
             }
           }

@@ -222,12 +222,24 @@ def _n_split(m_rows: int, n_cols: int, sms: int = 148) -> int:
     return max(1, min(n_tiles, (2 * sms + m_tiles - 1) // m_tiles))
 
 
+def _sm_count(dev) -> int:
+    try:
+        return int(torch.cuda.get_device_properties(dev).multi_processor_count)
+    except Exception:  # pragma: no cover - no device
+        return 148
+
+
 class Workspace:
     def __init__(self, dev, n: int, k: int, d: int, cfg: KMeansConfig):
         self.dev = dev
         self.cap = min(cfg.cand_cap, (k + 31) // 32 * 32)
-        # candidate slab bounded to ~2 GiB (8 B per candidate)
-        b = max(128, min(max(n, 1), cfg.x_batch_device, (2 << 30) // (8 * self.cap)))
+        # candidate slab bounded to ~4.5 GiB (8 B per candidate); batches are whole waves of
+        # 128-row gate-GEMM tiles over the SMs (one CTA per SM) so no launch ends on a
+        # partial wave except the last
+        per_wave = 128 * _sm_count(dev)
+        b = min(cfg.x_batch_device, (9 << 29) // (8 * self.cap))
+        b = max(per_wave, b // per_wave * per_wave) if b >= per_wave else max(128, b // 128 * 128)
+        b = max(128, min(max(n, 1), b))
         self.batch = b
         i32, f32 = torch.int32, torch.float32
         nn = max(n, 1)
