@@ -49,10 +49,11 @@ int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* o
 int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
                     long long ldo, void* stream);
 /* Gate-batch gather: ohi/olo[r, :cols] = hi/lo[idx[r], :cols], oxsq[r] = xsq[idx[r]],
- * othr[r] = thr[idx[r]] (rows in cluster order for the gate GEMM). */
+ * othr[r] = thr[idx[r]] (rows in cluster order for the gate GEMM); optionally (non-NULL) the
+ * certification terms oxsq_ext[r] = xsq_ext[idx[r]], othr1[r] = thr1[idx[r]]. */
 int skm_gather_front(const float* hi, const float* lo, long long ldi, const int* idx, int rows, int cols, float* ohi,
                      float* olo, long long ldo, const float* xsq, const float* thr, float* oxsq, float* othr,
-                     void* stream);
+                     const float* xsq_ext, const float* thr1, float* oxsq_ext, float* othr1, void* stream);
 int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
                         long long ldo, void* stream);
 int skm_fill_f32(float* p, long long n, float v, void* stream);
@@ -90,6 +91,10 @@ typedef struct skm_gemm_params {
   const float* thr;            /* GATE: per-row threshold (keep iff dist <= thr) */
   int* cand_idx; float* cand_val; int* cand_cnt; int cand_cap;
   long long row_offset;        /* ARGMIN/GATE output row offset */
+  /* GATE, optional: ext_k (64) more columns after K certify tail-block-0 prunes; certified
+   * candidates carry bit 31 in cand_idx.  xsq_ext/ysq_ext: norms over K + ext_k columns,
+   * thr1: per-row fl(tau * F[1]), cert_eps: margin relative to xsq_ext + ysq_ext. */
+  int ext_k; const float* xsq_ext; const float* ysq_ext; const float* thr1; float cert_eps;
 } skm_gemm_params;
 int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream);
 int skm_decode_argmin_keys(const unsigned long long* keys, int n, int* assign, float* tau, void* stream);
@@ -130,6 +135,7 @@ typedef struct skm_scan_params {
   unsigned long long* counters;                /* += {survivors, dims touched, changed} */
   int dense_mode;
   unsigned long long* counters_ext;            /* optional diagnostics: += {block sums computed} */
+  unsigned long long* prune_hist;              /* optional diagnostics: survivors by prune block */
 } skm_scan_params;
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
 /* Block-major tails T2[j][b][t] = C[j][d' + 64 b + t] (zero padded), the layout of the

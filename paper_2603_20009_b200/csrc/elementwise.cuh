@@ -56,7 +56,9 @@ __global__ void split_hilo_vec_kernel(const float4* __restrict__ x, long long ld
 __global__ void gather_front_kernel(const float* __restrict__ hi, const float* __restrict__ lo, long long ldi,
                                     const int* __restrict__ idx, int rows, int cols, float* __restrict__ ohi,
                                     float* __restrict__ olo, long long ldo, const float* __restrict__ xsq,
-                                    const float* __restrict__ thr, float* __restrict__ oxsq, float* __restrict__ othr) {
+                                    const float* __restrict__ thr, float* __restrict__ oxsq, float* __restrict__ othr,
+                                    const float* __restrict__ s3 = nullptr, float* __restrict__ o3 = nullptr,
+                                    const float* __restrict__ s4 = nullptr, float* __restrict__ o4 = nullptr) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const bool vec = ((ldi & 3) == 0) && ((ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(hi) & 15) == 0) &&
@@ -84,6 +86,8 @@ __global__ void gather_front_kernel(const float* __restrict__ hi, const float* _
     if (lane == 0) {
       oxsq[r] = xsq[src];
       othr[r] = thr[src];
+      if (s3) o3[r] = s3[src];
+      if (s4) o4[r] = s4[src];
     }
   }
 }

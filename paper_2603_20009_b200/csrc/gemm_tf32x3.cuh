@@ -45,7 +45,17 @@ struct GemmArgs {
   int* cand_cnt;              // GATE: per-row count (may exceed cap -> overflow)
   int cand_cap;
   long long row_offset;       // GATE/ARGMIN: added to the row index when writing outputs
+  // GATE, optional "certified block-0 prune" extension: ext_k (64) more columns after K are
+  // accumulated into one TMEM partial; a candidate whose distance over K + ext_k columns
+  // exceeds thr1 by the GEMM error margin is certainly pruned at tail block 0 (for any tau
+  // <= the seed tau) and is emitted with CAND_CERT0 set in its index.
+  int ext_k;
+  const float* xsq_ext;       // per-row norm over K + ext_k columns
+  const float* ysq_ext;       // per-column norm over K + ext_k columns
+  const float* thr1;          // per-row fl(tau * F[1])
+  float cert_eps;             // margin: eps * (xsq_ext + ysq_ext)
 };
+constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 256;
@@ -61,7 +71,7 @@ struct GemmSmem {
   static constexpr int B_BYTES = GEMM_BN * GEMM_BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
-  static constexpr int XCHG_BYTES = 2 * GEMM_PARTS * GEMM_BM * 4 + 2 * GEMM_BN * 4;  // slice exchange + ysq tiles
+  static constexpr int XCHG_BYTES = 2 * GEMM_PARTS * GEMM_BM * 4 + 4 * GEMM_BN * 4;  // slice exchange + ysq tiles (x2)
   static constexpr int TOTAL = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + XCHG_BYTES;
   static constexpr int TMEM_COLS = 2 * GEMM_BN;  // two k-block partial buffers
 };
@@ -80,6 +90,8 @@ template <int STAGES, int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
+                       const __grid_constant__ CUtensorMap tE_A_hi, const __grid_constant__ CUtensorMap tE_A_lo,
+                       const __grid_constant__ CUtensorMap tE_B_hi, const __grid_constant__ CUtensorMap tE_B_lo,
                        const GemmArgs args) {
   using L = GemmSmem<STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -98,6 +110,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int t_begin = blockIdx.y * args.tiles_per_cta;
   const int t_end = min(n_tiles, t_begin + args.tiles_per_cta);
   const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
+  // extension k-blocks (GATE certification): accumulated into ONE extra TMEM partial per tile
+  const int num_e = (MODE == GEMM_GATE) ? (args.ext_k + GEMM_BK - 1) / GEMM_BK : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tA_hi);
@@ -129,15 +143,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = t_begin; t < t_end; ++t) {
         const int n0 = t * GEMM_BN;
 #pragma unroll 1
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = 0; kb < num_k + num_e; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
           uint8_t* base = smem + s * L::STAGE_BYTES;
-          const int k0 = kb * GEMM_BK;
-          tma_load_2d(base, &tA_hi, &full[s], k0, m0);
-          tma_load_2d(base + L::A_BYTES, &tA_lo, &full[s], k0, m0);
-          tma_load_2d(base + 2 * L::A_BYTES, &tB_hi, &full[s], k0, n0);
-          tma_load_2d(base + 2 * L::A_BYTES + L::B_BYTES, &tB_lo, &full[s], k0, n0);
+          const bool ext = kb >= num_k;
+          const int k0 = (ext ? kb - num_k : kb) * GEMM_BK;
+          tma_load_2d(base, ext ? &tE_A_hi : &tA_hi, &full[s], k0, m0);
+          tma_load_2d(base + L::A_BYTES, ext ? &tE_A_lo : &tA_lo, &full[s], k0, m0);
+          tma_load_2d(base + 2 * L::A_BYTES, ext ? &tE_B_hi : &tB_hi, &full[s], k0, n0);
+          tma_load_2d(base + 2 * L::A_BYTES + L::B_BYTES, ext ? &tE_B_lo : &tB_lo, &full[s], k0, n0);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -152,10 +167,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
       for (int t = t_begin; t < t_end; ++t) {
 #pragma unroll 1
-        for (int kb = 0; kb < num_k; ++kb, ++kcount) {
+        for (int kb = 0; kb < num_k + num_e; ++kb) {
+          // extension k-blocks after the first one keep accumulating into the same partial
+          const bool cont = kb > num_k;
+          const bool last_of_partial = kb < num_k || kb == num_k + num_e - 1;
           const int buf = kcount & 1;
           const uint32_t use = kcount >> 1;
-          mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          if (!cont) mbar_wait(&tempty[buf], (use & 1) ^ 1);
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * GEMM_BN);
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
             const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);  // 8 tf32 = 32 bytes
-            mma_tf32(d_tmem, a_lo + adv, b_hi + adv, idesc, kk != 0);
+            mma_tf32(d_tmem, a_lo + adv, b_hi + adv, idesc, (kk != 0 || cont) ? 1u : 0u);
             mma_tf32(d_tmem, a_hi + adv, b_lo + adv, idesc, 1u);
           }
 #pragma unroll
@@ -176,7 +194,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mma_tf32(d_tmem, a_hi + adv, b_hi + adv, idesc, 1u);
           }
           mma_commit(&empty[s]);
-          mma_commit(&tfull[buf]);
+          if (last_of_partial) {
+            mma_commit(&tfull[buf]);
+            ++kcount;
+          }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -193,8 +214,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (MODE == GEMM_DIST || MODE == GEMM_ARGMIN || MODE == GEMM_GATE) {
       if (row_ok) xs = args.xsq[row];
     }
+    float xs_e = 0.0f, thr1 = 0.0f;
     if constexpr (MODE == GEMM_GATE) {
       if (row_ok) thr = args.thr[row];
+      if (num_e && row_ok) {
+        xs_e = args.xsq_ext[row];
+        thr1 = args.thr1[row];
+      }
     }
     float best = __int_as_float(0x7f800000);
     int best_j = 0x7fffffff;
@@ -222,16 +248,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // ---- tile complete: acc holds columns [col0, col0 + GEMM_HALF)
       const int col0 = t * GEMM_BN + half * GEMM_HALF;
       const float* ys_tile = nullptr;
+      const float* ye_tile = nullptr;
       if constexpr (MODE != GEMM_STORE) {
         // stage this tile's column norms in shared memory (double buffered by tile parity)
         float* yt = reinterpret_cast<float*>(xchg + 2 * GEMM_PARTS * GEMM_BM) + (t & 1) * GEMM_BN;
+        float* ye = yt + 2 * GEMM_BN;
         const int e = threadIdx.x - 64;
         if (e < GEMM_BN) {
           const int col = t * GEMM_BN + e;
           yt[e] = col < args.N ? __ldg(args.ysq + col) : 0.0f;
+          if (MODE == GEMM_GATE && num_e) ye[e] = col < args.N ? __ldg(args.ysq_ext + col) : 0.0f;
         }
         epi_bar_sync();
         ys_tile = yt + half * GEMM_HALF;
+        ye_tile = ye + half * GEMM_HALF;
       }
       if constexpr (MODE == GEMM_STORE || MODE == GEMM_DIST) {
         if (row_ok && col0 < args.N) {
@@ -264,19 +294,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       } else if constexpr (MODE == GEMM_GATE) {
         uint32_t mask[GEMM_HALF / 32];
+        uint32_t cert[GEMM_HALF / 32] = {};
         int my = 0;
         const int lim = row_ok ? args.N - col0 : 0;
+        uint32_t tbase_e = 0;
+        if (num_e) {
+          // certification partial (the ext_k columns after K): distance over K + ext_k columns
+          const int buf = kcount & 1;
+          mbar_wait(&tfull[buf], (kcount >> 1) & 1);
+          tc_fence_after();
+          tbase_e = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
+                    static_cast<uint32_t>(buf * GEMM_BN + half * GEMM_HALF);
+        }
 #pragma unroll
         for (int c = 0; c < GEMM_HALF / 32; ++c) {
-          uint32_t m = 0;
+          uint32_t m = 0, ce = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float dv = expand_dist(acc[c * 32 + j], xs, ys_tile[c * 32 + j]);
-            acc[c * 32 + j] = dv;
-            m |= ((c * 32 + j < lim) && !(dv > thr)) ? (1u << j) : 0u;
+          for (int h = 0; h < 2; ++h) {
+            float e16[16];
+            if (num_e) tmem_ld16(tbase_e + c * 32 + h * 16, e16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int jj = c * 32 + h * 16 + j;
+              if (num_e) {
+                const float ys_e = ye_tile[jj];
+                const float d64 = expand_dist(__fadd_rn(acc[jj], e16[j]), xs_e, ys_e);
+                if (__fsub_rn(d64, args.cert_eps * __fadd_rn(xs_e, ys_e)) > thr1) ce |= 1u << (h * 16 + j);
+              }
+              const float dv = expand_dist(acc[jj], xs, ys_tile[jj]);
+              acc[jj] = dv;
+              m |= ((jj < lim) && !(dv > thr)) ? (1u << (h * 16 + j)) : 0u;
+            }
           }
           mask[c] = m;
+          cert[c] = ce;
           my += __popc(m);
+        }
+        if (num_e) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[kcount & 1]);
+          ++kcount;
         }
         // order the column slices of this row: slice 0 first
         xchg[half * GEMM_BM + r_local] = my;
@@ -307,7 +365,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int j = 4 * g + jj;
                 if ((m >> j) & 1u) {
                   if (pos < args.cand_cap) {
-                    ci[pos] = col0 + c * 32 + j;
+                    ci[pos] = (col0 + c * 32 + j) | (((cert[c] >> j) & 1u) ? CAND_CERT0 : 0);
                     cv[pos] = acc[c * 32 + j];
                   }
                   ++pos;

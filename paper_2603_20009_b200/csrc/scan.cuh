@@ -78,6 +78,7 @@ struct ScanArgs {
   int* cx_rows;                  // complex rows (batch-local) appended by the speculative phase
   unsigned int* cx_count;
   const unsigned int* n_rows_dev;  // exact phase: row count read on device (overrides n_rows)
+  unsigned long long* prune_hist;  // optional diagnostics: survivors by prune block (nb = complete)
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -133,6 +134,10 @@ enum : int { ST_PENDING = 0, ST_NOTSURV = 1, ST_PRUNED = 2, ST_COMPLETE = 3 };
 __device__ __forceinline__ int walk_exact(float p, const float* rec_row, int nd, int nb, float tcur, float f0,
                                           const float* theta, int& pb, float& run) {
   if (p > __fmul_rn(tcur, f0)) return ST_NOTSURV;
+  if (nd < 0) {  // GEMM-certified: pruned at block 0 under any tau <= the seed tau
+    pb = 0;
+    return ST_PRUNED;
+  }
   run = p;
   for (int b = 0; b < nb; ++b) {
     if (b >= nd) return ST_PENDING;
@@ -244,6 +249,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         int j = 0;
         float p = 0.0f;
         bool ok = e < n_src;
+        bool cert = false;
         if (ok) {
           if constexpr (DENSE) {
             j = e;
@@ -251,6 +257,8 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           } else {
             j = lidx[e];
             p = lval[e];
+            cert = j < 0;  // CAND_CERT0: certified block-0 prune (gemm_tf32x3.cuh)
+            j &= 0x7fffffff;
           }
           ok = !(p > __fmul_rn(tcur, f0));
         }
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           const int qs = (F + __popc(m & ((1u << lane) - 1u))) % SCAN_WINDOW;
           W.qj[qs] = j;
           W.qp[qs] = p;
-          W.qdone[qs] = 0;
+          W.qdone[qs] = cert ? -1 : 0;  // -1 marks a certified entry: never takes a slot
           W.qstat[qs] = ST_PENDING;
           W.qver[qs] = -1;
         }
@@ -277,8 +285,12 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         while (nfree > 0 && D < F && D < R + SCAN_WINDOW) {
           const int lim = min(min(F, R + SCAN_WINDOW) - D, 32);
           const int pp = D + lane;
-          bool pass = false;
-          if (lane < lim) pass = !(W.qp[pp % SCAN_WINDOW] > __fmul_rn(tcur, f0));
+          bool pass = false, gate = false, cert = false;
+          if (lane < lim) {
+            gate = !(W.qp[pp % SCAN_WINDOW] > __fmul_rn(tcur, f0));
+            cert = W.qdone[pp % SCAN_WINDOW] < 0;
+            pass = gate && !cert;
+          }
           const unsigned pm = __ballot_sync(FULL, pass);
           // the first nfree passing positions get slots; cut = positions consumed this round
           int cut = lim;
@@ -286,9 +298,10 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             const bool nth = pass && __popc(pm & ((1u << lane) - 1u)) == nfree - 1;
             cut = __ffs(__ballot_sync(FULL, nth));
           }
-          if (lane < cut && !pass) {
+          if (lane < cut && !pass) {  // decided on the spot: not a survivor, or certified prune
             const int qs = pp % SCAN_WINDOW;
-            W.qstat[qs] = ST_NOTSURV;
+            W.qstat[qs] = (cert && gate) ? ST_PRUNED : ST_NOTSURV;
+            W.qpb[qs] = 0;
             W.qver[qs] = ver;
           }
           const unsigned took = pm & ((cut >= 32) ? FULL : ((1u << cut) - 1u));
@@ -360,6 +373,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         if (counted && (st == ST_PRUNED || st == ST_COMPLETE)) {
           surv_acc += 1;
           touched_acc += (st == ST_PRUNED) ? s_bdcum[pb + 1] : tail_dims;
+          if (a.prune_hist) atomicAdd(&a.prune_hist[st == ST_PRUNED ? pb : nb], 1ull);  // diagnostics only
         }
         const int src_lane = ev ? limit : 0;
         const int ev_improve = __shfl_sync(FULL, (int)improve, src_lane);

@@ -88,6 +88,16 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   if ((rc = make_tmap(&ta_lo, p->a_lo, p->M, p->K, p->lda, skm::GEMM_BM))) return rc;
   if ((rc = make_tmap(&tb_hi, p->b_hi, p->N, p->K, p->ldb, BN))) return rc;
   if ((rc = make_tmap(&tb_lo, p->b_lo, p->N, p->K, p->ldb, BN))) return rc;
+  // GATE certification extension: columns [K, K + ext_k) of the same operands
+  CUtensorMap te_a_hi = ta_hi, te_a_lo = ta_lo, te_b_hi = tb_hi, te_b_lo = tb_lo;
+  const int ext_k = (MODE == skm::GEMM_GATE) ? p->ext_k : 0;
+  if (ext_k > 0) {
+    if (p->K % 4 || !p->xsq_ext || !p->ysq_ext || !p->thr1) return fail(SKM_E_ARG, "gemm: ext_k needs K%4==0 and ext norms/thr1");
+    if ((rc = make_tmap(&te_a_hi, p->a_hi + p->K, p->M, ext_k, p->lda, skm::GEMM_BM))) return rc;
+    if ((rc = make_tmap(&te_a_lo, p->a_lo + p->K, p->M, ext_k, p->lda, skm::GEMM_BM))) return rc;
+    if ((rc = make_tmap(&te_b_hi, p->b_hi + p->K, p->N, ext_k, p->ldb, BN))) return rc;
+    if ((rc = make_tmap(&te_b_lo, p->b_lo + p->K, p->N, ext_k, p->ldb, BN))) return rc;
+  }
   auto kern = skm::gemm_tf32x3_kernel<STAGES, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -116,10 +126,15 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   a.cand_cnt = p->cand_cnt;
   a.cand_cap = p->cand_cap;
   a.row_offset = p->row_offset;
+  a.ext_k = ext_k;
+  a.xsq_ext = p->xsq_ext;
+  a.ysq_ext = p->ysq_ext;
+  a.thr1 = p->thr1;
+  a.cert_eps = p->cert_eps;
   if (MODE == skm::GEMM_ARGMIN && split > 1 && !p->keys) return fail(SKM_E_ARG, "ARGMIN with n_split>1 needs keys");
   if (MODE == skm::GEMM_GATE && split > 1) return fail(SKM_E_ARG, "GATE requires n_split == 1");
   dim3 grid((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM, split);
-  kern<<<grid, skm::GEMM_THREADS, L::TOTAL, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, a);
+  kern<<<grid, skm::GEMM_THREADS, L::TOTAL, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, te_a_hi, te_a_lo, te_b_hi, te_b_lo, a);
   SKM_LAUNCH_CHECK("gemm_tf32x3 launch");
   return SKM_OK;
 }
@@ -170,11 +185,11 @@ int skm_gather_rows(const float* in, long long ldi, const long long* idx, int ro
 
 int skm_gather_front(const float* hi, const float* lo, long long ldi, const int* idx, int rows, int cols, float* ohi,
                      float* olo, long long ldo, const float* xsq, const float* thr, float* oxsq, float* othr,
-                     void* stream) {
+                     const float* xsq_ext, const float* thr1, float* oxsq_ext, float* othr1, void* stream) {
   if (rows <= 0) return SKM_OK;
   if (cols > ldo || cols > ldi) return fail(SKM_E_ARG, "gather_front: cols exceeds a stride");
   skm::gather_front_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(
-      hi, lo, ldi, idx, rows, cols, ohi, olo, ldo, xsq, thr, oxsq, othr);
+      hi, lo, ldi, idx, rows, cols, ohi, olo, ldo, xsq, thr, oxsq, othr, xsq_ext, oxsq_ext, thr1, othr1);
   SKM_LAUNCH_CHECK("gather_front");
   return SKM_OK;
 }
@@ -443,6 +458,7 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.assign = p->assign;
   a.counters = p->counters;
   a.counters_ext = p->counters_ext;
+  a.prune_hist = p->prune_hist;
   const size_t smem = skm::scan_dyn_smem(p->nb);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);

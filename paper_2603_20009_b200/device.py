@@ -66,7 +66,8 @@ def row_sq_norms(x: torch.Tensor, dims: int, out: torch.Tensor | None = None) ->
 
 def gemm(a_hi, a_lo, b_hi, b_lo, M: int, N: int, K: int, mode: int, *, out=None, xsq=None, ysq=None,
          assign=None, tau=None, keys=None, thr=None, cand_idx=None, cand_val=None, cand_cnt=None,
-         cand_cap: int = 0, n_split: int = 1, row_offset: int = 0) -> None:
+         cand_cap: int = 0, n_split: int = 1, row_offset: int = 0, ext_k: int = 0, xsq_ext=None, ysq_ext=None,
+         thr1=None, cert_eps: float = 0.0) -> None:
     p = native.GemmParams()
     p.a_hi, p.a_lo, p.lda = a_hi.data_ptr(), a_lo.data_ptr(), a_hi.stride(0)
     p.b_hi, p.b_lo, p.ldb = b_hi.data_ptr(), b_lo.data_ptr(), b_hi.stride(0)
@@ -74,11 +75,13 @@ def gemm(a_hi, a_lo, b_hi, b_lo, M: int, N: int, K: int, mode: int, *, out=None,
     if out is not None:
         p.out, p.ldo = out.data_ptr(), out.stride(0)
     for name, t in (("xsq", xsq), ("ysq", ysq), ("assign", assign), ("tau", tau), ("keys", keys),
-                    ("thr", thr), ("cand_idx", cand_idx), ("cand_val", cand_val), ("cand_cnt", cand_cnt)):
+                    ("thr", thr), ("cand_idx", cand_idx), ("cand_val", cand_val), ("cand_cnt", cand_cnt),
+                    ("xsq_ext", xsq_ext), ("ysq_ext", ysq_ext), ("thr1", thr1)):
         if t is not None:
             setattr(p, name, t.data_ptr())
     p.cand_cap = cand_cap
     p.row_offset = row_offset
+    p.ext_k, p.cert_eps = ext_k, cert_eps
     native.check(native.load().skm_gemm_tf32x3(C.byref(p), stream_handle()), "skm_gemm_tf32x3")
 
 

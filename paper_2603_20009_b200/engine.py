@@ -52,6 +52,14 @@ from .hostmath import (
 # B200.  SKM_SCAN=spec selects the multi-round speculative pair scan (spec_scan.cuh, same
 # results bit for bit; see DESIGN.md section 3 for why it is not the default).
 TWO_PHASE_SCAN = os.environ.get("SKM_SCAN", "exact") == "spec"
+PRUNE_HIST = None  # diagnostics (tools/): device u64[nb + 1] histogram of prune blocks
+# GEMM-certified tail-block-0 prunes (gemm_tf32x3.cuh, GATE ext_k): the gate GEMM also sums
+# the first 64 tail dimensions and flags candidates whose distance there exceeds fl(tau F1)
+# by more than CERT_EPS * (|x|^2 + |c|^2) over those dimensions -- far above the 3xTF32 +
+# expansion error -- so the exact scan counts them (survivor, 64 dims) without walking them.
+# (a prefix of tail block 0 lower-bounds its running sum, so any ext <= 64 is a valid certificate)
+CERT_EXT = int(os.environ.get("SKM_CERT_EXT", "64")) if os.environ.get("SKM_CERT", "1") != "0" else 0
+CERT_EPS = 3e-5
 
 _U64_MAX = (1 << 64) - 1
 
@@ -174,6 +182,7 @@ class Centroids:
         self.ysq = torch.empty(self.k, dtype=torch.float32, device=c.device)
         self.tails = None
         self.tails_blk = None
+        self.ysq_ext = None
 
     def refresh(self, dims: int, d_prime: int | None):
         """Recompute split + norms over `dims` (+ tails at d_prime) after an update."""
@@ -181,6 +190,10 @@ class Centroids:
                     stream_handle())
         native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, dims, ptr(self.ysq), stream_handle())
         if d_prime is not None:
+            if self.ysq_ext is None:
+                self.ysq_ext = torch.empty(self.k, dtype=torch.float32, device=self.c.device)
+            native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, min(self.d, d_prime + 64), ptr(self.ysq_ext),
+                        stream_handle())
             nb = (self.d - d_prime + 63) // 64
             need = self.k * 64 * nb
             if self.tails is None or self.tails.numel() < need:
@@ -205,6 +218,8 @@ def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
         p.out, p.ldo = out.data_ptr(), out.stride(0)
     p.cand_cap = kw.pop("cand_cap", 0)
     p.row_offset = kw.pop("row_offset", 0)
+    p.ext_k = kw.pop("ext_k", 0)
+    p.cert_eps = kw.pop("cert_eps", 0.0)
     for name, t in kw.items():
         if t is not None:
             setattr(p, name, t.data_ptr())
@@ -261,6 +276,9 @@ class Workspace:
             self.scan_scratch = torch.empty((nbytes + 3) // 4, dtype=torch.int32, device=dev)
         self.bx = torch.empty(b, dtype=f32, device=dev)
         self.bthr = torch.empty(b, dtype=f32, device=dev)
+        self.thr1 = torch.empty(nn, dtype=f32, device=dev)
+        self.bx_ext = torch.empty(b, dtype=f32, device=dev)
+        self.bthr1 = torch.empty(b, dtype=f32, device=dev)
         self._front = None
         self.order = torch.empty(nn, dtype=i32, device=dev)
         self.counts = torch.empty(k, dtype=i32, device=dev)
@@ -347,11 +365,17 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
                     ptr(tau), st, nbytes=4.0 * n * d + 8.0 * n)
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
                 ptr(ws.thr[row0:row0 + n]), st)
+    # certification (exact scan only; the speculative scan does not decode the flag)
+    ext = CERT_EXT if (not TWO_PHASE_SCAN and not plan.sentinel and dp % 4 == 0 and dp + CERT_EXT <= d
+                       and plan.widths[0] == 64) else 0
+    if ext:
+        native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(ws.thr1[row0:row0 + n]), st)
+        xsq_ext = data.norms(dp + ext)
     xsq = data.norms(dp)
     k = cents.k
     ordered = order is not None and row0 == 0 and n == data.n
     if ordered:
-        fld = padded_ld(dp)
+        fld = padded_ld(dp + ext)
         ga_hi, ga_lo = ws.front_buffers(fld)
     for b0 in range(0, n, ws.batch):
         bn = min(ws.batch, n - b0)
@@ -360,17 +384,23 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         if ordered:
             rmap = order[b0:b0 + bn]
             # the front buffers may be wider than fld (allocated at a larger d'): use their stride
-            native.call("skm_gather_front", ptr(data.hi), ptr(data.lo), data.ld, ptr(rmap), bn, dp, ptr(ga_hi),
-                        ptr(ga_lo), ga_hi.stride(0), ptr(xsq), ptr(ws.thr), ptr(ws.bx), ptr(ws.bthr), st,
-                        nbytes=16.0 * bn * dp + 16.0 * bn)
+            native.call("skm_gather_front", ptr(data.hi), ptr(data.lo), data.ld, ptr(rmap), bn, dp + ext, ptr(ga_hi),
+                        ptr(ga_lo), ga_hi.stride(0), ptr(xsq), ptr(ws.thr), ptr(ws.bx), ptr(ws.bthr),
+                        ptr(xsq_ext) if ext else None, ptr(ws.thr1) if ext else None,
+                        ptr(ws.bx_ext) if ext else None, ptr(ws.bthr1) if ext else None, st,
+                        nbytes=16.0 * bn * (dp + ext) + 24.0 * bn)
+            cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=cents.ysq_ext, thr1=ws.bthr1[:bn],
+                        cert_eps=CERT_EPS) if ext else {}
             _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
                   ysq=cents.ysq, thr=ws.bthr[:bn], cand_idx=ws.cand_idx, cand_val=ws.cand_val, cand_cnt=ws.cand_cnt,
-                  cand_cap=ws.cap)
+                  cand_cap=ws.cap, **cert)
             sp.row_map = rmap.data_ptr()
         else:
+            cert = dict(ext_k=ext, xsq_ext=xsq_ext[r:r + bn], ysq_ext=cents.ysq_ext, thr1=ws.thr1[r:r + bn],
+                        cert_eps=CERT_EPS) if ext else {}
             _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE,
                   xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand_idx=ws.cand_idx,
-                  cand_val=ws.cand_val, cand_cnt=ws.cand_cnt, cand_cap=ws.cap)
+                  cand_val=ws.cand_val, cand_cnt=ws.cand_cnt, cand_cap=ws.cap, **cert)
         sp.cand_idx, sp.cand_val, sp.cand_cnt, sp.cap = (ws.cand_idx.data_ptr(), ws.cand_val.data_ptr(),
                                                           ws.cand_cnt.data_ptr(), ws.cap)
         sp.k, sp.n_rows, sp.row0 = k, bn, r
@@ -380,6 +410,8 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
         sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
         sp.counters_ext = ws.diag.data_ptr()
+        if PRUNE_HIST is not None:
+            sp.prune_hist = PRUNE_HIST.data_ptr()
         if TWO_PHASE_SCAN:
             native.call("skm_pruned_scan2", C.byref(sp), ptr(cents.tails_blk), ptr(ws.scan_scratch),
                         ws.scan_scratch.numel() * 4, st, tag="pruned_scan",

@@ -41,6 +41,7 @@ class GemmParams(C.Structure):
         ("thr", _vp),
         ("cand_idx", _vp), ("cand_val", _vp), ("cand_cnt", _vp), ("cand_cap", _i),
         ("row_offset", _ll),
+        ("ext_k", _i), ("xsq_ext", _vp), ("ysq_ext", _vp), ("thr1", _vp), ("cert_eps", _f),
     ]
 
 
@@ -57,6 +58,7 @@ class ScanParams(C.Structure):
         ("counters", _vp),
         ("dense_mode", _i),
         ("counters_ext", _vp),
+        ("prune_hist", _vp),
     ]
 
 
@@ -89,7 +91,8 @@ _SIGS = {
     "skm_build_tails": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
     "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp], _i),
     "skm_pruned_scan": ([C.POINTER(ScanParams), _vp], _i),
-    "skm_gather_front": ([_vp, _vp, _ll, _vp, _i, _i, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp], _i),
+    "skm_gather_front": ([_vp, _vp, _ll, _vp, _i, _i, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                         _i),
     "skm_build_tails_blk": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
     "skm_scan2_scratch_bytes": ([_i, _i], _ll),
     "skm_pruned_scan2": ([C.POINTER(ScanParams), _vp, _vp, _ll, _vp], _i),

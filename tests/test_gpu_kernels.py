@@ -206,15 +206,17 @@ SCAN_CASES = [
 
 
 @pytest.mark.parametrize("seed,n,k,d,dp,sentinel", SCAN_CASES)
-@pytest.mark.parametrize("two_phase,prev_mode", [(False, "random"), (True, "random"), (True, "nearest"),
-                                                 (True, "mixed")])
-def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, prev_mode):
+@pytest.mark.parametrize("two_phase,prev_mode,cert", [(False, "random", False), (True, "random", False),
+                                                      (True, "nearest", False), (True, "mixed", False),
+                                                      (False, "nearest", True), (False, "mixed", True)])
+def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, prev_mode, cert):
     """Production scan equals the sequential reference scan over all centroids, including the
     survivor/dims counters: the one-phase exact kernel (candidate lists + speculative waves +
     in-order resolve) and the two-phase scan (speculative pair scan for rows whose tau can only
     change at their previous centroid + exact kernel on the rest).  ``prev_mode`` picks the
     previous assignment: random (most rows re-assign), the nearest centroid (steady state: the
-    speculative phase owns almost every row) or 90% nearest."""
+    speculative phase owns almost every row) or 90% nearest.  ``cert``: the gate GEMM also
+    certifies tail-block-0 prunes (ext_k = 64) and the exact scan skips walking them."""
     from oracle import kernels_np as O
     from paper_2603_20009_b200 import native
     from paper_2603_20009_b200.config import pdxify, tail_block_layout
@@ -231,8 +233,9 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
         near = d2.argmin(1).astype(np.int32)
         prev = near if prev_mode == "nearest" else np.where(rng.random(n) < 0.9, near, prev).astype(np.int32)
     X, Cm = _pad(x), _pad(c)
-    xh, xl = dev.split_hilo(X, dp)
-    ch, cl = dev.split_hilo(Cm, dp)
+    # the certification extension reads columns [dp, dp + 64) of the same split operands
+    xh, xl = dev.split_hilo(X, d if cert else dp)
+    ch, cl = dev.split_hilo(Cm, d if cert else dp)
     xs = dev.row_sq_norms(X, dp)
     cs = dev.row_sq_norms(Cm, dp)
     D = torch.empty((n, dev.padded_ld(k)), dtype=torch.float32, device="cuda")
@@ -266,8 +269,26 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     ci = torch.empty((n, cap), dtype=torch.int32, device="cuda")
     cv = torch.empty((n, cap), dtype=torch.float32, device="cuda")
     cc = torch.empty(n, dtype=torch.int32, device="cuda")
+    widths, _ = tail_block_layout(d, dp)
+    ext = 64 if cert and not sentinel and dp % 4 == 0 and dp + 64 <= d and widths[0] == 64 else 0
+    if cert and not ext:
+        pytest.skip("certification needs d' % 4 == 0 and a full first tail block")
+    kw = {}
+    if ext:
+        thr1 = torch.empty(n, dtype=torch.float32, device="cuda")
+        native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[1]), 0, dev.ptr(thr1), dev.stream_handle())
+        kw = dict(ext_k=ext, xsq_ext=dev.row_sq_norms(X, dp + ext), ysq_ext=dev.row_sq_norms(Cm, dp + ext), thr1=thr1,
+                  cert_eps=3e-5)
     dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand_idx=ci, cand_val=cv,
-             cand_cnt=cc, cand_cap=cap)
+             cand_cnt=cc, cand_cap=cap, **kw)
+    if ext:
+        valid = torch.arange(cap, device="cuda")[None, :] < cc.clamp(max=cap)[:, None]
+        n_cert = int(((ci < 0) & valid).sum().item())
+        print(f"certified block-0 prunes: {n_cert} of {int(valid.sum().item())} candidates")
+        if prev_mode == "mixed" and d >= 1024:
+            assert n_cert > 0  # re-assigning rows have far candidates: the extension must fire
+        # certified entries carry the same centroid index (bit 31 aside) and partial distance
+        assert int((ci & 0x7fffffff)[valid].max().item()) < k
     nb = len(widths)
     tails = torch.empty(k * 64 * nb, dtype=torch.float32, device="cuda")
     native.call("skm_build_tails", dev.ptr(Cm), Cm.stride(0), k, d, dp, dev.ptr(tails), dev.stream_handle())
