@@ -164,6 +164,31 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
     comm = comm or Comm()
     dev = x_dev.device
     timer = _Timer()
+    ws = None
+    first_pass_done = False
+    n_local0 = x_dev.shape[0]
+    if isinstance(rotation, _RotationJob):
+        if comm.world == 1 and cfg.etr is None and 0 < n_local0 and not (cfg.k > n_local0):
+            # The host QR of R is still running.  Iteration 1 is a full argmin and squared
+            # distances are rotation invariant, so it runs on the unrotated rows against the
+            # unrotated Forgy rows now (same assignments up to distance near-ties, like any
+            # GEMM-vs-OpenBLAS difference); the loop then starts from its result.
+            from .engine import Centroids, Workspace, full_assign_pass
+            from .hostmath import init_indices as _ii
+            timer.start("gemm")
+            d0 = DeviceData(x_dev, d)
+            idx0 = torch.tensor(_ii(n_local0, cfg.k, [cfg.seed, 2]), dtype=torch.int64, device=dev)
+            rows0 = torch.zeros((cfg.k, d0.ld), dtype=torch.float32, device=dev)
+            native.call("skm_gather_rows", ptr(d0.x), d0.ld, ptr(idx0), cfg.k, d0.ld, ptr(rows0), d0.ld,
+                        stream_handle())
+            c0 = Centroids(rows0, d)
+            c0.refresh(d, None)
+            ws = Workspace(dev, n_local0, cfg.k, d, cfg)
+            full_assign_pass(d0, c0, ws)
+            del d0, c0, rows0
+            first_pass_done = True
+            timer.stop("gemm")
+        rotation = rotation.get()
     timer.start("rotation")
     rot = DeviceRotation(rotation, dev)
     xr = rot.apply(x_dev)
@@ -189,7 +214,7 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
         etr = EtrState(cfg)
     phase = dict(timer.collect())
     out = fit_rotated_device(data, cfg, inspect=inspect, comm=comm, n_global=n, row_lo=row_lo, init_rows=init_rows,
-                             init_idx=init_idx, etr=etr, timer=timer)
+                             init_idx=init_idx, etr=etr, timer=timer, ws=ws, first_pass_done=first_pass_done)
     phase.update(out.phase_seconds)
     timer.start("unrotate")
     cent = rot.apply(out.centroids_dev, inverse=True)
@@ -209,9 +234,9 @@ def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
     sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
     xs = x if sidx is None else x[sidx]
     job = _RotationJob(d, cfg.seed)       # host PCG64 + LAPACK QR (persisted-model contract) ...
-    x_dev = _h2d(xs, dev)                  # ... overlapped with the host->device copy
-    rotation = job.get()
-    res = fit_device(x_dev, d, cfg, rotation, inspect=inspect)
+    x_dev = _h2d(xs, dev)                  # ... overlapped with the host->device copy and iteration 1
+    res = fit_device(x_dev, d, cfg, job, inspect=inspect)
+    rotation = res.rotation
     del x_dev
     out = res.loop
     phase = dict(res.phase)

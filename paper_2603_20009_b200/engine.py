@@ -505,7 +505,8 @@ def assign_stats(ws: Workspace, n: int, with_prev: bool) -> None:
 # ------------------------------------------------------------------------------ the loop
 def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: Comm | None = None,
                        n_global: int | None = None, row_lo: int = 0, init_rows: torch.Tensor | None = None,
-                       init_idx: np.ndarray | None = None, etr=None, timer: _Timer | None = None) -> LoopOutput:
+                       init_idx: np.ndarray | None = None, etr=None, timer: _Timer | None = None,
+                       ws: Workspace | None = None, first_pass_done: bool = False) -> LoopOutput:
     """Device twin of core._fit_rotated.  ``data`` holds this rank's rows; ``n_global`` the
     total across ranks.  ``init_rows`` (k, ld) are the Forgy rows gathered from all ranks."""
     comm = comm or Comm()
@@ -523,7 +524,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(idx), k, data.ld, ptr(init_rows), data.ld,
                     stream_handle())
     cents = Centroids(init_rows, d)
-    ws = Workspace(dev, n_local, k, d, cfg)
+    ws = ws or Workspace(dev, n_local, k, d, cfg)
     rng_split = np.random.default_rng([cfg.seed, 3])
     pruned_mode = pruning_supported(d)
     d_prime = initial_d_prime(d, cfg.d_prime_init_fraction) if pruned_mode else None
@@ -554,8 +555,9 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             native.call("skm_copy_i32", ptr(ws.assign), ptr(ws.prev), n_local, stream_handle())
         if not pruned_iter:
             timer.start("gemm")
-            cents.refresh(d, None)
-            full_assign_pass(data, cents, ws)
+            if not (it == 1 and first_pass_done):  # else: ran on the unrotated rows (api.fit_device)
+                cents.refresh(d, None)
+                full_assign_pass(data, cents, ws)
             timer.stop("gemm")
             work.full_pair_dims += n * k * d
         else:
