@@ -48,6 +48,12 @@ int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* o
 /* out[r,:cols] = in[idx[r],:cols] */
 int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
                     long long ldo, void* stream);
+/* Vector-file ingestion (dataio.py:57-112): validate + scatter `rows` staged records (fvecs:
+ * rec_words = d + 1, header_words = 1; fbin: d, 0) starting at file row row0 into out (ld ldo).
+ * bad_dim / bad_val[row / 4096] = min(bad record row) / min(non-finite flat index). */
+int skm_ingest_records(const void* raw, long long rows, int d, int rec_words, int header_words, long long row0,
+                       float* out, long long ldo, unsigned long long* bad_dim, unsigned long long* bad_val,
+                       void* stream);
 /* Gate-batch gather: ohi/olo[r, :cols] = hi/lo[idx[r], :cols], oxsq[r] = xsq[idx[r]],
  * othr[r] = thr[idx[r]] (rows in cluster order for the gate GEMM); optionally (non-NULL) the
  * certification terms oxsq_ext[r] = xsq_ext[idx[r]], othr1[r] = thr1[idx[r]]. */

@@ -10,6 +10,11 @@ the reference package's Python API.
 
 from .api import KMeansResult, final_assign, fit
 from .config import (
+    ChecksumMismatch,
+    InconsistentDim,
+    MalformedHeader,
+    TruncatedFile,
+    VersionMismatch,
     D_PRIME_ALIGN,
     D_PRIME_MIN,
     MAX_BANK,
@@ -70,6 +75,10 @@ def __getattr__(name):
                 "probe_eval", "ivf_probe_search", "recall_at_k"):
         from . import etr
         return getattr(etr, name)
+    if name in ("load_vectors", "load_vectors_device", "write_fvecs", "write_fbin", "infer_format", "sha256_file",
+                "CentroidModel", "save_centroids", "load_centroids", "save_ground_truth", "load_ground_truth"):
+        from . import dataio
+        return getattr(dataio, name)
     if name in ("apply_rotation", "unapply_rotation", "sample_training_set", "init_centroids", "compute_norms",
                 "update_centroids", "split_empty_clusters"):
         from . import extras

@@ -92,6 +92,41 @@ __global__ void gather_front_kernel(const float* __restrict__ hi, const float* _
   }
 }
 
+// Vector-file ingestion (dataio.py:57-112): one staged chunk of `rows` records starting at
+// file row `row0` is validated and scattered into the padded device matrix.  fvecs records are
+// [int32 d][d float32] (rec_words = d + 1, header_words = 1); fbin rows are bare (0 / d).
+// For every 4096-row reporting chunk the first bad record (declared dim != d) and the first
+// non-finite element (flat row-major index) are kept with atomicMin -- the host then reports
+// the reference's error for the first reporting chunk holding either (dims take precedence).
+constexpr int INGEST_CHUNK_ROWS = 4096;
+__global__ void ingest_records_kernel(const uint32_t* __restrict__ raw, long long rows, int d, int rec_words,
+                                      int header_words, long long row0, float* __restrict__ out, long long ldo,
+                                      unsigned long long* __restrict__ bad_dim, unsigned long long* __restrict__ bad_val) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (long long r = blockIdx.x * (long long)wpb + (threadIdx.x >> 5); r < rows; r += (long long)gridDim.x * wpb) {
+    const uint32_t* rec = raw + r * rec_words;
+    const long long grow = row0 + r;
+    const long long rc = grow / INGEST_CHUNK_ROWS;
+    if (header_words && lane == 0 && static_cast<int>(rec[0]) != d)
+      atomicMin(bad_dim + rc, static_cast<unsigned long long>(grow));
+    const float* v = reinterpret_cast<const float*>(rec + header_words);
+    float* o = out + grow * ldo;
+    unsigned long long first = ~0ull;
+    for (int c = lane; c < d; c += 32) {
+      const float x = v[c];
+      if (!isfinite(x) && first == ~0ull) first = static_cast<unsigned long long>(grow) * d + c;
+      o[c] = x;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, first, s);
+      first = o2 < first ? o2 : first;
+    }
+    if (lane == 0 && first != ~0ull) atomicMin(bad_val + rc, first);
+  }
+}
+
 // Squared row norms over the leading `dims` columns, double accumulation rounded to
 // fp32 (preprocess.py:95-101).  One warp per row.
 __global__ void row_sq_norms_kernel(const float* __restrict__ x, long long ldx, int rows, int dims,

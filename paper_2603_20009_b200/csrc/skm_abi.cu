@@ -194,6 +194,17 @@ int skm_gather_front(const float* hi, const float* lo, long long ldi, const int*
   return SKM_OK;
 }
 
+int skm_ingest_records(const void* raw, long long rows, int d, int rec_words, int header_words, long long row0,
+                       float* out, long long ldo, unsigned long long* bad_dim, unsigned long long* bad_val,
+                       void* stream) {
+  if (rows <= 0) return SKM_OK;
+  if (d <= 0 || ldo < d || rec_words < d + header_words) return fail(SKM_E_ARG, "ingest_records: bad shape");
+  skm::ingest_records_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uint32_t*>(raw), rows, d, rec_words, header_words, row0, out, ldo, bad_dim, bad_val);
+  SKM_LAUNCH_CHECK("ingest_records");
+  return SKM_OK;
+}
+
 int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
                         long long ldo, void* stream) {
   if (rows <= 0) return SKM_OK;

@@ -190,7 +190,62 @@ def probes():
     return out
 
 
+DATAIO_CASES = {
+    # name: (format, n, d, mutations) -- files are rebuilt by tests/dataio_cases.py
+    "fvecs_ok": ("fvecs", 9000, 37, []),
+    "fbin_ok": ("fbin", 9000, 37, []),
+    "fvecs_nan_row": ("fvecs", 9000, 20, [("val", 5000, 3, "nan")]),
+    "fvecs_inf_first_chunk": ("fvecs", 9000, 20, [("val", 4095, 19, "inf"), ("dim", 4097, 0, 21)]),
+    "fvecs_dim_vs_nan_same_chunk": ("fvecs", 9000, 20, [("val", 100, 2, "nan"), ("dim", 2000, 0, 7)]),
+    "fbin_nan_two": ("fbin", 5000, 16, [("val", 4200, 15, "-inf"), ("val", 4100, 0, "nan")]),
+    "fvecs_trailing_match": ("fvecs", 100, 8, [("trail", 4, 0, 8)]),
+    "fvecs_trailing_mismatch": ("fvecs", 100, 8, [("trail", 12, 0, 9)]),
+    "fvecs_trailing_short": ("fvecs", 100, 8, [("trail", 3, 0, 0)]),
+    "fbin_truncated": ("fbin", 100, 8, [("truncate", 30, 0, 0)]),
+    "fbin_bad_header": ("fbin", 10, 4, [("header", -1, 4, 0)]),
+    "fvecs_bad_header": ("fvecs", 10, 4, [("header", 0, 0, 0)]),
+}
+
+
+def dataio_golden():
+    """Reference outcomes of load_vectors on generated (valid and malformed) files, and the
+    reference's SKMC / SKGT bytes for small models."""
+    import tempfile
+    sys.path.insert(0, os.path.dirname(HERE))
+    from dataio_cases import build_case  # tests/dataio_cases.py
+    from superkmeans import dataio as rdio
+    from superkmeans.evaluation import GroundTruth as RGT
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, spec in DATAIO_CASES.items():
+            path = build_case(td, name, spec)
+            try:
+                x = rdio.load_vectors(path)
+                out[f"{name}_outcome"] = np.array("ok")
+                out[f"{name}_sum"] = np.float64(x.astype(np.float64).sum())
+                out[f"{name}_shape"] = np.array(x.shape)
+            except Exception as e:  # noqa: BLE001
+                out[f"{name}_outcome"] = np.array(type(e).__name__)
+                out[f"{name}_msg"] = np.array(str(e).replace(td, "<dir>"))
+                out[f"{name}_rowcol"] = np.array([getattr(e, "row", -1), getattr(e, "col", -1)])
+        rng = np.random.default_rng(5)
+        c = rng.standard_normal((7, 5)).astype(np.float32)
+        rdio.save_centroids(os.path.join(td, "m0.skmc"), c, 42)
+        rdio.save_centroids(os.path.join(td, "m1.skmc"), c, 7, cluster_lists=[np.arange(i) for i in range(7)])
+        gt = RGT(indices=rng.integers(0, 100, (3, 4)), distances=rng.random((3, 4)).astype(np.float32), k_gt=4)
+        rdio.save_ground_truth(os.path.join(td, "g.skgt"), gt)
+        out["model_centroids"] = c
+        out["gt_indices"] = gt.indices
+        out["gt_distances"] = gt.distances
+        for f in ("m0.skmc", "m1.skmc", "g.skgt"):
+            out["bytes_" + f.replace(".", "_")] = np.frombuffer(open(os.path.join(td, f), "rb").read(), np.uint8)
+    return out
+
+
 def main():
+    if "--only-dataio" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "dataio.npz"), **dataio_golden())
+        return
     if "--only-probes" in sys.argv:
         np.savez_compressed(os.path.join(HERE, "probes.npz"), **probes())
         return
