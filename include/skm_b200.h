@@ -48,6 +48,11 @@ int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* o
 /* out[r,:cols] = in[idx[r],:cols] */
 int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
                     long long ldo, void* stream);
+/* evaluation.wcss (evaluation.py:205-215): *out = sum_i |x_i - c_{assign_i}|^2 (f64),
+ * deterministic; workspace: skm_wcss_workspace_bytes() of device memory. */
+long long skm_wcss_workspace_bytes(void);
+int skm_wcss(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign, long long n,
+             int d, double* out, void* workspace, void* stream);
 /* Vector-file ingestion (dataio.py:57-112): validate + scatter `rows` staged records (fvecs:
  * rec_words = d + 1, header_words = 1; fbin: d, 0) starting at file row row0 into out (ld ldo).
  * bad_dim / bad_val[row / 4096] = min(bad record row) / min(non-finite flat index). */

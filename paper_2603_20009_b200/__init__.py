@@ -72,7 +72,7 @@ def __getattr__(name):
         from . import hierarchical
         return getattr(hierarchical, name)
     if name in ("brute_force_topk", "etr_probe", "build_cluster_lists", "GroundTruth", "RecallHistory",
-                "probe_eval", "ivf_probe_search", "recall_at_k"):
+                "probe_eval", "ivf_probe_search", "recall_at_k", "wcss", "balance_stats"):
         from . import etr
         return getattr(etr, name)
     if name in ("load_vectors", "load_vectors_device", "write_fvecs", "write_fbin", "infer_format", "sha256_file",

@@ -127,6 +127,49 @@ __global__ void ingest_records_kernel(const uint32_t* __restrict__ raw, long lon
   }
 }
 
+// evaluation.wcss (evaluation.py:205-215): sum_i |x_i - c_{a_i}|^2 in double.  Warp per row
+// (f64 differences, lanes strided, shuffle tree), then per-block partials reduced in a fixed
+// order by wcss_final_kernel: deterministic run to run (the CLI report is compared for
+// determinism), equal to the reference's einsum up to f64 summation order.
+constexpr int WCSS_THREADS = 256;
+__global__ void __launch_bounds__(WCSS_THREADS) wcss_partial_kernel(const float* __restrict__ x, long long ldx,
+                                                                    const float* __restrict__ c, long long ldc,
+                                                                    const int* __restrict__ assign, long long n,
+                                                                    int d, double* __restrict__ part) {
+  __shared__ double ws[WCSS_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  const long long beg = per * blockIdx.x, end = min(n, beg + per);
+  double acc = 0.0;
+  for (long long r = beg + warp; r < end; r += WCSS_THREADS / 32) {
+    const float* xr = x + r * ldx;
+    const float* cr = c + static_cast<long long>(assign[r]) * ldc;
+    double s = 0.0;
+    for (int t = lane; t < d; t += 32) {
+      const double df = static_cast<double>(xr[t]) - static_cast<double>(cr[t]);
+      s += df * df;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    acc += s;
+  }
+  if (lane == 0) ws[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < WCSS_THREADS / 32; ++w) t += ws[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void wcss_final_kernel(const double* __restrict__ part, int parts, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < parts; ++i) t += part[i];
+    *out = t;
+  }
+}
+
 // Squared row norms over the leading `dims` columns, double accumulation rounded to
 // fp32 (preprocess.py:95-101).  One warp per row.
 __global__ void row_sq_norms_kernel(const float* __restrict__ x, long long ldx, int rows, int dims,

@@ -205,6 +205,23 @@ int skm_ingest_records(const void* raw, long long rows, int d, int rec_words, in
   return SKM_OK;
 }
 
+long long skm_wcss_workspace_bytes() { return 8LL * 1024; }
+
+int skm_wcss(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign, long long n,
+             int d, double* out, void* workspace, void* stream) {
+  if (n <= 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), as_stream(stream));
+    return e == cudaSuccess ? SKM_OK : cuda_fail(e, "wcss zero");
+  }
+  const int parts = static_cast<int>(std::min<long long>(1024, (n + 7) / 8));
+  double* part = reinterpret_cast<double*>(workspace);
+  skm::wcss_partial_kernel<<<parts, skm::WCSS_THREADS, 0, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d,
+                                                                               part);
+  skm::wcss_final_kernel<<<1, 32, 0, as_stream(stream)>>>(part, parts, out);
+  SKM_LAUNCH_CHECK("wcss");
+  return SKM_OK;
+}
+
 int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
                         long long ldo, void* stream) {
   if (rows <= 0) return SKM_OK;

@@ -337,3 +337,28 @@ def recall_at_k(result_ids, gt_row, k: int) -> float:
     if len(result_ids) < k or len(gt_row) < k:
         raise ValueError(f"need at least {k} entries on both sides")
     return np.intersect1d(result_ids[:k], gt_row[:k]).size / k
+
+
+def wcss(x, centroids, assignments, batch: int = 4096, device=None) -> float:
+    """Sum of squared distances to the assigned centroids in double (evaluation.py:205-215),
+    on the B200 (deterministic fixed-order reduction)."""
+    from .api import _h2d
+    from .config import DimensionMismatch
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    c = np.ascontiguousarray(centroids, dtype=np.float32)
+    if x.shape[1] != c.shape[1]:
+        raise DimensionMismatch("dim mismatch between vectors and centroids")
+    dev = require_cuda(device)
+    X, Cd = _h2d(x, dev), _h2d(c, dev)
+    A = torch.from_numpy(np.ascontiguousarray(assignments, dtype=np.int32)).to(dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    ws = torch.empty(int(native.load().skm_wcss_workspace_bytes()) // 8, dtype=torch.float64, device=dev)
+    native.call("skm_wcss", ptr(X), X.shape[1], ptr(Cd), Cd.shape[1], ptr(A), x.shape[0], x.shape[1], ptr(out),
+                ptr(ws), stream_handle())
+    return float(out.item())
+
+
+def balance_stats(counts) -> dict:
+    """Points-per-cluster mean and population standard deviation (evaluation.py:218-222)."""
+    counts = np.asarray(counts, dtype=np.float64)
+    return {"mean": float(counts.mean()), "std_dev": float(counts.std())}

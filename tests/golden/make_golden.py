@@ -242,7 +242,37 @@ def dataio_golden():
     return out
 
 
+def cli_golden():
+    """The reference CLI's fit / gt / eval reports on a small fbin dataset."""
+    import json
+    import tempfile
+    from superkmeans import dataio as rdio
+    from superkmeans.cli import main as rmain
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        x = make_blobs(2000, 48, 12, seed=8)
+        path = os.path.join(td, "d.fbin")
+        rdio.write_fbin(path, x)
+        rep = os.path.join(td, "fit.json")
+        model = os.path.join(td, "m.skmc")
+        assert rmain(["fit", "--input", path, "--k", "12", "--iters", "4", "--seed", "9", "--eval-queries", "50",
+                      "--out-centroids", model, "--report", rep]) == 0
+        out["fit_report"] = np.array(json.dumps(rdio.RunReport.load(rep).comparable(), sort_keys=True))
+        gtp = os.path.join(td, "g.skgt")
+        assert rmain(["gt", "--input", path, "--n-queries", "40", "--topk", "20", "--seed", "3", "--out", gtp]) == 0
+        out["gt_bytes"] = np.frombuffer(open(gtp, "rb").read(), np.uint8)
+        rep2 = os.path.join(td, "eval.json")
+        assert rmain(["eval", "--centroids", model, "--input", path, "--gt", gtp, "--n-queries", "40", "--seed", "3",
+                      "--topk", "20", "--report", rep2]) == 0
+        out["eval_report"] = np.array(json.dumps(rdio.RunReport.load(rep2).comparable(), sort_keys=True))
+        out["model_bytes"] = np.frombuffer(open(model, "rb").read(), np.uint8)
+    return out
+
+
 def main():
+    if "--only-cli" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "cli.npz"), **cli_golden())
+        return
     if "--only-dataio" in sys.argv:
         np.savez_compressed(os.path.join(HERE, "dataio.npz"), **dataio_golden())
         return
