@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int kb = 0; kb < num_k; ++kb, ++kcount) {
         const int buf = kcount & 1;
         const uint32_t use = kcount >> 1;
-        mbar_wait(&tfull[buf], use & 1);
+        mbar_wait_sleep(&tfull[buf], use & 1);
         tc_fence_after();
         const uint32_t tbase = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
                                static_cast<uint32_t>(buf * GEMM_BN + half * GEMM_HALF);
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (e < GEMM_BN) {
           const int col = t * GEMM_BN + e;
           yt[e] = col < args.N ? __ldg(args.ysq + col) : 0.0f;
-          if (MODE == GEMM_GATE && num_e) ye[e] = col < args.N ? __ldg(args.ysq_ext + col) : 0.0f;
+          if (MODE == GEMM_GATE && num_e) ye[e] = col < args.N ? (1.0f - args.cert_eps) * __ldg(args.ysq_ext + col) : 0.0f;
         }
         epi_bar_sync();
         ys_tile = yt + half * GEMM_HALF;
@@ -298,10 +298,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int my = 0;
         const int lim = row_ok ? args.N - col0 : 0;
         uint32_t tbase_e = 0;
+        const float cert_a = thr1 - (1.0f - args.cert_eps) * xs_e;  // row side of the folded test
         if (num_e) {
           // certification partial (the ext_k columns after K): distance over K + ext_k columns
           const int buf = kcount & 1;
-          mbar_wait(&tfull[buf], (kcount >> 1) & 1);
+          mbar_wait_sleep(&tfull[buf], (kcount >> 1) & 1);
           tc_fence_after();
           tbase_e = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
                     static_cast<uint32_t>(buf * GEMM_BN + half * GEMM_HALF);
@@ -317,9 +318,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int j = 0; j < 16; ++j) {
               const int jj = c * 32 + h * 16 + j;
               if (num_e) {
-                const float ys_e = ye_tile[jj];
-                const float d64 = expand_dist(__fadd_rn(acc[jj], e16[j]), xs_e, ys_e);
-                if (__fsub_rn(d64, args.cert_eps * __fadd_rn(xs_e, ys_e)) > thr1) ce |= 1u << (h * 16 + j);
+                // distance over K + ext_k columns minus the margin, folded: (1 - eps)(|x|^2 +
+                // |c|^2) - 2 ip > thr1 with the per-column term pre-scaled in shared memory
+                // (rounding of the fold is ~1e-7 relative, far inside the 3e-5 margin)
+                if (fmaf(-2.0f, __fadd_rn(acc[jj], e16[j]), ye_tile[jj]) > cert_a) ce |= 1u << (h * 16 + j);
               }
               const float dv = expand_dist(acc[jj], xs, ys_tile[jj]);
               acc[jj] = dv;
