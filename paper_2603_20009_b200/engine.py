@@ -248,11 +248,12 @@ class Workspace:
     def __init__(self, dev, n: int, k: int, d: int, cfg: KMeansConfig):
         self.dev = dev
         self.cap = min(cfg.cand_cap, (k + 31) // 32 * 32)
-        # candidate slab bounded to ~4.5 GiB (8 B per candidate); batches are whole waves of
+        # candidate slab (8 B per candidate, rows as wide as k by default so no row overflows
+        # into the dense pass) bounded to 16 GiB of the 180 GB; batches are whole waves of
         # 128-row gate-GEMM tiles over the SMs (one CTA per SM) so no launch ends on a
         # partial wave except the last
         per_wave = 128 * _sm_count(dev)
-        b = min(cfg.x_batch_device, (9 << 29) // (8 * self.cap))
+        b = min(cfg.x_batch_device, (16 << 30) // (8 * self.cap))
         b = max(per_wave, b // per_wave * per_wave) if b >= per_wave else max(128, b // 128 * 128)
         b = max(128, min(max(n, 1), b))
         self.batch = b
