@@ -53,6 +53,7 @@ from .hostmath import (
 # results bit for bit; see DESIGN.md section 3 for why it is not the default).
 TWO_PHASE_SCAN = os.environ.get("SKM_SCAN", "exact") == "spec"
 PRUNE_HIST = None  # diagnostics (tools/): device u64[nb + 1] histogram of prune blocks
+COLLECT_DIAG = os.environ.get("SKM_DIAG", "0") == "1"  # read scan diagnostics back every iteration
 # GEMM-certified tail-block-0 prunes (gemm_tf32x3.cuh, GATE ext_k): the gate GEMM also sums
 # the first 64 tail dimensions and flags candidates whose distance there exceeds fl(tau F1)
 # by more than CERT_EPS * (|x|^2 + |c|^2) over those dimensions -- far above the 3xTF32 +
@@ -463,17 +464,20 @@ def _dense_overflow(data, cents, ws, plan, glob_rows, n_over, xsq):
 
 
 def update_centroids_device(data: DeviceData, cents: Centroids, ws: Workspace, comm: Comm,
-                            sums_buf: torch.Tensor | None = None) -> np.ndarray:
+                            sums_buf: torch.Tensor | None = None, sorted_counts: np.ndarray | None = None
+                            ) -> np.ndarray:
     """Mean of member rows (f64 ordered sums), empties keep their previous centroid.
-    Returns host int64 counts (global)."""
+    Returns host int64 counts (global).  ``sorted_counts``: the cluster sort already ran
+    (ws.order / counts / offsets current) and these are its counts."""
     st = stream_handle()
     k, d = cents.k, cents.d
-    native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
-                ptr(ws.sort_ws), ws.sort_ws.numel(), st, nbytes=32.0 * data.n)
+    if sorted_counts is None:
+        native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
+                    ptr(ws.sort_ws), ws.sort_ws.numel(), st, nbytes=32.0 * data.n)
     if comm.world == 1:
         native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k, d,
                     None, 0, ptr(cents.c), cents.ld, 0, st, nbytes=4.0 * data.n * d + 4.0 * k * d)
-        return ws.counts.cpu().numpy().astype(np.int64)
+        return sorted_counts if sorted_counts is not None else ws.counts.cpu().numpy().astype(np.int64)
     # multi-GPU: local ordered sums -> one packed allreduce [sums | counts] -> finalize
     packed = sums_buf if sums_buf is not None else torch.empty(k * d + k, dtype=torch.float64, device=data.x.device)
     sums = packed[: k * d]
@@ -541,6 +545,8 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
     if comm.world > 1:
         sums_buf = torch.empty(k * d + k, dtype=torch.float64, device=dev)
     scal = torch.zeros(4, dtype=torch.float64, device=dev)
+    pin_scal = torch.empty(4, dtype=torch.float64, pin_memory=True)
+    pin_counts = torch.empty(k, dtype=torch.int32, pin_memory=True)
     have_order = False
     scan_blocks: list[int] = []
     scan_waves: list[int] = []
@@ -579,14 +585,28 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         scal[2] = ws.counters[0].to(torch.float64)
         scal[3] = ws.counters[1].to(torch.float64)
         comm.allreduce_(scal)
-        wcss, ch, sv, td = scal.tolist()
+        sorted_counts = None
+        if comm.world == 1:
+            # one host synchronisation per iteration: the stable cluster sort of the update (it
+            # does not touch the centroids, so a converged stop below is unaffected) runs first and
+            # its counts come back together with the scalars
+            native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
+                        ptr(ws.sort_ws), ws.sort_ws.numel(), stream_handle(), nbytes=32.0 * data.n)
+            pin_scal.copy_(scal, non_blocking=True)
+            pin_counts.copy_(ws.counts, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            wcss, ch, sv, td = pin_scal.tolist()
+            sorted_counts = pin_counts.numpy().astype(np.int64)
+        else:
+            wcss, ch, sv, td = scal.tolist()
         if it > 1:
             n_changed = int(round(ch))
         if pruned_iter:
-            dg = ws.diag.tolist()
-            scan_blocks.append(int(dg[0] + dg[2]))
-            scan_waves.append(int(dg[1] + dg[3]))
-            scan_diag.append([int(v) for v in dg[:6]])
+            if COLLECT_DIAG:
+                dg = ws.diag.tolist()
+                scan_blocks.append(int(dg[0] + dg[2]))
+                scan_waves.append(int(dg[1] + dg[3]))
+                scan_diag.append([int(v) for v in dg[:6]])
             survivors, touched = int(round(sv)), int(round(td))
             prune_rate = prune_rate_from_totals(survivors, n, k)
             work.tail_dims += touched
@@ -605,7 +625,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             terminated = "converged"
             break
         timer.start("update")
-        counts = update_centroids_device(data, cents, ws, comm, sums_buf)
+        counts = update_centroids_device(data, cents, ws, comm, sums_buf, sorted_counts=sorted_counts)
         have_order = True  # ws.order now lists rows grouped by their current assignment
         n_splits = apply_splits_device(cents, counts, rng_split) if cfg.split_empty else 0
         timer.stop("update")

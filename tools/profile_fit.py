@@ -8,6 +8,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
+os.environ.setdefault("SKM_DIAG", "1")  # scan diagnostics read back per iteration
+
 from bench import make_shard_device  # noqa: E402
 from paper_2603_20009_b200 import api  # noqa: E402
 from paper_2603_20009_b200.config import KMeansConfig  # noqa: E402
