@@ -162,3 +162,45 @@ def test_fit_c1_shape_vs_oracle():
     print("c1 centroid rel-L2", rel)
     if split_at is None:
         assert rel <= 2e-3
+
+
+def test_fit_c2_shape_vs_oracle():
+    """Config-2 dimensionality and k (d = 1536, k = 4096, 10 iterations, skewed blobs of the
+    reference's prune-band fixture) on a 62 500-row sample, against the oracle: the same bar as
+    the c1 test, plus final IVF recall@10 within 0.5 points."""
+    import paper_2603_20009_b200 as skb
+    from conftest import make_skewed_blobs
+    from oracle import skm_ref
+    x = make_skewed_blobs(62_500, 1536, 8192, seed=0)
+    cfg = skb.KMeansConfig(k=4096, max_iters=10, seed=0)
+    snaps = []
+    res = skb.fit(x, cfg, inspect=lambda it, ctx: snaps.append(ctx["assignments"]))
+    ref = skm_ref.fit(x, skm_ref.Params(k=4096, max_iters=10, seed=0))
+    ours_dp = [s.d_prime for s in res.stats]
+    ref_dp = [s.d_prime for s in ref.stats]
+    print("c2-shape d' ours", ours_dp, "ref", ref_dp)
+    split_at = None
+    for it, (a, s) in enumerate(zip(snaps, ref.snapshots)):
+        agree = float(np.mean(a == s["assignments"]))
+        print(f"c2-shape it{it + 1}: d' {ours_dp[it]}/{ref_dp[it]} agree {agree:.6f} "
+              f"surv {res.stats[it].survivors}/{ref.stats[it].survivors}")
+        if split_at is None and ours_dp[it] != ref_dp[it]:
+            split_at = it
+        if split_at is None:
+            assert agree >= 0.999, (it, agree)
+    if split_at is not None:
+        rate = ref.stats[split_at - 1].prune_rate_after_gemm
+        edge = min(abs(rate - cfg.prune_target_low), abs(rate - cfg.prune_target_high))
+        assert edge <= 1e-3, (split_at, rate)
+    else:
+        assert _rel_l2(res.centroids, ref.centroids) <= 1e-4
+    assert abs(res.stats[-1].wcss - ref.stats[-1].wcss) / ref.stats[-1].wcss <= 0.005
+    q = x[np.random.default_rng(7).choice(x.shape[0], 500, replace=False)]
+    gi, gd = skm_ref.brute_force_topk(x, q, 10)
+    nprobe = int(np.ceil(0.01 * cfg.k))
+    ours = skb.probe_eval(res.centroids, skb.build_cluster_lists(res.assignments, cfg.k), x, q,
+                          skb.GroundTruth(indices=gi, distances=gd, k_gt=10), nprobe, top_ks=(10,))
+    theirs = skm_ref.probe_eval(ref.centroids, skm_ref.cluster_lists(ref.assignments, cfg.k), x, q, gi, 10, nprobe,
+                                top_ks=(10,))
+    print("c2-shape recall@10 ours", ours["recall_at_10"], "ref", theirs["recall_at_10"])
+    assert abs(ours["recall_at_10"] - theirs["recall_at_10"]) <= 0.005
