@@ -53,6 +53,10 @@ int skm_gather_rows(const float* in, long long ldi, const long long* idx, int ro
 long long skm_wcss_workspace_bytes(void);
 int skm_wcss(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign, long long n,
              int d, double* out, void* workspace, void* stream);
+/* validate_vector_set's finiteness check (model.py:84-87): *first = min row-major flat index
+ * (row * cols + col) of a NaN/Inf in the leading cols columns, or ~0 when all finite. */
+int skm_first_nonfinite(const float* x, long long ldx, long long rows, int cols, unsigned long long* first,
+                        void* stream);
 /* Vector-file ingestion (dataio.py:57-112): validate + scatter `rows` staged records (fvecs:
  * rec_words = d + 1, header_words = 1; fbin: d, 0) starting at file row row0 into out (ld ldo).
  * bad_dim / bad_val[row / 4096] = min(bad record row) / min(non-finite flat index). */

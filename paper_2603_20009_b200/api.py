@@ -17,6 +17,7 @@ import torch
 
 from . import native
 from .config import (
+    NonFiniteValue,
     KMeansConfig,
     DimensionMismatch,
     RotationMatrix,
@@ -104,12 +105,34 @@ def _split(x: torch.Tensor, cols: int):
     return hi, lo
 
 
-def _h2d(x: np.ndarray, dev) -> torch.Tensor:
+def _h2d(x: np.ndarray, dev, check_finite: bool = False) -> torch.Tensor:
+    """(n, ld) device copy with zero pad columns.  ``check_finite``: validate_vector_set's
+    NaN/Inf check (model.py:84-87) on the device after the copy -- the host scan costs ~0.3 s
+    per GB, more than the fit -- raising the same NonFiniteValue(first row, col)."""
     n, d = x.shape
     out = torch.zeros((n, padded_ld(d)), dtype=torch.float32, device=dev)
     if n:
         out[:, :d].copy_(torch.from_numpy(x))
+        if check_finite:
+            first = torch.empty(1, dtype=torch.int64, device=dev)
+            native.call("skm_first_nonfinite", ptr(out), out.shape[1], n, d, ptr(first), stream_handle())
+            f = int(first.cpu().numpy().view(np.uint64)[0])
+            if f != (1 << 64) - 1:
+                from .config import NonFiniteValue
+                raise NonFiniteValue(f // d, f % d)
     return out
+
+
+def _h2d_check_only(x: np.ndarray, dev, chunk_rows: int = 1 << 18) -> None:
+    """Finiteness of a host matrix checked on the device chunk by chunk (bounded memory)."""
+    for r0 in range(0, x.shape[0], chunk_rows):
+        try:
+            _h2d(x[r0:r0 + chunk_rows], dev, check_finite=True)
+        except Exception as e:  # re-base the row of the first bad value
+            from .config import NonFiniteValue
+            if isinstance(e, NonFiniteValue):
+                raise NonFiniteValue(e.row + r0, e.col) from None
+            raise
 
 
 def _device_bytes_values(*ts) -> int:
@@ -228,13 +251,18 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
 
 def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
     """Sample, rotate, cluster and un-rotate on the B200 (core.py:417-460)."""
-    x = validate_vector_set(x)
+    x = validate_vector_set(x, check_finite=False)  # finiteness: on the device, below
     dev = require_cuda(device)
     n_total, d = x.shape
-    sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
-    xs = x if sidx is None else x[sidx]
     job = _RotationJob(d, cfg.seed)       # host PCG64 + LAPACK QR (persisted-model contract) ...
-    x_dev = _h2d(xs, dev)                  # ... overlapped with the host->device copy and iteration 1
+    if cfg.sampling_fraction == 1:
+        x_dev = _h2d(x, dev, check_finite=True)  # ... overlapped with the copy and iteration 1
+        sidx = None
+    else:
+        # the reference validates the whole input before sampling (core.py:425-436)
+        _h2d_check_only(x, dev)
+        sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
+        x_dev = _h2d(x[sidx], dev)
     res = fit_device(x_dev, d, cfg, job, inspect=inspect)
     rotation = res.rotation
     del x_dev
@@ -268,7 +296,7 @@ def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, b
 
     Rows are rotated lazily in batches; tau is seeded from the training assignment for sampled
     rows (centroid 0 otherwise), exactly like the reference."""
-    x_full = validate_vector_set(x_full)
+    x_full = validate_vector_set(x_full, check_finite=False)  # finiteness: on the device, per batch
     dev = require_cuda(device)
     n, d = x_full.shape
     if d != result.rotation.dim:
@@ -292,7 +320,11 @@ def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, b
     cfg_ws = KMeansConfig(k=k, x_batch_device=cfg.x_batch_device, cand_cap=cfg.cand_cap)
     for s0 in range(0, n, batch_rows):
         e0 = min(n, s0 + batch_rows)
-        data = DeviceData(rot.apply(_h2d(x_full[s0:e0], dev)), d)
+        try:
+            xb = _h2d(x_full[s0:e0], dev, check_finite=True)
+        except NonFiniteValue as e:
+            raise NonFiniteValue(e.row + s0, e.col) from None
+        data = DeviceData(rot.apply(xb), d)
         ws = Workspace(dev, e0 - s0, k, d, cfg_ws)
         ws.assign[: e0 - s0].copy_(torch.from_numpy(assign[s0:e0]))
         if pruned:

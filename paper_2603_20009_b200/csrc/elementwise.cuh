@@ -170,6 +170,25 @@ __global__ void wcss_final_kernel(const double* __restrict__ part, int parts, do
   }
 }
 
+// validate_vector_set's finiteness check (model.py:84-87) on the device: *first = min flat
+// row-major index (row * cols + col) of a NaN/Inf among the leading `cols` columns.
+__global__ void first_nonfinite_kernel(const float* __restrict__ x, long long ldx, long long rows, int cols,
+                                       unsigned long long* __restrict__ first) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (long long r = blockIdx.x * (long long)wpb + (threadIdx.x >> 5); r < rows; r += (long long)gridDim.x * wpb) {
+    unsigned long long f = ~0ull;
+    for (int c = lane; c < cols; c += 32)
+      if (!isfinite(x[r * ldx + c]) && f == ~0ull) f = static_cast<unsigned long long>(r) * cols + c;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, f, s);
+      f = o < f ? o : f;
+    }
+    if (lane == 0 && f != ~0ull) atomicMin(first, f);
+  }
+}
+
 // Squared row norms over the leading `dims` columns, double accumulation rounded to
 // fp32 (preprocess.py:95-101).  One warp per row.
 __global__ void row_sq_norms_kernel(const float* __restrict__ x, long long ldx, int rows, int dims,

@@ -222,6 +222,16 @@ int skm_wcss(const float* x, long long ldx, const float* centroids, long long ld
   return SKM_OK;
 }
 
+int skm_first_nonfinite(const float* x, long long ldx, long long rows, int cols, unsigned long long* first,
+                        void* stream) {
+  cudaError_t e = cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "first_nonfinite reset");
+  if (rows <= 0 || cols <= 0) return SKM_OK;
+  skm::first_nonfinite_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, first);
+  SKM_LAUNCH_CHECK("first_nonfinite");
+  return SKM_OK;
+}
+
 int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
                         long long ldo, void* stream) {
   if (rows <= 0) return SKM_OK;

@@ -91,6 +91,7 @@ _SIGS = {
     "skm_build_tails": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
     "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp], _i),
     "skm_pruned_scan": ([C.POINTER(ScanParams), _vp], _i),
+    "skm_first_nonfinite": ([_vp, _ll, _ll, _i, _vp, _vp], _i),
     "skm_wcss_workspace_bytes": ([], _ll),
     "skm_wcss": ([_vp, _ll, _vp, _ll, _vp, _ll, _i, _vp, _vp, _vp], _i),
     "skm_ingest_records": ([_vp, _ll, _i, _i, _i, _ll, _vp, _ll, _vp, _vp, _vp], _i),

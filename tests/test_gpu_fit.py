@@ -204,3 +204,27 @@ def test_fit_c2_shape_vs_oracle():
                                 top_ks=(10,))
     print("c2-shape recall@10 ours", ours["recall_at_10"], "ref", theirs["recall_at_10"])
     assert abs(ours["recall_at_10"] - theirs["recall_at_10"]) <= 0.005
+
+
+def test_nonfinite_input_rejected_on_device():
+    """validate_vector_set's NaN/Inf contract (model.py:84-87) is checked on the device after the
+    copy: same exception, same first (row, col) in row-major order, for fit (with and without
+    sampling), hierarchical_fit and final_assign (checked per batch)."""
+    import paper_2603_20009_b200 as skb
+    x = make_blobs(3000, 96, 8, seed=1)
+    bad = x.copy()
+    bad[1700, 90] = np.inf
+    bad[2200, 3] = np.nan
+    bad[1700, 5] = np.nan
+    for cfg in (skb.KMeansConfig(k=8, max_iters=2), skb.KMeansConfig(k=8, max_iters=2, sampling_fraction=0.5)):
+        with pytest.raises(skb.NonFiniteValue) as e:
+            skb.fit(bad, cfg)
+        assert (e.value.row, e.value.col) == (1700, 5)
+    with pytest.raises(skb.NonFiniteValue) as e:
+        skb.hierarchical_fit(bad, skb.HierarchicalConfig(k_total=16, seed=0))
+    assert (e.value.row, e.value.col) == (1700, 5)
+    cfg = skb.KMeansConfig(k=8, max_iters=2)
+    res = skb.fit(x, cfg)
+    with pytest.raises(skb.NonFiniteValue) as e:
+        skb.final_assign(bad, res, cfg, batch_rows=1000)
+    assert (e.value.row, e.value.col) == (1700, 5)
