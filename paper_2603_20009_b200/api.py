@@ -78,17 +78,25 @@ class DeviceRotation:
         self.r_hi, self.r_lo = _split(r, d)     # rows of R   -> X @ R^T (unrotate)
         self.rt_hi, self.rt_lo = _split(rt, d)  # rows of R^T -> X @ R   (rotate)
 
-    def apply(self, x_dev: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = False) -> torch.Tensor:
-        """out = x @ R (or x @ R^T); x_dev (n, ld) padded."""
+    def apply(self, x_dev: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = False,
+              inplace: bool = False, chunk_rows: int = 1 << 20) -> torch.Tensor:
+        """out = x @ R (or x @ R^T); x_dev (n, ld) padded.  Row chunks are split and multiplied
+        one at a time, so the extra HBM is one chunk's hi/lo operands; ``inplace`` writes each
+        chunk's result over its input rows (the operands are the split copies)."""
         n = x_dev.shape[0]
-        if out is None:
+        if inplace:
+            out = x_dev
+        elif out is None:
             out = torch.zeros((n, padded_ld(self.d)), dtype=torch.float32, device=x_dev.device)
         if n == 0:
             return out
-        x_hi, x_lo = _split(x_dev, self.d)
         b_hi, b_lo = (self.r_hi, self.r_lo) if inverse else (self.rt_hi, self.rt_lo)
-        _gemm(x_hi, x_lo, b_hi, b_lo, n, self.d, self.d, native.GEMM_STORE, out=out,
-              n_split=_store_split(n, self.d))
+        for r0 in range(0, n, chunk_rows):
+            m = min(chunk_rows, n - r0)
+            x_hi, x_lo = _split(x_dev[r0:r0 + m], self.d)
+            _gemm(x_hi, x_lo, b_hi, b_lo, m, self.d, self.d, native.GEMM_STORE, out=out[r0:r0 + m],
+                  n_split=_store_split(m, self.d))
+            del x_hi, x_lo
         return out
 
 
@@ -179,7 +187,7 @@ class DeviceFit:
 
 def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: RotationMatrix, inspect=None,
                comm: Comm | None = None, n_global: int | None = None, row_lo: int = 0, keep_data: bool = False,
-               init_rows: torch.Tensor | None = None) -> DeviceFit:
+               init_rows: torch.Tensor | None = None, consume_input: bool = False) -> DeviceFit:
     """The hot path with inputs already in HBM: rotate (tcgen05 GEMM), Lloyd loop, un-rotate.
 
     ``x_dev`` is this rank's (n_local, ld) shard (pad columns zero); with ``comm.world > 1``
@@ -214,7 +222,7 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
         rotation = rotation.get()
     timer.start("rotation")
     rot = DeviceRotation(rotation, dev)
-    xr = rot.apply(x_dev)
+    xr = rot.apply(x_dev, inplace=consume_input)  # consume_input: x_dev is a private copy
     data = DeviceData(xr, d)
     timer.stop("rotation")
     n_local = data.n
@@ -263,7 +271,7 @@ def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
         _h2d_check_only(x, dev)
         sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
         x_dev = _h2d(x[sidx], dev)
-    res = fit_device(x_dev, d, cfg, job, inspect=inspect)
+    res = fit_device(x_dev, d, cfg, job, inspect=inspect, consume_input=True)
     rotation = res.rotation
     del x_dev
     out = res.loop

@@ -9,6 +9,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200 import profiling  # noqa: E402
 from paper_2603_20009_b200.hierarchical import HierarchicalConfig, hierarchical_fit  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -23,7 +24,10 @@ cfg = HierarchicalConfig(k_total=a.k, meso_k=a.meso_k, seed=0) if a.meso_k else 
 hierarchical_fit(x[:50000], HierarchicalConfig(k_total=256, seed=0))  # warm-up
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-r = hierarchical_fit(x, cfg)
+prof = profiling.KernelTimer()
+with profiling.active(prof):
+    r = hierarchical_fit(x, cfg)
 torch.cuda.synchronize()
+print("kernels ms:", {kk: round(v["ms"], 1) for kk, v in sorted(prof.summary().items(), key=lambda kv: -kv[1]["ms"])})
 print(f"hierarchical n={a.n} d={a.d} k_total={a.k}: achieved k={r.k} wall={time.perf_counter() - t0:.3f}s "
       f"phase={ {k: round(v, 3) for k, v in r.phase_seconds.items()} }")
