@@ -70,6 +70,23 @@ def test_hierarchical_matches_reference():
     assert rel <= 1e-3, rel
 
 
+def test_hierarchical_concurrent_groups_bitwise_equal_serial(monkeypatch):
+    """The fine phase runs its groups on concurrent streams; the result must be bitwise the
+    sequential one (groups are independent fits writing disjoint slices)."""
+    import paper_2603_20009_b200 as skb
+    from paper_2603_20009_b200 import hierarchical as hmod
+    x = make_blobs(40000, 96, 300, seed=7, spread=4.0, noise=1.0)
+    cfg = dict(k_total=900, seed=3)
+    monkeypatch.setattr(hmod, "FINE_STREAMS", 1)
+    a = skb.hierarchical_fit(x, skb.HierarchicalConfig(**cfg))
+    monkeypatch.setattr(hmod, "FINE_STREAMS", 6)
+    b = skb.hierarchical_fit(x, skb.HierarchicalConfig(**cfg))
+    assert a.k == b.k
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids_rotated, b.centroids_rotated)
+    assert a.work == b.work
+
+
 def test_update_centroids_bitwise_vs_oracle():
     import paper_2603_20009_b200 as skb
     from oracle import skm_ref
