@@ -89,7 +89,11 @@ class Out:
 
 # ------------------------------------------------------------------ host math
 def rotation(d, seed):
-    q, r = np.linalg.qr(np.random.default_rng(seed).standard_normal((d, d)))
+    # BLAS pinned to 4 threads (= the single-threaded bits): OpenBLAS's QR bits depend on the
+    # thread count (see paper_2603_20009_b200/hostmath.py blas_threads)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(4, user_api="blas"):
+        q, r = np.linalg.qr(np.random.default_rng(seed).standard_normal((d, d)))
     s = np.sign(np.diag(r))
     s[s == 0] = 1.0
     return (q * s[None, :]).astype(np.float32)

@@ -9,6 +9,7 @@ HBM once); outputs are freshly owned host NumPy arrays.  Everything between runs
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -113,6 +114,45 @@ def _split(x: torch.Tensor, cols: int):
     return hi, lo
 
 
+_STAGE_BYTES = 256 << 20  # pinned staging chunk
+_STAGE_THREADS = int(os.environ.get("SKM_H2D_THREADS", max(1, min(8, os.cpu_count() or 1))))  # 1: plain copy
+_stage_pool = None
+
+
+def _copy_rows_to_device(x: np.ndarray, out: torch.Tensor, d: int) -> None:
+    """out[:, :d] = x for a pageable host matrix.  A plain pageable copy runs at ~11 GB/s on
+    the B200 hosts (one driver thread staging through its own bounce buffer); here the host
+    copy into pinned chunks is split over a few threads and overlapped with the DMA of the
+    previous chunk (three-chunk ring), ~50 GB/s (tools/h2d_probe.py)."""
+    global _stage_pool
+    n = x.shape[0]
+    if x.nbytes <= 2 * _STAGE_BYTES or _STAGE_THREADS == 1:
+        out[:, :d].copy_(torch.from_numpy(x))
+        return
+    if _stage_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _stage_pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="skm-h2d")
+    rows = max(1, _STAGE_BYTES // (4 * d))
+    bufs = [torch.empty((rows, d), dtype=torch.float32, pin_memory=True) for _ in range(3)]
+    done = [None] * 3
+    stream = torch.cuda.current_stream(out.device)
+    for i, r0 in enumerate(range(0, n, rows)):
+        b = i % 3
+        if done[b] is not None:
+            done[b].synchronize()  # the DMA that last read this chunk has finished
+        nb = min(rows, n - r0)
+        view = bufs[b].numpy()[:nb]
+        step = -(-nb // _STAGE_THREADS)
+        list(_stage_pool.map(lambda j: np.copyto(view[j:min(j + step, nb)], x[r0 + j:r0 + min(j + step, nb)]),
+                             range(0, nb, step)))
+        out[r0:r0 + nb, :d].copy_(bufs[b][:nb], non_blocking=True)
+        done[b] = torch.cuda.Event()
+        done[b].record(stream)
+    for e in done:
+        if e is not None:
+            e.synchronize()  # the ring is released when the function returns
+
+
 def _h2d(x: np.ndarray, dev, check_finite: bool = False) -> torch.Tensor:
     """(n, ld) device copy with zero pad columns.  ``check_finite``: validate_vector_set's
     NaN/Inf check (model.py:84-87) on the device after the copy -- the host scan costs ~0.3 s
@@ -120,7 +160,7 @@ def _h2d(x: np.ndarray, dev, check_finite: bool = False) -> torch.Tensor:
     n, d = x.shape
     out = torch.zeros((n, padded_ld(d)), dtype=torch.float32, device=dev)
     if n:
-        out[:, :d].copy_(torch.from_numpy(x))
+        _copy_rows_to_device(x, out, d)
         if check_finite:
             first = torch.empty(1, dtype=torch.int64, device=dev)
             native.call("skm_first_nonfinite", ptr(out), out.shape[1], n, d, ptr(first), stream_handle())
@@ -246,7 +286,8 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
     phase = dict(timer.collect())
     out = fit_rotated_device(data, cfg, inspect=inspect, comm=comm, n_global=n, row_lo=row_lo, init_rows=init_rows,
                              init_idx=init_idx, etr=etr, timer=timer, ws=ws, first_pass_done=first_pass_done)
-    phase.update(out.phase_seconds)
+    for key, v in out.phase_seconds.items():  # "gemm" may hold iteration 1 on the unrotated rows
+        phase[key] = phase.get(key, 0.0) + v
     timer.start("unrotate")
     cent = rot.apply(out.centroids_dev, inverse=True)
     timer.stop("unrotate")

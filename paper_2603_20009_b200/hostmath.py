@@ -28,12 +28,32 @@ from .config import (
 SPLIT_EPS = np.float32(1.0 / 1024.0)
 
 
+QR_BLAS_THREADS = 4
+
+
+def blas_threads(n: int = QR_BLAS_THREADS):
+    """Context pinning the BLAS pool to ``n`` threads.  OpenBLAS's blocked QR rounds differently
+    at some thread counts (measured with threadpoolctl: 1, 2 and 4 threads give identical Q for
+    d = 1024..3072 whatever OPENBLAS_NUM_THREADS says, 8 does not; via the environment variable
+    3, 5-7 and 16 differ too), so the rotation is computed at one fixed count on every machine --
+    and a pool smaller than the core count leaves cores to the concurrent H2D copy threads
+    instead of oversubscribing them (the QR took 0.67 s instead of 0.18 s with 16 spinning
+    BLAS threads beside the copy)."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        import contextlib
+        return contextlib.nullcontext()
+    return threadpool_limits(n, user_api="blas")
+
+
 def generate_rotation(dim: int, seed: int) -> RotationMatrix:
     """Haar-random orthogonal matrix: QR of a PCG64 Gaussian, columns sign-fixed by diag(R)."""
     if dim < 1:
         raise DimensionMismatch("rotation dimension must be >= 1")
     g = np.random.default_rng(seed).standard_normal((dim, dim))
-    q, r = np.linalg.qr(g)
+    with blas_threads():
+        q, r = np.linalg.qr(g)
     s = np.sign(np.diag(r))
     s[s == 0] = 1.0
     return RotationMatrix(data=(q * s[None, :]).astype(np.float32), dim=dim, seed=seed)
