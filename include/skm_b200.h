@@ -104,10 +104,10 @@ typedef struct skm_gemm_params {
   int* assign; float* tau;     /* ARGMIN, n_split == 1 */
   unsigned long long* keys;    /* ARGMIN, n_split > 1: pre-filled with ~0ull */
   const float* thr;            /* GATE: per-row threshold (keep iff dist <= thr) */
-  int* cand_idx; float* cand_val; int* cand_cnt; int cand_cap;
+  int* cand; int* cand_cnt; int cand_cap;  /* cand: [M][cand_cap] records {index, float bits} */
   long long row_offset;        /* ARGMIN/GATE output row offset */
   /* GATE, optional: ext_k (64) more columns after K certify tail-block-0 prunes; certified
-   * candidates carry bit 31 in cand_idx.  xsq_ext/ysq_ext: norms over K + ext_k columns,
+   * candidates carry bit 31 in the record's index.  xsq_ext/ysq_ext: norms over K + ext_k columns,
    * thr1: per-row fl(tau * F[1]), cert_eps: margin relative to xsq_ext + ysq_ext. */
   int ext_k; const float* xsq_ext; const float* ysq_ext; const float* thr1; float cert_eps;
 } skm_gemm_params;
@@ -138,7 +138,7 @@ int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n
 int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream);
 int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, void* stream);
 typedef struct skm_scan_params {
-  const int* cand_idx; const float* cand_val; const int* cand_cnt; int cap;  /* list mode */
+  const int* cand; const int* cand_cnt; int cap;  /* list mode: [rows][cap] {index, float bits} */
   const float* dense; long long ld_dense; const int* dense_row; int k;       /* dense mode */
   const int* rows; int n_rows; long long row0;  /* batch-local rows to scan (NULL = 0..n_rows-1) */
   const int* row_map;                          /* optional global row of each batch-local row */

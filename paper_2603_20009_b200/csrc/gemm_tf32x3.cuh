@@ -13,8 +13,11 @@
 //   warp 0      TMA producer: A_hi, A_lo, B_hi, B_lo k-block tiles (SWIZZLE_128B, K-major)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..17 epilogue: warp w reads TMEM lane quadrant (w%4) and column slice (w-2)/4;
-//               thread = one output row x 64 columns, running sums in registers.
-// A CTA owns one 128-row M tile and walks a contiguous range of 256-wide N tiles in
+//               thread = one output row x BN/4 columns, running sums in registers.
+// The 512 TMEM columns hold 512/BN k-block partials in flight: BN = 256 for STORE / DIST /
+// ARGMIN, BN = 128 for GATE, whose per-tile gate pass would otherwise hold the MMA issuer
+// (two partials in flight) and whose 64 running sums spilled at the 96-register cap.
+// A CTA owns one 128-row M tile and walks a contiguous range of BN-wide N tiles in
 // ascending order, so per-row reductions (argmin, candidate emission) see columns in
 // ascending index order like the reference's bank loop (core.py:183-190, 243-260).
 #pragma once
@@ -40,8 +43,7 @@ struct GemmArgs {
   float* tau;
   unsigned long long* keys;   // ARGMIN (grid.y > 1): atomicMin((dist_bits<<32)|col)
   const float* thr;           // GATE: per-row threshold
-  int* cand_idx;              // GATE: per-row candidate slab [M][cap]
-  float* cand_val;
+  int2* cand;                 // GATE: per-row candidate slab [M][cap] of {index, float bits}
   int* cand_cnt;              // GATE: per-row count (may exceed cap -> overflow)
   int cand_cap;
   long long row_offset;       // GATE/ARGMIN: added to the row index when writing outputs
@@ -54,26 +56,37 @@ struct GemmArgs {
   const float* ysq_ext;       // per-column norm over K + ext_k columns
   const float* thr1;          // per-row fl(tau * F[1])
   float cert_eps;             // margin: eps * (xsq_ext + ysq_ext)
+  int dbg;                    // experiments: 1 = GATE drains partials only (no gate phase)
 };
 constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 
+#ifndef SKM_GATE_LDS
+#define SKM_GATE_LDS 1       // GATE reads the staged column norms with explicit ld.shared.v4
+#endif
+#ifndef SKM_GATE_PREFETCH
+#define SKM_GATE_PREFETCH 1  // GATE loads the next tile's column norms during the drains
+#endif
+
 constexpr int GEMM_BM = 128;
-constexpr int GEMM_BN = 256;
-constexpr int GEMM_BK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int GEMM_BN = 256;       // STORE / DIST / ARGMIN tile width
+constexpr int GEMM_BN_GATE = 128;  // GATE tile width: 4-deep TMEM partial ring, 32 sums per thread
+constexpr int GEMM_BK = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int GEMM_EPI_WARPS = 16;
 constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;
-constexpr int GEMM_PARTS = GEMM_EPI_WARPS / 4;      // column slices per TMEM lane quadrant
-constexpr int GEMM_HALF = GEMM_BN / GEMM_PARTS;     // columns per epilogue thread
+constexpr int GEMM_PARTS = GEMM_EPI_WARPS / 4;  // column slices per TMEM lane quadrant
+constexpr int GEMM_TMEM_COLS = 512;             // the whole TMEM of the SM (one CTA per SM)
 
-template <int STAGES>
+template <int STAGES, int BN>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 4;
-  static constexpr int B_BYTES = GEMM_BN * GEMM_BK * 4;
+  static constexpr int B_BYTES = BN * GEMM_BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
-  static constexpr int XCHG_BYTES = 2 * GEMM_PARTS * GEMM_BM * 4 + 4 * GEMM_BN * 4;  // slice exchange + ysq tiles (x2)
+  static constexpr int NBUF = GEMM_TMEM_COLS / BN;  // k-block partials in flight
+  static constexpr int HALF = BN / GEMM_PARTS;      // columns per epilogue thread
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * NBUF) + 16;
+  // slice exchange (double buffered by tile parity) + column-norm tiles (ysq, ysq_ext; x2)
+  static constexpr int XCHG_BYTES = 2 * GEMM_PARTS * GEMM_BM * 4 + 4 * BN * 4;
   static constexpr int TOTAL = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + XCHG_BYTES;
-  static constexpr int TMEM_COLS = 2 * GEMM_BN;  // two k-block partial buffers
 };
 
 __device__ __forceinline__ float expand_dist(float acc, float xs, float ys) {
@@ -86,27 +99,39 @@ __device__ __forceinline__ void epi_bar_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
 }
 
-template <int STAGES, int MODE>
+__device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float f4_get(const float4& v, int q) {
+  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
+}
+
+template <int STAGES, int MODE, int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                        const __grid_constant__ CUtensorMap tE_A_hi, const __grid_constant__ CUtensorMap tE_A_lo,
                        const __grid_constant__ CUtensorMap tE_B_hi, const __grid_constant__ CUtensorMap tE_B_lo,
                        const GemmArgs args) {
-  using L = GemmSmem<STAGES>;
+  using L = GemmSmem<STAGES, BN>;
+  constexpr int NBUF = L::NBUF;
+  constexpr int HALF = L::HALF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
   int* xchg = reinterpret_cast<int*>(smem + STAGES * L::STAGE_BYTES + L::BAR_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * GEMM_BM;
-  const int n_tiles = (args.N + GEMM_BN - 1) / GEMM_BN;
+  const int n_tiles = (args.N + BN - 1) / BN;
   const int t_begin = blockIdx.y * args.tiles_per_cta;
   const int t_end = min(n_tiles, t_begin + args.tiles_per_cta);
   const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
@@ -122,13 +147,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NBUF; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], GEMM_EPI_WARPS);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc<GEMM_TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -141,7 +166,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t ph = 0;
 #pragma unroll 1
       for (int t = t_begin; t < t_end; ++t) {
-        const int n0 = t * GEMM_BN;
+        const int n0 = t * BN;
 #pragma unroll 1
         for (int kb = 0; kb < num_k + num_e; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -160,10 +185,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && t_begin < t_end && num_k > 0) {
-      constexpr uint32_t idesc = idesc_tf32(GEMM_BM, GEMM_BN);
+      constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN);
       int s = 0;
       uint32_t ph = 0;
-      uint32_t kcount = 0;  // global k-block counter -> TMEM buffer ring
+      uint32_t kcount = 0;  // global partial counter -> TMEM buffer ring
 #pragma unroll 1
       for (int t = t_begin; t < t_end; ++t) {
 #pragma unroll 1
@@ -171,12 +196,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // extension k-blocks after the first one keep accumulating into the same partial
           const bool cont = kb > num_k;
           const bool last_of_partial = kb < num_k || kb == num_k + num_e - 1;
-          const int buf = kcount & 1;
-          const uint32_t use = kcount >> 1;
+          const int buf = kcount % NBUF;
+          const uint32_t use = kcount / NBUF;
           if (!cont) mbar_wait(&tempty[buf], (use & 1) ^ 1);
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * GEMM_BN);
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
           const uint32_t base = smem_u32(smem + s * L::STAGE_BYTES);
           const uint64_t a_hi = sw128_kmajor_desc(base);
           const uint64_t a_lo = sw128_kmajor_desc(base + L::A_BYTES);
@@ -206,10 +231,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int eq = warp & 3;            // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;           // column slice of the 256-wide tile
+    const int half = ew >> 2;           // column slice of the tile
     const int r_local = eq * 32 + lane;
     const int row = m0 + r_local;
     const bool row_ok = row < args.M;
+    const int e_thr = threadIdx.x - 64;  // epilogue thread index: the first BN stage column norms
     float xs = 0.0f, thr = 0.0f;
     if constexpr (MODE == GEMM_DIST || MODE == GEMM_ARGMIN || MODE == GEMM_GATE) {
       if (row_ok) xs = args.xsq[row];
@@ -222,61 +248,81 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         thr1 = args.thr1[row];
       }
     }
+    // column norms of the next tile, loaded into registers one tile ahead (the loads are in
+    // flight during the tile's k-block drains) and staged in shared memory at the tile end
+    float ys_next = 0.0f, ye_next = 0.0f;
+    auto load_norms = [&](int t) {
+      if (e_thr < BN) {
+        const int col = t * BN + e_thr;
+        ys_next = col < args.N ? __ldg(args.ysq + col) : 0.0f;
+        if (MODE == GEMM_GATE && num_e)
+          ye_next = col < args.N ? (1.0f - args.cert_eps) * __ldg(args.ysq_ext + col) : 0.0f;
+      }
+    };
+    // GATE: column norms prefetched one tile ahead; DIST / ARGMIN (measured faster that way)
+    // load them at the tile end
+    constexpr bool kPrefetchNorms = MODE == GEMM_GATE && SKM_GATE_PREFETCH;
+    if constexpr (kPrefetchNorms) {
+      if (t_begin < t_end) load_norms(t_begin);
+    }
     float best = __int_as_float(0x7f800000);
     int best_j = 0x7fffffff;
     int cnt = 0;
     const long long out_row = static_cast<long long>(row) + args.row_offset;
-    float acc[GEMM_HALF];
+    float acc[HALF];
     uint32_t kcount = 0;
 #pragma unroll 1
     for (int t = t_begin; t < t_end; ++t) {
 #pragma unroll 1
       for (int kb = 0; kb < num_k; ++kb, ++kcount) {
-        const int buf = kcount & 1;
-        const uint32_t use = kcount >> 1;
-        mbar_wait_sleep(&tfull[buf], use & 1);
+        const int buf = kcount % NBUF;
+        mbar_wait_sleep(&tfull[buf], (kcount / NBUF) & 1);
         tc_fence_after();
         const uint32_t tbase = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
-                               static_cast<uint32_t>(buf * GEMM_BN + half * GEMM_HALF);
+                               static_cast<uint32_t>(buf * BN + half * HALF);
 #pragma unroll
-        for (int c = 0; c < GEMM_HALF / 16; ++c)
+        for (int c = 0; c < HALF / 16; ++c)
           tmem_ld16_accum(tbase + c * 16, *reinterpret_cast<float(*)[16]>(&acc[c * 16]), kb == 0);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
-      // ---- tile complete: acc holds columns [col0, col0 + GEMM_HALF)
-      const int col0 = t * GEMM_BN + half * GEMM_HALF;
+      // ---- tile complete: acc holds columns [col0, col0 + HALF)
+      const int col0 = t * BN + half * HALF;
+      uint32_t ys_s = 0, ye_s = 0;  // shared addresses of this thread's slice of the norm tiles
       const float* ys_tile = nullptr;
       const float* ye_tile = nullptr;
       if constexpr (MODE != GEMM_STORE) {
-        // stage this tile's column norms in shared memory (double buffered by tile parity)
-        float* yt = reinterpret_cast<float*>(xchg + 2 * GEMM_PARTS * GEMM_BM) + (t & 1) * GEMM_BN;
-        float* ye = yt + 2 * GEMM_BN;
-        const int e = threadIdx.x - 64;
-        if (e < GEMM_BN) {
-          const int col = t * GEMM_BN + e;
-          yt[e] = col < args.N ? __ldg(args.ysq + col) : 0.0f;
-          if (MODE == GEMM_GATE && num_e) ye[e] = col < args.N ? (1.0f - args.cert_eps) * __ldg(args.ysq_ext + col) : 0.0f;
+        float* yt = reinterpret_cast<float*>(xchg + 2 * GEMM_PARTS * GEMM_BM) + (t & 1) * BN;
+        float* ye = yt + 2 * BN;
+        if constexpr (!kPrefetchNorms) load_norms(t);
+        if (e_thr < BN) {
+          yt[e_thr] = ys_next;
+          if (MODE == GEMM_GATE && num_e) ye[e_thr] = ye_next;
+        }
+        if constexpr (kPrefetchNorms) {
+          if (t + 1 < t_end) load_norms(t + 1);
         }
         epi_bar_sync();
-        ys_tile = yt + half * GEMM_HALF;
-        ye_tile = ye + half * GEMM_HALF;
+        ys_s = smem_u32(yt + half * HALF);
+        ye_s = smem_u32(ye + half * HALF);
+        ys_tile = yt + half * HALF;
+        ye_tile = ye + half * HALF;
       }
       if constexpr (MODE == GEMM_STORE || MODE == GEMM_DIST) {
         if (row_ok && col0 < args.N) {
           if constexpr (MODE == GEMM_DIST) {
 #pragma unroll
-            for (int j = 0; j < GEMM_HALF; ++j) acc[j] = expand_dist(acc[j], xs, ys_tile[j]);
+            for (int j = 0; j < HALF; ++j) acc[j] = expand_dist(acc[j], xs, ys_tile[j]);
           }
           float* o = args.out + static_cast<long long>(row) * args.ldo + col0;
-          if (col0 + GEMM_HALF <= args.N && (args.ldo & 3) == 0) {
+          if (col0 + HALF <= args.N && (args.ldo & 3) == 0) {
 #pragma unroll
-            for (int j = 0; j < GEMM_HALF; j += 4)
+            for (int j = 0; j < HALF; j += 4)
               *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
           } else {
 #pragma unroll
-            for (int j = 0; j < GEMM_HALF; ++j)
+            for (int j = 0; j < HALF; ++j)
               if (col0 + j < args.N) o[j] = acc[j];
           }
         }
@@ -286,78 +332,102 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float bv = best;
           int bl = -1;
 #pragma unroll
-          for (int j = 0; j < GEMM_HALF; ++j) {
+          for (int j = 0; j < HALF; ++j) {
             const float dv = expand_dist(acc[j], xs, ys_tile[j]);
             if (j < lim && dv < bv) { bv = dv; bl = j; }
           }
           if (bl >= 0) { best = bv; best_j = col0 + bl; }
         }
       } else if constexpr (MODE == GEMM_GATE) {
-        uint32_t mask[GEMM_HALF / 32];
-        uint32_t cert[GEMM_HALF / 32] = {};
-        int my = 0;
-        const int lim = row_ok ? args.N - col0 : 0;
-        uint32_t tbase_e = 0;
-        const float cert_a = thr1 - (1.0f - args.cert_eps) * xs_e;  // row side of the folded test
+        constexpr int W = HALF / 32;  // 32-column mask words per thread
+        uint32_t cert[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) cert[w] = 0u;
         if (num_e) {
-          // certification partial (the ext_k columns after K): distance over K + ext_k columns
-          const int buf = kcount & 1;
-          mbar_wait_sleep(&tfull[buf], (kcount >> 1) & 1);
+          // certification partial (the ext_k columns after K): consumed first so its TMEM
+          // buffer returns to the MMA issuer before the gate pass
+          const int buf = kcount % NBUF;
+          mbar_wait_sleep(&tfull[buf], (kcount / NBUF) & 1);
           tc_fence_after();
-          tbase_e = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
-                    static_cast<uint32_t>(buf * GEMM_BN + half * GEMM_HALF);
-        }
+          const uint32_t tb = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
+                              static_cast<uint32_t>(buf * BN + half * HALF);
+          if (args.dbg != 1) {
+            // distance over K + ext_k columns minus the margin, folded: (1 - eps)(|x|^2 + |c|^2)
+            // - 2 ip > thr1 with the per-column term pre-scaled in shared memory (rounding of
+            // the fold is ~1e-7 relative, far inside the 3e-5 margin)
+            const float cert_a = thr1 - (1.0f - args.cert_eps) * xs_e;
 #pragma unroll
-        for (int c = 0; c < GEMM_HALF / 32; ++c) {
-          uint32_t m = 0, ce = 0;
+            for (int c = 0; c < HALF / 16; ++c) {
+              float e16[16];
+              tmem_ld16(tb + c * 16, e16);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float e16[16];
-            if (num_e) tmem_ld16(tbase_e + c * 32 + h * 16, e16);
+              for (int j = 0; j < 16; j += 4) {
+#if SKM_GATE_LDS
+                const float4 y4 = lds_f32x4(ye_s + 4 * (c * 16 + j));
+#else
+                const float4 y4 = *reinterpret_cast<const float4*>(ye_tile + c * 16 + j);
+#endif
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int jj = c * 32 + h * 16 + j;
-              if (num_e) {
-                // distance over K + ext_k columns minus the margin, folded: (1 - eps)(|x|^2 +
-                // |c|^2) - 2 ip > thr1 with the per-column term pre-scaled in shared memory
-                // (rounding of the fold is ~1e-7 relative, far inside the 3e-5 margin)
-                if (fmaf(-2.0f, __fadd_rn(acc[jj], e16[j]), ye_tile[jj]) > cert_a) ce |= 1u << (h * 16 + j);
+                for (int q = 0; q < 4; ++q) {
+                  const int jj = c * 16 + j + q;
+                  if (fmaf(-2.0f, __fadd_rn(acc[jj], e16[j + q]), f4_get(y4, q)) > cert_a)
+                    cert[jj >> 5] |= 1u << (jj & 31);
+                }
               }
-              const float dv = expand_dist(acc[jj], xs, ys_tile[jj]);
-              acc[jj] = dv;
-              m |= ((jj < lim) && !(dv > thr)) ? (1u << (h * 16 + j)) : 0u;
             }
           }
-          mask[c] = m;
-          cert[c] = ce;
-          my += __popc(m);
-        }
-        if (num_e) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[kcount & 1]);
+          if (lane == 0) mbar_arrive(&tempty[buf]);
           ++kcount;
         }
-        // order the column slices of this row: slice 0 first
-        xchg[half * GEMM_BM + r_local] = my;
+        if (args.dbg == 1) continue;
+        const int lim = row_ok ? args.N - col0 : 0;
+        uint32_t mask[W];
+        int my = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+#if SKM_GATE_LDS
+            const float4 y4 = lds_f32x4(ys_s + 4 * (w * 32 + j));
+#else
+            const float4 y4 = *reinterpret_cast<const float4*>(ys_tile + w * 32 + j);
+#endif
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int jj = w * 32 + j + q;
+              const float dv = expand_dist(acc[jj], xs, f4_get(y4, q));
+              acc[jj] = dv;
+              m |= (dv > thr ? 0u : 1u) << (j + q);
+            }
+          }
+          const int l = lim - w * 32;
+          m &= l >= 32 ? 0xffffffffu : (l <= 0 ? 0u : ((1u << l) - 1u));
+          mask[w] = m;
+          my += __popc(m);
+        }
+        // order the column slices of this row: slice 0 first (exchange double buffered by tile
+        // parity, so one barrier per tile orders both the writes and the next tile's reuse)
+        int* xc = xchg + (t & 1) * GEMM_PARTS * GEMM_BM;
+        xc[half * GEMM_BM + r_local] = my;
         epi_bar_sync();
         int before = 0, total = 0;
 #pragma unroll
         for (int q = 0; q < GEMM_PARTS; ++q) {
-          const int cq = xchg[q * GEMM_BM + r_local];
+          const int cq = xc[q * GEMM_BM + r_local];
           before += (q < half) ? cq : 0;
           total += cq;
         }
-        epi_bar_sync();
         int pos = cnt + before;
-        if (row_ok) {
-          int* ci = args.cand_idx + out_row * args.cand_cap;
-          float* cv = args.cand_val + out_row * args.cand_cap;
+        if (row_ok && args.dbg != 2) {
+          int2* cr = args.cand + out_row * args.cand_cap;  // one 8-byte record per candidate
 #pragma unroll
-          for (int c = 0; c < GEMM_HALF / 32; ++c) {
+          for (int w = 0; w < W; ++w) {
             // skip empty 4-column groups (about a tenth of the columns pass the gate); static
             // register indices keep acc[] out of local memory
-            const uint32_t m = mask[c];
+            const uint32_t m = mask[w];
             if (m == 0) continue;
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
@@ -367,8 +437,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int j = 4 * g + jj;
                 if ((m >> j) & 1u) {
                   if (pos < args.cand_cap) {
-                    ci[pos] = (col0 + c * 32 + j) | (((cert[c] >> j) & 1u) ? CAND_CERT0 : 0);
-                    cv[pos] = acc[c * 32 + j];
+                    cr[pos] = make_int2((col0 + w * 32 + j) | (((cert[w] >> j) & 1u) ? CAND_CERT0 : 0),
+                                        __float_as_int(acc[w * 32 + j]));
                   }
                   ++pos;
                 }
@@ -414,7 +484,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+    tmem_dealloc<GEMM_TMEM_COLS>(tmem_base);
   }
 }
 

@@ -47,8 +47,7 @@ constexpr int SCAN_WARPS = SKM_SCAN_WARPS;     // warps per CTA
 
 struct ScanArgs {
   // candidate source (list mode)
-  const int* cand_idx;
-  const float* cand_val;
+  const int2* cand;  // [rows][cap] {centroid index | CAND_CERT0, float bits of the front distance}
   const int* cand_cnt;
   int cap;
   // candidate source (dense mode): row r reads dense[dense_row[r] * ld_dense + j], j < k
@@ -231,13 +230,11 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     int spos = -1, snxt = 0, sb = 0, sver = -1;
     float srun = 0.0f;
     const float* dense_row = nullptr;
-    const int* lidx = nullptr;
-    const float* lval = nullptr;
+    const int2* lrec = nullptr;
     if constexpr (DENSE) {
       dense_row = a.dense + static_cast<long long>(a.dense_row[rl]) * a.ld_dense;
     } else {
-      lidx = a.cand_idx + static_cast<long long>(rl) * a.cap;
-      lval = a.cand_val + static_cast<long long>(rl) * a.cap;
+      lrec = a.cand + static_cast<long long>(rl) * a.cap;
     }
     cp_async_wait_all();
     __syncwarp();
@@ -255,8 +252,9 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             j = e;
             p = dense_row[e];
           } else {
-            j = lidx[e];
-            p = lval[e];
+            const int2 rec = lrec[e];
+            j = rec.x;
+            p = __int_as_float(rec.y);
             cert = j < 0;  // CAND_CERT0: certified block-0 prune (gemm_tf32x3.cuh)
             j &= 0x7fffffff;
           }

@@ -78,10 +78,9 @@ int make_tmap(CUtensorMap* m, const float* ptr, long long rows, long long cols, 
   return SKM_OK;
 }
 
-template <int STAGES, int MODE>
+template <int STAGES, int MODE, int BN>
 int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
-  constexpr int BN = skm::GEMM_BN;
-  using L = skm::GemmSmem<STAGES>;
+  using L = skm::GemmSmem<STAGES, BN>;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc;
   if ((rc = make_tmap(&ta_hi, p->a_hi, p->M, p->K, p->lda, skm::GEMM_BM))) return rc;
@@ -98,7 +97,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
     if ((rc = make_tmap(&te_b_hi, p->b_hi + p->K, p->N, ext_k, p->ldb, BN))) return rc;
     if ((rc = make_tmap(&te_b_lo, p->b_lo + p->K, p->N, ext_k, p->ldb, BN))) return rc;
   }
-  auto kern = skm::gemm_tf32x3_kernel<STAGES, MODE>;
+  auto kern = skm::gemm_tf32x3_kernel<STAGES, MODE, BN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
@@ -121,8 +120,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   a.tau = p->tau;
   a.keys = p->keys;
   a.thr = p->thr;
-  a.cand_idx = p->cand_idx;
-  a.cand_val = p->cand_val;
+  a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
   a.cand_cnt = p->cand_cnt;
   a.cand_cap = p->cand_cap;
   a.row_offset = p->row_offset;
@@ -131,6 +129,11 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   a.ysq_ext = p->ysq_ext;
   a.thr1 = p->thr1;
   a.cert_eps = p->cert_eps;
+  {
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("SKM_GEMM_DBG"); dbg = e ? atoi(e) : 0; }
+    a.dbg = dbg;
+  }
   if (MODE == skm::GEMM_ARGMIN && split > 1 && !p->keys) return fail(SKM_E_ARG, "ARGMIN with n_split>1 needs keys");
   if (MODE == skm::GEMM_GATE && split > 1) return fail(SKM_E_ARG, "GATE requires n_split == 1");
   dim3 grid((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM, split);
@@ -421,10 +424,10 @@ int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream) {
   if (p->K <= 0) return fail(SKM_E_ARG, "gemm: K must be > 0");
   cudaStream_t st = as_stream(stream);
   switch (p->mode) {
-    case SKM_GEMM_STORE: return launch_gemm<2, skm::GEMM_STORE>(p, st);
-    case SKM_GEMM_DIST: return launch_gemm<2, skm::GEMM_DIST>(p, st);
-    case SKM_GEMM_ARGMIN: return launch_gemm<2, skm::GEMM_ARGMIN>(p, st);
-    case SKM_GEMM_GATE: return launch_gemm<2, skm::GEMM_GATE>(p, st);
+    case SKM_GEMM_STORE: return launch_gemm<2, skm::GEMM_STORE, skm::GEMM_BN>(p, st);
+    case SKM_GEMM_DIST: return launch_gemm<2, skm::GEMM_DIST, skm::GEMM_BN>(p, st);
+    case SKM_GEMM_ARGMIN: return launch_gemm<2, skm::GEMM_ARGMIN, skm::GEMM_BN>(p, st);
+    case SKM_GEMM_GATE: return launch_gemm<3, skm::GEMM_GATE, skm::GEMM_BN_GATE>(p, st);
     default: return fail(SKM_E_ARG, "gemm: unknown mode");
   }
 }
@@ -465,8 +468,7 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   if (p->n_rows <= 0) return SKM_OK;
   if (p->nb <= 0 || p->nb > skm::SCAN_NB_MAX) return fail(SKM_E_ARG, "pruned_scan: tail block count out of range");
   skm::ScanArgs a{};
-  a.cand_idx = p->cand_idx;
-  a.cand_val = p->cand_val;
+  a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
   a.cand_cnt = p->cand_cnt;
   a.cap = p->cap;
   a.dense = p->dense;
@@ -570,8 +572,7 @@ int skm_pruned_scan2(const skm_scan_params* p, const float* tails_blk, void* scr
       (reinterpret_cast<uintptr_t>(outcome + n * static_cast<long long>(p->cap)) + 63) & ~uintptr_t(63));
 
   skm::ScanArgs a{};
-  a.cand_idx = p->cand_idx;
-  a.cand_val = p->cand_val;
+  a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
   a.cand_cnt = p->cand_cnt;
   a.cap = p->cap;
   a.k = p->k;

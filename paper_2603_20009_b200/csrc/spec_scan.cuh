@@ -211,18 +211,18 @@ __global__ void __launch_bounds__(PREP_WARPS * 32) row_prep_kernel(const ScanArg
       D.best_r = R.st_best[rl];
     }
     D.t_hi = D.t_lo;
-    const int* lidx = a.cand_idx + static_cast<long long>(rl) * cap;
+    const int2* lrec = a.cand + static_cast<long long>(rl) * cap;
     int spos = -1;
     for (int e0 = D.pos_in; e0 < n_src; e0 += 32) {
       const int e = e0 + lane;
-      const int j = (e < n_src) ? lidx[e] : 0x7fffffff;
+      const int j = (e < n_src) ? lrec[e].x : 0x7fffffff;
       const unsigned hit = __ballot_sync(FULL, j == a0);
       if (hit) { spos = e0 + __ffs(hit) - 1; break; }
       if (__ballot_sync(FULL, j > a0)) break;
     }
     if (spos >= 0) {
       int* lout = R.outcome + static_cast<long long>(rl) * cap;
-      const float p0 = a.cand_val[static_cast<long long>(rl) * cap + spos];
+      const float p0 = __int_as_float(lrec[spos].y);
       const float t = D.t_lo;
       if (!(p0 > __fmul_rn(t, f0))) {
         __syncwarp();
@@ -609,8 +609,9 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 1)
       if (f_src < f_n && qt - qh <= SPEC_QUEUE - 32) {
         const int e = f_src + lane;
         if (e < f_n) {
-          lj = a.cand_idx[static_cast<long long>(f_rl) * cap + e];
-          lp = a.cand_val[static_cast<long long>(f_rl) * cap + e];
+          const int2 rec = a.cand[static_cast<long long>(f_rl) * cap + e];
+          lj = rec.x;
+          lp = __int_as_float(rec.y);
         }
         chunk_base = f_src;
         f_src += 32;
@@ -960,8 +961,9 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 1)
         if (f_src < f_n && qt - qh <= SPEC_QUEUE - 32) {
           const int e = f_src + lane;
           if (e < f_n) {
-            lj = a.cand_idx[static_cast<long long>(f_rl) * cap + e];
-            lp = a.cand_val[static_cast<long long>(f_rl) * cap + e];
+            const int2 rec = a.cand[static_cast<long long>(f_rl) * cap + e];
+            lj = rec.x;
+            lp = __int_as_float(rec.y);
           }
           chunk_base = f_src;
           f_src += 32;

@@ -265,8 +265,7 @@ class Workspace:
         self.tau = torch.full((nn,), float("inf"), dtype=f32, device=dev)
         self.thr = torch.empty(nn, dtype=f32, device=dev)
         self.keys = None
-        self.cand_idx = torch.empty((b, self.cap), dtype=i32, device=dev)
-        self.cand_val = torch.empty((b, self.cap), dtype=f32, device=dev)
+        self.cand = torch.empty((b, self.cap, 2), dtype=i32, device=dev)  # {index, float bits} records
         self.cand_cnt = torch.empty(b, dtype=i32, device=dev)
         self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
         self.work = torch.zeros(256, dtype=torch.int32, device=dev)  # per-SM scan row queues
@@ -394,17 +393,16 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
             cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=cents.ysq_ext, thr1=ws.bthr1[:bn],
                         cert_eps=CERT_EPS) if ext else {}
             _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
-                  ysq=cents.ysq, thr=ws.bthr[:bn], cand_idx=ws.cand_idx, cand_val=ws.cand_val, cand_cnt=ws.cand_cnt,
+                  ysq=cents.ysq, thr=ws.bthr[:bn], cand=ws.cand, cand_cnt=ws.cand_cnt,
                   cand_cap=ws.cap, **cert)
             sp.row_map = rmap.data_ptr()
         else:
             cert = dict(ext_k=ext, xsq_ext=xsq_ext[r:r + bn], ysq_ext=cents.ysq_ext, thr1=ws.thr1[r:r + bn],
                         cert_eps=CERT_EPS) if ext else {}
             _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE,
-                  xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand_idx=ws.cand_idx,
-                  cand_val=ws.cand_val, cand_cnt=ws.cand_cnt, cand_cap=ws.cap, **cert)
-        sp.cand_idx, sp.cand_val, sp.cand_cnt, sp.cap = (ws.cand_idx.data_ptr(), ws.cand_val.data_ptr(),
-                                                          ws.cand_cnt.data_ptr(), ws.cap)
+                  xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand=ws.cand,
+                  cand_cnt=ws.cand_cnt, cand_cap=ws.cap, **cert)
+        sp.cand, sp.cand_cnt, sp.cap = ws.cand.data_ptr(), ws.cand_cnt.data_ptr(), ws.cap
         sp.k, sp.n_rows, sp.row0 = k, bn, r
         sp.work = ws.work.data_ptr()
         sp.x, sp.ldx = data.x.data_ptr(), data.ld

@@ -39,7 +39,7 @@ class GemmParams(C.Structure):
         ("assign", _vp), ("tau", _vp),
         ("keys", _vp),
         ("thr", _vp),
-        ("cand_idx", _vp), ("cand_val", _vp), ("cand_cnt", _vp), ("cand_cap", _i),
+        ("cand", _vp), ("cand_cnt", _vp), ("cand_cap", _i),
         ("row_offset", _ll),
         ("ext_k", _i), ("xsq_ext", _vp), ("ysq_ext", _vp), ("thr1", _vp), ("cert_eps", _f),
     ]
@@ -47,7 +47,7 @@ class GemmParams(C.Structure):
 
 class ScanParams(C.Structure):
     _fields_ = [
-        ("cand_idx", _vp), ("cand_val", _vp), ("cand_cnt", _vp), ("cap", _i),
+        ("cand", _vp), ("cand_cnt", _vp), ("cap", _i),
         ("dense", _vp), ("ld_dense", _ll), ("dense_row", _vp), ("k", _i),
         ("rows", _vp), ("n_rows", _i), ("row0", _ll),
         ("row_map", _vp), ("work", _vp),

@@ -108,13 +108,13 @@ def test_gemm_dist_argmin_gate_consistent():
     # gate
     thr = torch.tensor(np.quantile(Dn, 0.05, axis=1).astype(np.float32), device="cuda")
     cap = 64
-    ci = torch.empty((M, cap), dtype=torch.int32, device="cuda")
-    cv = torch.empty((M, cap), dtype=torch.float32, device="cuda")
+    rec = torch.empty((M, cap, 2), dtype=torch.int32, device="cuda")  # {index, float bits}
     cc = torch.empty(M, dtype=torch.int32, device="cuda")
-    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand_idx=ci, cand_val=cv,
+    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand=rec,
              cand_cnt=cc, cand_cap=cap)
     thr_n = thr.cpu().numpy()
-    ci_n, cv_n, cc_n = ci.cpu().numpy(), cv.cpu().numpy(), cc.cpu().numpy()
+    rec_n, cc_n = rec.cpu().numpy(), cc.cpu().numpy()
+    ci_n, cv_n = rec_n[..., 0], rec_n[..., 1].view(np.float32)
     for i in range(0, M, 37):
         want = np.flatnonzero(~(Dn[i] > thr_n[i]))
         assert cc_n[i] == want.size
@@ -266,8 +266,8 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     thr = torch.empty(n, dtype=torch.float32, device="cuda")
     native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[0]), int(sentinel), dev.ptr(thr), dev.stream_handle())
     cap = 128
-    ci = torch.empty((n, cap), dtype=torch.int32, device="cuda")
-    cv = torch.empty((n, cap), dtype=torch.float32, device="cuda")
+    rec = torch.empty((n, cap, 2), dtype=torch.int32, device="cuda")  # {index, float bits}
+    ci = rec[..., 0]
     cc = torch.empty(n, dtype=torch.int32, device="cuda")
     widths, _ = tail_block_layout(d, dp)
     ext = 64 if cert and not sentinel and dp % 4 == 0 and dp + 64 <= d and widths[0] == 64 else 0
@@ -279,7 +279,7 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
         native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[1]), 0, dev.ptr(thr1), dev.stream_handle())
         kw = dict(ext_k=ext, xsq_ext=dev.row_sq_norms(X, dp + ext), ysq_ext=dev.row_sq_norms(Cm, dp + ext), thr1=thr1,
                   cert_eps=3e-5)
-    dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand_idx=ci, cand_val=cv,
+    dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand=rec,
              cand_cnt=cc, cand_cap=cap, **kw)
     if ext:
         valid = torch.arange(cap, device="cuda")[None, :] < cc.clamp(max=cap)[:, None]
@@ -296,7 +296,7 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     theta = torch.tensor(fs, device="cuda")
     bdims = torch.tensor(widths, device="cuda")
     p = native.ScanParams()
-    p.cand_idx, p.cand_val, p.cand_cnt, p.cap = ci.data_ptr(), cv.data_ptr(), cc.data_ptr(), cap
+    p.cand, p.cand_cnt, p.cap = rec.data_ptr(), cc.data_ptr(), cap
     p.k, p.n_rows, p.row0 = k, n, 0
     p.x, p.ldx = X.data_ptr(), X.stride(0)
     p.tails, p.nb, p.d_prime = tails.data_ptr(), nb, dp

@@ -24,9 +24,9 @@ if MODE == "self":
     thr1_np[:] = 0.0
 thr1 = torch.tensor(thr1_np, device="cuda")
 cap = 512
-ci = torch.empty((n, cap), dtype=torch.int32, device="cuda"); cv = torch.empty((n, cap), device="cuda"); cc = torch.empty(n, dtype=torch.int32, device="cuda")
+rec = torch.empty((n, cap, 2), dtype=torch.int32, device="cuda"); ci = rec[..., 0]; cv = rec[..., 1].view(torch.float32); cc = torch.empty(n, dtype=torch.int32, device="cuda")
 dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_GATE, xsq=dev.row_sq_norms(X, dp), ysq=dev.row_sq_norms(Cm, dp), thr=thr,
-         cand_idx=ci, cand_val=cv, cand_cnt=cc, cand_cap=cap, ext_k=64, xsq_ext=dev.row_sq_norms(X, dp + 64),
+         cand=rec, cand_cnt=cc, cand_cap=cap, ext_k=64, xsq_ext=dev.row_sq_norms(X, dp + 64),
          ysq_ext=dev.row_sq_norms(Cm, dp + 64), thr1=thr1, cert_eps=3e-5 if MODE == "self" else 0.0)
 torch.cuda.synchronize()
 idx = ci.cpu().numpy()

@@ -28,13 +28,17 @@ cfg = KMeansConfig(k=a.k, max_iters=a.iters, seed=0)
 rot = generate_rotation(a.d, 0)
 from paper_2603_20009_b200 import profiling  # noqa: E402
 prof = profiling.KernelTimer()
+import time  # noqa: E402
 for i in range(a.reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     if i == a.reps - 1:
         with profiling.active(prof):
             r = api.fit_device(x, a.d, cfg, rot)
     else:
         r = api.fit_device(x, a.d, cfg, rot)
-torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    print(f"rep {i}: fit wall {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
 print("kernels ms:", {k: round(v["ms"], 2) for k, v in sorted(prof.summary().items(), key=lambda kv: -kv[1]["ms"])})
 st = r.loop.stats
 print("d'", [s.d_prime for s in st], "surv/vec", [round(s.survivors / a.n, 1) for s in st],

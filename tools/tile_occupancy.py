@@ -27,7 +27,7 @@ def spy(data, cents, ws, plan, order=None, **kw):
     orig(data, cents, ws, plan, order=order, **kw)
     bn = min(ws.batch, data.n)
     cnt = ws.cand_cnt[:bn].clone()
-    idx = ws.cand_idx[:bn].clone()
+    idx = ws.cand[:bn, :, 0].clone()
     captured.setdefault("it", []).append((cnt, idx, ws.cap, cents.k, plan.d_prime))
 
 
