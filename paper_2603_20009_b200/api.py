@@ -102,8 +102,8 @@ class DeviceRotation:
 
 
 def _store_split(m, n):
-    from .engine import _n_split
-    return _n_split(m, n)
+    from .engine import _l2_split
+    return _l2_split(m, n, n, 6)
 
 
 def _split(x: torch.Tensor, cols: int):

@@ -34,7 +34,9 @@ enum GemmMode : int {
 
 struct GemmArgs {
   int M, N, K;
-  int tiles_per_cta;          // N tiles handled by one CTA (grid.y splits N)
+  int tiles_per_cta;          // N tiles handled by one CTA
+  int n_split;                // CTAs per M tile along N; block b -> M tile b / n_split, N range
+                              // b % n_split, so one M tile's CTAs run side by side (L2 reuse of A)
   float* out;                 // STORE / DIST
   long long ldo;
   const float* xsq;           // DIST / ARGMIN / GATE: per-row norm term
@@ -130,9 +132,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * GEMM_BM;
+  const int m0 = (blockIdx.x / args.n_split) * GEMM_BM;
   const int n_tiles = (args.N + BN - 1) / BN;
-  const int t_begin = blockIdx.y * args.tiles_per_cta;
+  const int t_begin = (blockIdx.x % args.n_split) * args.tiles_per_cta;
   const int t_end = min(n_tiles, t_begin + args.tiles_per_cta);
   const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
   // extension k-blocks (GATE certification): accumulated into ONE extra TMEM partial per tile
@@ -273,19 +275,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t kcount = 0;
 #pragma unroll 1
     for (int t = t_begin; t < t_end; ++t) {
-#pragma unroll 1
-      for (int kb = 0; kb < num_k; ++kb, ++kcount) {
+      // first k-block of the tile overwrites the sums, the rest add into them (peeled: a
+      // branch in the loop body made ptxas spill the 64 sums of the BN = 256 modes)
+      auto drain_wait = [&]() -> uint32_t {
         const int buf = kcount % NBUF;
         mbar_wait_sleep(&tfull[buf], (kcount / NBUF) & 1);
         tc_fence_after();
-        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(eq * 32) << 16) +
-                               static_cast<uint32_t>(buf * BN + half * HALF);
-#pragma unroll
-        for (int c = 0; c < HALF / 16; ++c)
-          tmem_ld16_accum(tbase + c * 16, *reinterpret_cast<float(*)[16]>(&acc[c * 16]), kb == 0);
+        return tmem_base + (static_cast<uint32_t>(eq * 32) << 16) + static_cast<uint32_t>(buf * BN + half * HALF);
+      };
+      auto drain_release = [&]() {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) mbar_arrive(&tempty[kcount % NBUF]);
+        ++kcount;
+      };
+      if (num_k > 0) {
+        const uint32_t tbase = drain_wait();
+#pragma unroll
+        for (int c = 0; c < HALF / 16; ++c) tmem_ld16_set(tbase + c * 16, *reinterpret_cast<float(*)[16]>(&acc[c * 16]));
+        drain_release();
+      }
+#pragma unroll 1
+      for (int kb = 1; kb < num_k; ++kb) {
+        const uint32_t tbase = drain_wait();
+#pragma unroll
+        for (int c = 0; c < HALF / 16; ++c) tmem_ld16_add(tbase + c * 16, *reinterpret_cast<float(*)[16]>(&acc[c * 16]));
+        drain_release();
       }
       // ---- tile complete: acc holds columns [col0, col0 + HALF)
       const int col0 = t * BN + half * HALF;
@@ -465,7 +480,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             best_j = j1;
           }
         }
-        if (gridDim.y == 1) {
+        if (args.n_split == 1) {
           args.assign[out_row] = best_j;
           args.tau[out_row] = best;
         } else {

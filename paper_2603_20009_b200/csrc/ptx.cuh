@@ -108,34 +108,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// acc[i] (+)= TMEM[lane][col0 + i], i < 16: load, wait and fp32 round-to-nearest add in ONE asm
+// acc[i] += TMEM[lane][col0 + i], i < 16: load, wait and fp32 round-to-nearest add in ONE asm
 // block, so the 16 temporaries never outlive it (keeps the epilogue's register footprint to
-// the running sums).  first != 0 overwrites instead of adding.
-__device__ __forceinline__ void tmem_ld16_accum(uint32_t taddr, float (&a)[16], int first) {
+// the running sums).  The first k-block of a tile uses tmem_ld16 straight into the sums (a
+// predicated mov/add pair compiled to FADD + SEL per element, doubling the drain's issue cost).
+__device__ __forceinline__ void tmem_ld16_add(uint32_t taddr, float (&a)[16]) {
   asm volatile(
-      "{\n\t.reg .b32 t<16>;\n\t.reg .pred pf;\n\t"
-      "setp.ne.b32 pf, %17, 0;\n\t"
+      "{\n\t.reg .b32 t<16>;\n\t"
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {t0,t1,t2,t3,t4,t5,t6,t7,t8,t9,t10,t11,t12,t13,t14,t15}, [%16];\n\t"
       "tcgen05.wait::ld.sync.aligned;\n\t"
-      "@pf mov.b32 %0, t0;\n\t@!pf add.rn.f32 %0, %0, t0;\n\t"
-      "@pf mov.b32 %1, t1;\n\t@!pf add.rn.f32 %1, %1, t1;\n\t"
-      "@pf mov.b32 %2, t2;\n\t@!pf add.rn.f32 %2, %2, t2;\n\t"
-      "@pf mov.b32 %3, t3;\n\t@!pf add.rn.f32 %3, %3, t3;\n\t"
-      "@pf mov.b32 %4, t4;\n\t@!pf add.rn.f32 %4, %4, t4;\n\t"
-      "@pf mov.b32 %5, t5;\n\t@!pf add.rn.f32 %5, %5, t5;\n\t"
-      "@pf mov.b32 %6, t6;\n\t@!pf add.rn.f32 %6, %6, t6;\n\t"
-      "@pf mov.b32 %7, t7;\n\t@!pf add.rn.f32 %7, %7, t7;\n\t"
-      "@pf mov.b32 %8, t8;\n\t@!pf add.rn.f32 %8, %8, t8;\n\t"
-      "@pf mov.b32 %9, t9;\n\t@!pf add.rn.f32 %9, %9, t9;\n\t"
-      "@pf mov.b32 %10, t10;\n\t@!pf add.rn.f32 %10, %10, t10;\n\t"
-      "@pf mov.b32 %11, t11;\n\t@!pf add.rn.f32 %11, %11, t11;\n\t"
-      "@pf mov.b32 %12, t12;\n\t@!pf add.rn.f32 %12, %12, t12;\n\t"
-      "@pf mov.b32 %13, t13;\n\t@!pf add.rn.f32 %13, %13, t13;\n\t"
-      "@pf mov.b32 %14, t14;\n\t@!pf add.rn.f32 %14, %14, t14;\n\t"
-      "@pf mov.b32 %15, t15;\n\t@!pf add.rn.f32 %15, %15, t15;\n\t}"
+      "add.rn.f32 %0, %0, t0;\n\tadd.rn.f32 %1, %1, t1;\n\tadd.rn.f32 %2, %2, t2;\n\t"
+      "add.rn.f32 %3, %3, t3;\n\tadd.rn.f32 %4, %4, t4;\n\tadd.rn.f32 %5, %5, t5;\n\t"
+      "add.rn.f32 %6, %6, t6;\n\tadd.rn.f32 %7, %7, t7;\n\tadd.rn.f32 %8, %8, t8;\n\t"
+      "add.rn.f32 %9, %9, t9;\n\tadd.rn.f32 %10, %10, t10;\n\tadd.rn.f32 %11, %11, t11;\n\t"
+      "add.rn.f32 %12, %12, t12;\n\tadd.rn.f32 %13, %13, t13;\n\tadd.rn.f32 %14, %14, t14;\n\t"
+      "add.rn.f32 %15, %15, t15;\n\t}"
       : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]), "+f"(a[7]),
         "+f"(a[8]), "+f"(a[9]), "+f"(a[10]), "+f"(a[11]), "+f"(a[12]), "+f"(a[13]), "+f"(a[14]), "+f"(a[15])
-      : "r"(taddr), "r"(first)
+      : "r"(taddr)
+      : "memory");
+}
+
+// a[i] = TMEM[lane][col0 + i], i < 16 (load + wait, outputs bound straight to the sums).
+__device__ __forceinline__ void tmem_ld16_set(uint32_t taddr, float (&a)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]), "=f"(a[4]), "=f"(a[5]), "=f"(a[6]), "=f"(a[7]),
+        "=f"(a[8]), "=f"(a[9]), "=f"(a[10]), "=f"(a[11]), "=f"(a[12]), "=f"(a[13]), "=f"(a[14]), "=f"(a[15])
+      : "r"(taddr)
       : "memory");
 }
 

@@ -112,6 +112,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   int split = std::max(1, std::min(p->n_split, n_tiles));
   a.tiles_per_cta = (n_tiles + split - 1) / split;
   split = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+  a.n_split = split;
   a.out = p->out;
   a.ldo = p->ldo;
   a.xsq = p->xsq;
@@ -136,7 +137,9 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   }
   if (MODE == skm::GEMM_ARGMIN && split > 1 && !p->keys) return fail(SKM_E_ARG, "ARGMIN with n_split>1 needs keys");
   if (MODE == skm::GEMM_GATE && split > 1) return fail(SKM_E_ARG, "GATE requires n_split == 1");
-  dim3 grid((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM, split);
+  const long long blocks = static_cast<long long>((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM) * split;
+  if (blocks > 0x7fffffffLL) return fail(SKM_E_ARG, "gemm: grid too large");
+  dim3 grid(static_cast<unsigned>(blocks));
   kern<<<grid, skm::GEMM_THREADS, L::TOTAL, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, te_a_hi, te_a_lo, te_b_hi, te_b_lo, a);
   SKM_LAUNCH_CHECK("gemm_tf32x3 launch");
   return SKM_OK;

@@ -238,6 +238,16 @@ def _n_split(m_rows: int, n_cols: int, sms: int = 148) -> int:
     return max(1, min(n_tiles, (2 * sms + m_tiles - 1) // m_tiles))
 
 
+def _l2_split(m_rows: int, n_cols: int, k_dim: int, cap: int, sms: int = 148) -> int:
+    """N split for a long GEMM whose concurrent A tiles (one 128-row hi+lo tile per SM, K wide)
+    would overflow the 126 MB L2: the CTAs of one M tile run side by side (block order), so A
+    is fetched from HBM about once instead of once per N tile (c2 ARGMIN: 148 x 1.5 MB)."""
+    s = _n_split(m_rows, n_cols, sms)
+    if s == 1 and sms * 128 * k_dim * 8 > (48 << 20):
+        s = min(cap, (n_cols + 255) // 256)
+    return max(1, s)
+
+
 def _sm_count(dev) -> int:
     try:
         return int(torch.cuda.get_device_properties(dev).multi_processor_count)
@@ -311,7 +321,7 @@ def full_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, row0: in
         return
     d = data.d
     xsq = data.norms(d)
-    split = _n_split(n, cents.k)
+    split = _l2_split(n, cents.k, d, 4)
     a_hi = data.hi[row0:row0 + n]
     a_lo = data.lo[row0:row0 + n]
     if split == 1:

@@ -21,7 +21,43 @@ xs = (x.double() ** 2).sum(1).float()
 ys = (c.double() ** 2).sum(1).float()
 assign = torch.empty(m, dtype=torch.int32, device=dev)
 tau = torch.empty(m, dtype=torch.float32, device=dev)
-for rep in range(2):
+keys = torch.empty(m, dtype=torch.int64, device=dev)
+ref = None
+for split in (1, 4, 8, 16):
+    def run():
+        if split == 1:
+            _gemm(x_hi, x_lo, c_hi, c_lo, m, k, d, native.GEMM_ARGMIN, xsq=xs, ysq=ys, assign=assign, tau=tau)
+        else:
+            keys.fill_(-1)
+            _gemm(x_hi, x_lo, c_hi, c_lo, m, k, d, native.GEMM_ARGMIN, xsq=xs, ysq=ys, keys=keys, n_split=split)
+            native.call("skm_decode_argmin_keys", keys.data_ptr(), m, assign.data_ptr(), tau.data_ptr(), None)
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    got = (assign.clone(), tau.clone())
+    same = ref is None or (torch.equal(ref[0], got[0]) and torch.equal(ref[1], got[1]))
+    ref = ref or got
+    print(f"argmin split={split}: {ms:.2f} ms  {6.0 * m * k * d / ms / 1e9:.0f} TFLOP/s  identical={same}", flush=True)
+out = torch.empty((m, d), dtype=torch.float32, device=dev)
+for split in (1, 2, 3, 6):
+    _gemm(x_hi, x_lo, c_hi[:d] if False else x_hi[:d], x_lo[:d], m, d, d, native.GEMM_STORE, out=out, n_split=split)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        _gemm(x_hi, x_lo, x_hi[:d], x_lo[:d], m, d, d, native.GEMM_STORE, out=out, n_split=split)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    print(f"store {m}x{d}x{d} split={split}: {ms:.2f} ms  {6.0 * m * d * d / ms / 1e9:.0f} TFLOP/s  "
+          f"checksum {float(out[::4097].double().sum()):.6e}", flush=True)
+for rep in range(0):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
