@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "ptx.cuh"
+
 namespace skm {
 
 constexpr float kInf = __builtin_huge_valf();
@@ -277,6 +279,76 @@ __global__ void __launch_bounds__(SEED_ROWS)
       const float diff = __fsub_rn(xs[tid][tt], cs[tid][tt]);
       acc = __fadd_rn(acc, __fmul_rn(diff, diff));
     }
+  }
+  if (r0 + tid < n) out[r0 + tid] = acc;
+}
+
+// Same chain as seed_thresholds_kernel, fed by 16-byte zero-filling cp.async copies straight
+// into a double-buffered [row][36] shared tile (no register round trip, row pointers hoisted out
+// of the chunk loop, LDS.128 reads); the zero-filled columns past d add +0.0 to a non-negative
+// running sum, so the result is bitwise the d-column chain.  Needs 16-byte aligned rows.
+constexpr int SEEDA_LD = 36;  // padded row (floats): LDS.128 quarter-warps hit 8 distinct bank groups
+constexpr int SEEDA_SMEM = 2 * 2 * SEED_ROWS * SEEDA_LD * 4;
+__global__ void __launch_bounds__(SEED_ROWS)
+    seed_thresholds_async_kernel(const float* __restrict__ x, long long ldx, const float* __restrict__ cent,
+                                 long long ldc, const int* __restrict__ assign, int n, int d,
+                                 float* __restrict__ out) {
+  extern __shared__ __align__(16) float seed_smem[];  // [buf][x|c][row][SEEDA_LD], 73.7 KB
+  auto tile = reinterpret_cast<float(*)[2][SEED_ROWS][SEEDA_LD]>(seed_smem);
+  const int r0 = blockIdx.x * SEED_ROWS;
+  const int tid = threadIdx.x;
+  // copy mapping: segment s = tid + 128 i (i < 8) -> row s / 8, 16-byte column group s % 8
+  const int q = tid & 7;
+  const float* xp[8];
+  const float* cp[8];
+  int rowq[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (tid >> 3) + 16 * i;
+    rowq[i] = r;
+    const int row = r0 + r;
+    const bool ok = row < n;
+    xp[i] = ok ? x + static_cast<long long>(row) * ldx + 4 * q : nullptr;
+    cp[i] = ok ? cent + static_cast<long long>(__ldg(assign + row)) * ldc + 4 * q : nullptr;
+  }
+  auto issue = [&](int t0, int buf) {
+    const int rem = d - t0 - 4 * q;  // valid floats from this thread's column group on
+    const int bytes = rem >= 4 ? 16 : (rem > 0 ? 4 * rem : 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int b = xp[i] ? bytes : 0;
+      cp_async_16_zfill(&tile[buf][0][rowq[i]][4 * q], b ? xp[i] + t0 : x, b);
+      cp_async_16_zfill(&tile[buf][1][rowq[i]][4 * q], b ? cp[i] + t0 : cent, b);
+    }
+    cp_async_commit();
+  };
+  const int nchunk = (d + 31) / 32;
+  float acc = 0.0f;
+  issue(0, 0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunk) {
+      issue(32 * (ch + 1), buf ^ 1);
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    const float4* xr = reinterpret_cast<const float4*>(&tile[buf][0][tid][0]);
+    const float4* cr = reinterpret_cast<const float4*>(&tile[buf][1][tid][0]);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const float4 a = xr[v], c = cr[v];
+      float df = __fsub_rn(a.x, c.x);
+      acc = __fadd_rn(acc, __fmul_rn(df, df));
+      df = __fsub_rn(a.y, c.y);
+      acc = __fadd_rn(acc, __fmul_rn(df, df));
+      df = __fsub_rn(a.z, c.z);
+      acc = __fadd_rn(acc, __fmul_rn(df, df));
+      df = __fsub_rn(a.w, c.w);
+      acc = __fadd_rn(acc, __fmul_rn(df, df));
+    }
+    __syncthreads();  // buf is refilled by the next iteration's issue
   }
   if (r0 + tid < n) out[r0 + tid] = acc;
 }

@@ -264,8 +264,22 @@ int skm_copy_i32(const int* src, int* dst, int n, void* stream) {
 int skm_seed_thresholds(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign,
                         int n, int d, float* out, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::seed_thresholds_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, 0, as_stream(stream)>>>(
-      x, ldx, centroids, ldc, assign, n, d, out);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(centroids)) & 15) == 0 &&
+                       ldx % 4 == 0 && ldc % 4 == 0;
+  if (aligned) {
+    static bool set = false;
+    if (!set) {
+      cudaError_t e = cudaFuncSetAttribute(skm::seed_thresholds_async_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
+      if (e != cudaSuccess) return cuda_fail(e, "seed_thresholds smem attribute");
+      set = true;
+    }
+    skm::seed_thresholds_async_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, skm::SEEDA_SMEM,
+                                        as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out);
+  } else {
+    skm::seed_thresholds_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, 0, as_stream(stream)>>>(
+        x, ldx, centroids, ldc, assign, n, d, out);
+  }
   SKM_LAUNCH_CHECK("seed_thresholds");
   return SKM_OK;
 }
@@ -355,9 +369,23 @@ int skm_cluster_sort(const int* assign, int n, int k, int* order, int* counts, i
 int skm_cluster_sums(const float* x, long long ldx, const int* order, const int* offsets, const int* counts, int k,
                      int d, double* sums, int accumulate, float* centroids, long long ldc, int mode, void* stream) {
   if (k <= 0 || d <= 0) return SKM_OK;
-  dim3 grid(k, (d + skm::SUM_THREADS - 1) / skm::SUM_THREADS);
-  skm::ordered_cluster_sums_kernel<<<grid, skm::SUM_THREADS, 0, as_stream(stream)>>>(
-      x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && ldx % 4 == 0) {
+    const int groups = (d + 3) / 4;
+    const int threads = std::min(768, (groups + 31) / 32 * 32);  // ring <= 768 x 16 x 16 B = 192 KB
+    static bool set = false;
+    if (!set) {
+      cudaError_t e = cudaFuncSetAttribute(skm::ordered_cluster_sums_vec_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SUMV_RING * 768 * 16);
+      if (e != cudaSuccess) return cuda_fail(e, "cluster_sums smem attribute");
+      set = true;
+    }
+    skm::ordered_cluster_sums_vec_kernel<<<k, threads, skm::SUMV_RING * threads * 16, as_stream(stream)>>>(
+        x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
+  } else {
+    dim3 grid(k, (d + skm::SUM_THREADS - 1) / skm::SUM_THREADS);
+    skm::ordered_cluster_sums_kernel<<<grid, skm::SUM_THREADS, 0, as_stream(stream)>>>(
+        x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
+  }
   SKM_LAUNCH_CHECK("cluster_sums");
   return SKM_OK;
 }

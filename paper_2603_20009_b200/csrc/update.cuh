@@ -9,6 +9,7 @@
 // The sorted row order doubles as the cluster lists used by ETR / IVF probing
 // (evaluation.py:78-83) and as a cluster-coherent vector order for the pruning scan.
 #pragma once
+#include "ptx.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -140,6 +141,63 @@ __global__ void __launch_bounds__(SUM_THREADS)
     sums_io[static_cast<long long>(c) * d + col] = s;
   } else if (cnt > 0) {
     cent[static_cast<long long>(c) * ldc + col] = __double2float_rn(__ddiv_rn(s, static_cast<double>(cnt)));
+  }
+}
+
+// Same sums, one CTA per cluster: thread = 4 consecutive columns (16-byte aligned rows, ld % 4
+// == 0 so the padded columns past d are readable), four f64 chains in member order (bitwise the
+// per-column kernel).  A member row is read as one contiguous run by one CTA, and each thread
+// keeps SUMV_RING member rows in flight through a private cp.async ring in shared memory (it
+// consumes exactly the 16 bytes it copied, so no block barrier): the chain of a large cluster
+// is bound by memory latency / ring depth, not by 4 loads per round trip.
+constexpr int SUMV_RING = 16;
+__device__ __forceinline__ void sumv_add(double (&s)[4], const float4& v) {
+  s[0] = __dadd_rn(s[0], static_cast<double>(v.x));
+  s[1] = __dadd_rn(s[1], static_cast<double>(v.y));
+  s[2] = __dadd_rn(s[2], static_cast<double>(v.z));
+  s[3] = __dadd_rn(s[3], static_cast<double>(v.w));
+}
+__global__ void __launch_bounds__(768)
+    ordered_cluster_sums_vec_kernel(const float* __restrict__ x, long long ldx, const int* __restrict__ order,
+                                    const int* __restrict__ offsets, const int* __restrict__ counts, int d,
+                                    double* __restrict__ sums_io, int accumulate_sums, float* __restrict__ cent,
+                                    long long ldc, int mode) {
+  extern __shared__ __align__(16) float4 sumv_ring[];  // [SUMV_RING][blockDim.x]
+  const int c = blockIdx.x;
+  const int beg = offsets[c], cnt = counts[c];
+  const int* ord = order + beg;
+  const int ng = (d + 3) / 4;
+  const int bd = blockDim.x;
+  float4* ring = sumv_ring + threadIdx.x;
+  for (int g = threadIdx.x; g < ng; g += bd) {
+    const int col = 4 * g;
+    const long long so = static_cast<long long>(c) * d + col;
+    double s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = (accumulate_sums && col + i < d) ? sums_io[so + i] : 0.0;
+    auto issue = [&](int m) {
+      if (m < cnt)
+        cp_async_16_zfill(ring + (m % SUMV_RING) * bd, x + static_cast<long long>(__ldg(ord + m)) * ldx + col, 16);
+      cp_async_commit();  // empty groups keep the wait count uniform
+    };
+#pragma unroll 1
+    for (int m = 0; m < SUMV_RING - 1; ++m) issue(m);
+#pragma unroll 1
+    for (int m = 0; m < cnt; ++m) {
+      issue(m + SUMV_RING - 1);
+      cp_async_wait_group<SUMV_RING - 1>();  // member m has landed
+      sumv_add(s, ring[(m % SUMV_RING) * bd]);
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (col + i >= d) break;
+      if (mode == 1) {
+        sums_io[so + i] = s[i];
+      } else if (cnt > 0) {
+        cent[static_cast<long long>(c) * ldc + col + i] = __double2float_rn(__ddiv_rn(s[i], static_cast<double>(cnt)));
+      }
+    }
   }
 }
 
