@@ -141,13 +141,15 @@ def cpu_reference_sample(args, sample_rows, iters=10):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    import multiprocessing
     cores = os.cpu_count() or 1
     per_step = []
     desc = ""
-    n_warm, n_steps = min(args.warmup, 1), min(args.steps, 2)  # each sample is ~10-30 s of CPU work
+    n_warm, n_steps = args.warmup, args.steps
+    # each step is a bounded sample (n/16 rows x all iterations, ~10-15 s of CPU work on the GPU
+    # boxes' host cores), shrunk when many steps are asked for so the run stays within minutes
+    rows = args.cpu_sample or max(args.n // 64, int(args.n // 16 * min(1.0, 10.0 / max(1, n_warm + n_steps))))
     for i in range(n_warm + n_steps):
-        v, dt, desc = cpu_reference_sample(args, args.cpu_sample or args.n // 16, iters=args.iters)
+        v, dt, desc = cpu_reference_sample(args, rows, iters=args.iters)
         if i >= n_warm:
             per_step.append(v)
     value = float(np.median(per_step))
