@@ -68,7 +68,7 @@ def available_backends():
 
 def __getattr__(name):
     # lazily resolved, GPU-backed helpers
-    if name in ("hierarchical_fit", "HierarchicalConfig", "reconcile_k"):
+    if name in ("hierarchical_fit", "hierarchical_fit_device", "HierarchicalConfig", "reconcile_k"):
         from . import hierarchical
         return getattr(hierarchical, name)
     if name in ("brute_force_topk", "etr_probe", "build_cluster_lists", "GroundTruth", "RecallHistory",

@@ -171,6 +171,35 @@ def _h2d(x: np.ndarray, dev, check_finite: bool = False) -> torch.Tensor:
     return out
 
 
+def _nonfinite_key(out: torch.Tensor, n: int, d: int) -> int:
+    """Flat index row * d + col of the first NaN/Inf of a padded device matrix, 2^64 - 1 if none."""
+    if n == 0:
+        return (1 << 64) - 1
+    first = torch.empty(1, dtype=torch.int64, device=out.device)
+    native.call("skm_first_nonfinite", ptr(out), out.shape[1], n, d, ptr(first), stream_handle())
+    return int(first.cpu().numpy().view(np.uint64)[0])
+
+
+def _check_finite_sharded(x: np.ndarray, dev, row_offset: int, comm, chunk_rows: int = 1 << 18) -> None:
+    """validate_vector_set's finiteness check of a row-sharded host matrix: every rank scans its
+    rows [row_offset, row_offset + len(x)) on the device, one allreduce(min) of the first bad
+    flat index, and every rank raises the same NonFiniteValue(row, col) (no rank is left
+    waiting in a collective)."""
+    n, d = x.shape
+    key = (1 << 64) - 1
+    for r0 in range(0, n, chunk_rows):
+        k = _nonfinite_key(_h2d(x[r0:r0 + chunk_rows], dev), min(chunk_rows, n - r0), d)
+        if k != (1 << 64) - 1:
+            key = (row_offset + r0) * d + k
+            break
+    t = torch.tensor([min(key, (1 << 63) - 1)], dtype=torch.int64, device=dev)
+    comm.allreduce_min_(t)
+    g = int(t.item())
+    if g != (1 << 63) - 1:
+        from .config import NonFiniteValue
+        raise NonFiniteValue(g // d, g % d)
+
+
 def _h2d_check_only(x: np.ndarray, dev, chunk_rows: int = 1 << 18) -> None:
     """Finiteness of a host matrix checked on the device chunk by chunk (bounded memory)."""
     for r0 in range(0, x.shape[0], chunk_rows):
@@ -270,15 +299,8 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
     from .hostmath import init_indices
     init_idx = init_indices(n, cfg.k, [cfg.seed, 2])
     if init_rows is None and comm.world > 1:
-        init_rows = torch.zeros((cfg.k, data.ld), dtype=torch.float32, device=dev)
-        mine = np.flatnonzero((init_idx >= row_lo) & (init_idx < row_lo + n_local))
-        if mine.size:
-            src = torch.tensor(init_idx[mine] - row_lo, dtype=torch.int64, device=dev)
-            tmp = torch.empty((mine.size, data.ld), dtype=torch.float32, device=dev)
-            native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(src), int(mine.size), data.ld, ptr(tmp),
-                        data.ld, stream_handle())
-            init_rows[torch.tensor(mine, dtype=torch.int64, device=dev)] = tmp
-        comm.allreduce_(init_rows)
+        from .engine import sharded_init_rows
+        init_rows = sharded_init_rows(data, cfg.k, init_idx, row_lo, comm)
     etr = None
     if cfg.etr is not None:
         from .etr import EtrState

@@ -88,6 +88,11 @@ class Comm:
             self.dist.all_reduce(t, group=self.group)
         return t
 
+    def allreduce_min_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return t
+
     def shard(self, n: int) -> tuple[int, int]:
         """Contiguous row range of this rank."""
         per = (n + self.world - 1) // self.world
@@ -516,6 +521,21 @@ def assign_stats(ws: Workspace, n: int, with_prev: bool) -> None:
 
 
 # ------------------------------------------------------------------------------ the loop
+def sharded_init_rows(data: "DeviceData", k: int, init_idx: np.ndarray, row_lo: int, comm: Comm) -> torch.Tensor:
+    """Forgy rows (k, ld) assembled across ranks: each rank fills the rows it owns (global
+    indices in [row_lo, row_lo + n_local)) and one allreduce(sum) completes the replica."""
+    dev = data.x.device
+    rows = torch.zeros((k, data.ld), dtype=torch.float32, device=dev)
+    mine = np.flatnonzero((init_idx >= row_lo) & (init_idx < row_lo + data.n))
+    if mine.size:
+        src = torch.tensor(init_idx[mine] - row_lo, dtype=torch.int64, device=dev)
+        tmp = torch.empty((mine.size, data.ld), dtype=torch.float32, device=dev)
+        native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(src), int(mine.size), data.ld, ptr(tmp), data.ld,
+                    stream_handle())
+        rows[torch.tensor(mine, dtype=torch.int64, device=dev)] = tmp
+    return comm.allreduce_(rows)
+
+
 def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: Comm | None = None,
                        n_global: int | None = None, row_lo: int = 0, init_rows: torch.Tensor | None = None,
                        init_idx: np.ndarray | None = None, etr=None, timer: _Timer | None = None,

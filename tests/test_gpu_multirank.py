@@ -77,3 +77,58 @@ def test_two_ranks_match_single_rank(etr):
         rel = np.linalg.norm(two[r]["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
         assert rel <= 1e-6, rel
     assert np.array_equal(two[0]["cent"], two[1]["cent"])  # replicas stay identical
+
+
+def _run_hier(rank, world, port, q, layout):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2603_20009_b200 as skb
+        from paper_2603_20009_b200.engine import Comm
+        torch.cuda.set_device(0)
+        x = make_blobs(16000, 96, 150, seed=5, spread=4.0)
+        if layout == "sorted":  # spatially coherent shards: many groups live on one rank only
+            x = np.ascontiguousarray(x[np.argsort(x[:, 0], kind="stable")])
+        res = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=400, seed=7), comm=Comm())
+        q.put((rank, {"assign": res.assignments, "cent": res.centroids_rotated, "k": res.k,
+                      "dp": [s.d_prime for s in res.stats], "work": res.work}))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("layout", ["shuffled", "sorted"])
+def test_hierarchical_two_ranks_match_single_rank(layout):
+    """Sharded hierarchical fit (BASELINE c5's data-sharded form): meso loop sharded,
+    every group fitted as a sharded loop over its members' rank-local rows.  Integer outputs
+    equal the single-process fit, centroids up to the cross-rank f64 summation order, replicas
+    identical."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    outs = {}
+    for world in (1, 2):
+        q = ctx.Queue()
+        port = 29900 + world + (os.getpid() % 500) + (50 if layout == "sorted" else 0)
+        ps = [ctx.Process(target=_run_hier, args=(r, world, port, q, layout)) for r in range(world)]
+        for p in ps:
+            p.start()
+        res = dict(q.get(timeout=600) for _ in range(world))
+        for p in ps:
+            p.join(timeout=120)
+        for r, v in res.items():
+            assert isinstance(v, dict), v
+        outs[world] = res
+    one = outs[1][0]
+    for r, two in outs[2].items():
+        assert two["k"] == one["k"]
+        assert two["dp"] == one["dp"]
+        assert np.array_equal(two["assign"], one["assign"])
+        assert two["work"] == one["work"]
+        rel = np.linalg.norm(two["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
+        assert rel <= 1e-6, rel
+    assert np.array_equal(outs[2][0]["cent"], outs[2][1]["cent"])
