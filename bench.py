@@ -239,7 +239,10 @@ def main():
     st_last = res.loop.stats
     scan_bytes = args.steps * sum(4.0 * args.n * (args.d - s.d_prime) + 4.0 * s.tail_dims_touched
                                   for s in st_last if s.d_prime is not None)
-    roof = prof.roofline(args.steps, bytes_override={"pruned_scan": scan_bytes})
+    scan_launches = prof.summary().get("pruned_scan", {}).get("launches", 0)
+    scan_rows = args.steps * (hi - lo) * sum(1 for s in st_last if s.d_prime is not None)
+    roof = prof.roofline(args.steps, bytes_override={"pruned_scan": scan_bytes},
+                         rows_per_launch={"pruned_scan": scan_rows / max(1, scan_launches)})
 
     # ---- end to end through the public entry with host (pinned) input ----
     e2e = None

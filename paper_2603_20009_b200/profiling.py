@@ -61,7 +61,7 @@ class KernelTimer:
             s["bytes"] += by
         return agg
 
-    def roofline(self, steps: int, bytes_override: dict | None = None) -> dict:
+    def roofline(self, steps: int, bytes_override: dict | None = None, rows_per_launch: dict | None = None) -> dict:
         agg = self.summary()
         for k_, v_ in (bytes_override or {}).items():
             if k_ in agg:
@@ -92,7 +92,25 @@ class KernelTimer:
                                 "rows (HBM) + 4 B per touched (vector, centroid, dim) of the L2-resident "
                                 "centroid tails (exact dims-touched counter)"})
         out["per_kernel_ms_per_step"] = {k: round(v["ms"] / steps, 3) for k, v in agg.items()}
+        tr = _traffic_record(name)
+        if tr and rows_per_launch:
+            # DRAM bytes (read + write) of one launch of this kernel from a committed ncu --set full
+            # capture, scaled per row to this run's average launch
+            out["traffic"] = tr["dram_bytes"] / tr["rows"] * rows_per_launch.get(name, tr["rows"])
+            out["traffic_source"] = tr["source"]
         return out
+
+
+def _traffic_record(kernel: str) -> dict | None:
+    """profiles/traffic.json: {kernel: {"dram_bytes": B, "rows": R, "source": "..."}} written from
+    an ncu --set full capture (tools/prof/r1c_capture.sh)."""
+    import json
+    path = os.path.join(_ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 @contextlib.contextmanager
