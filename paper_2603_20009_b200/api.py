@@ -119,15 +119,16 @@ _STAGE_THREADS = int(os.environ.get("SKM_H2D_THREADS", max(1, min(8, os.cpu_coun
 _stage_pool = None
 
 
-def _copy_rows_to_device(x: np.ndarray, out: torch.Tensor, d: int) -> None:
-    """out[:, :d] = x for a pageable host matrix.  A plain pageable copy runs at ~11 GB/s on
-    the B200 hosts (one driver thread staging through its own bounce buffer); here the host
-    copy into pinned chunks is split over a few threads and overlapped with the DMA of the
-    previous chunk (three-chunk ring), ~50 GB/s (tools/h2d_probe.py)."""
+def _copy_rows_to_device(x: np.ndarray, out: torch.Tensor, d: int, idx: np.ndarray | None = None) -> None:
+    """out[:, :d] = x (or x[idx], a row gather) for a pageable host matrix.  A plain pageable
+    copy runs at ~11 GB/s on the B200 hosts (one driver thread staging through its own bounce
+    buffer); here the host copy (or gather) into pinned chunks is split over a few threads and
+    overlapped with the DMA of the previous chunk (three-chunk ring), ~50 GB/s
+    (tools/h2d_probe.py)."""
     global _stage_pool
-    n = x.shape[0]
-    if x.nbytes <= 2 * _STAGE_BYTES or _STAGE_THREADS == 1:
-        out[:, :d].copy_(torch.from_numpy(x))
+    n = x.shape[0] if idx is None else idx.shape[0]
+    if n * d * 4 <= 2 * _STAGE_BYTES or _STAGE_THREADS == 1:
+        out[:, :d].copy_(torch.from_numpy(x if idx is None else x[idx]))
         return
     if _stage_pool is None:
         from concurrent.futures import ThreadPoolExecutor
@@ -143,8 +144,13 @@ def _copy_rows_to_device(x: np.ndarray, out: torch.Tensor, d: int) -> None:
         nb = min(rows, n - r0)
         view = bufs[b].numpy()[:nb]
         step = -(-nb // _STAGE_THREADS)
-        list(_stage_pool.map(lambda j: np.copyto(view[j:min(j + step, nb)], x[r0 + j:r0 + min(j + step, nb)]),
-                             range(0, nb, step)))
+        if idx is None:
+            list(_stage_pool.map(lambda j: np.copyto(view[j:min(j + step, nb)], x[r0 + j:r0 + min(j + step, nb)]),
+                                 range(0, nb, step)))
+        else:  # np.take releases the GIL; mode="clip" writes straight into the pinned view
+            list(_stage_pool.map(lambda j: np.take(x, idx[r0 + j:r0 + min(j + step, nb)], axis=0,
+                                                   out=view[j:min(j + step, nb)], mode="clip"),
+                                 range(0, nb, step)))
         out[r0:r0 + nb, :d].copy_(bufs[b][:nb], non_blocking=True)
         done[b] = torch.cuda.Event()
         done[b].record(stream)
@@ -153,14 +159,16 @@ def _copy_rows_to_device(x: np.ndarray, out: torch.Tensor, d: int) -> None:
             e.synchronize()  # the ring is released when the function returns
 
 
-def _h2d(x: np.ndarray, dev, check_finite: bool = False) -> torch.Tensor:
-    """(n, ld) device copy with zero pad columns.  ``check_finite``: validate_vector_set's
-    NaN/Inf check (model.py:84-87) on the device after the copy -- the host scan costs ~0.3 s
-    per GB, more than the fit -- raising the same NonFiniteValue(first row, col)."""
-    n, d = x.shape
+def _h2d(x: np.ndarray, dev, check_finite: bool = False, idx: np.ndarray | None = None) -> torch.Tensor:
+    """(n, ld) device copy of x (or of the rows x[idx]) with zero pad columns.  ``check_finite``:
+    validate_vector_set's NaN/Inf check (model.py:84-87) on the device after the copy -- the
+    host scan costs ~0.3 s per GB, more than the fit -- raising the same NonFiniteValue(first
+    row, col) (row numbered within the copied rows)."""
+    n = x.shape[0] if idx is None else idx.shape[0]
+    d = x.shape[1]
     out = torch.zeros((n, padded_ld(d)), dtype=torch.float32, device=dev)
     if n:
-        _copy_rows_to_device(x, out, d)
+        _copy_rows_to_device(x, out, d, idx)
         if check_finite:
             first = torch.empty(1, dtype=torch.int64, device=dev)
             native.call("skm_first_nonfinite", ptr(out), out.shape[1], n, d, ptr(first), stream_handle())
@@ -210,6 +218,86 @@ def _h2d_check_only(x: np.ndarray, dev, chunk_rows: int = 1 << 18) -> None:
             if isinstance(e, NonFiniteValue):
                 raise NonFiniteValue(e.row + r0, e.col) from None
             raise
+
+
+class _FiniteCheckJob:
+    """validate_vector_set's whole-input NaN/Inf check run on a host thread + its own CUDA
+    stream while the caller works on a sample; ``result()`` re-raises the first
+    NonFiniteValue(row, col) in row order, exactly the error the up-front check would give."""
+
+    def __init__(self, x: np.ndarray, dev):
+        import threading
+        self.error = None
+        stream = torch.cuda.Stream(dev)
+
+        def run():
+            try:
+                with torch.cuda.stream(stream):
+                    _h2d_check_only(x, dev)
+            except BaseException as e:  # surfaced in result()
+                self.error = e
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+
+    def result(self) -> None:
+        self.thread.join()
+        if self.error is not None:
+            raise self.error
+
+
+def _prefetch_batches(x: np.ndarray, batch_rows: int, dev):
+    """Yield (s0, e0, device rows) for consecutive row batches of a host matrix; batch i + 1 is
+    staged (threaded pinned ring, own CUDA stream) while the caller computes on batch i.  The
+    main stream waits on each batch's copy event; at most three batches are resident."""
+    import queue
+    import threading
+    n = x.shape[0]
+    q: queue.Queue = queue.Queue(maxsize=1)
+    stop = threading.Event()
+    stream = torch.cuda.Stream(dev)
+
+    def put(item) -> bool:
+        while not stop.is_set():
+            try:
+                q.put(item, timeout=0.05)
+                return True
+            except queue.Full:
+                continue
+        return False
+
+    def work():
+        try:
+            with torch.cuda.stream(stream):
+                for s0 in range(0, n, batch_rows):
+                    e0 = min(n, s0 + batch_rows)
+                    xb = _h2d(x[s0:e0], dev)
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    if not put((s0, e0, xb, ev)):
+                        return
+        except BaseException as e:  # surfaced on the consumer side
+            put(e)
+            return
+        put(None)
+
+    t = threading.Thread(target=work, daemon=True)
+    t.start()
+    main = torch.cuda.current_stream(dev)
+    try:
+        while True:
+            item = q.get()
+            if item is None:
+                break
+            if isinstance(item, BaseException):
+                raise item
+            s0, e0, xb, ev = item
+            main.wait_event(ev)
+            xb.record_stream(main)
+            yield s0, e0, xb
+    finally:
+        stop.set()
+        t.join()
 
 
 def _device_bytes_values(*ts) -> int:
@@ -329,12 +417,22 @@ def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
     if cfg.sampling_fraction == 1:
         x_dev = _h2d(x, dev, check_finite=True)  # ... overlapped with the copy and iteration 1
         sidx = None
+        res = fit_device(x_dev, d, cfg, job, inspect=inspect, consume_input=True)
     else:
-        # the reference validates the whole input before sampling (core.py:425-436)
-        _h2d_check_only(x, dev)
-        sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
-        x_dev = _h2d(x[sidx], dev)
-    res = fit_device(x_dev, d, cfg, job, inspect=inspect, consume_input=True)
+        # The reference validates the whole input before sampling (core.py:425-436).  Here the
+        # whole-input check streams on its own stream while the sample is gathered (threaded,
+        # into the pinned ring) and fitted; it is joined before anything is returned, and any
+        # earlier error defers to it, so a non-finite input raises exactly the reference's
+        # NonFiniteValue(first row, col).
+        check = _FiniteCheckJob(x, dev)
+        try:
+            sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
+            x_dev = _h2d(x, dev, check_finite=True, idx=sidx)
+            res = fit_device(x_dev, d, cfg, job, inspect=inspect, consume_input=True)
+        except BaseException:
+            check.result()
+            raise
+        check.result()
     rotation = res.rotation
     del x_dev
     out = res.loop
@@ -389,14 +487,12 @@ def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, b
         cents.refresh(d, None)
         plan = None
     cfg_ws = KMeansConfig(k=k, x_batch_device=cfg.x_batch_device, cand_cap=cfg.cand_cap)
-    for s0 in range(0, n, batch_rows):
-        e0 = min(n, s0 + batch_rows)
-        try:
-            xb = _h2d(x_full[s0:e0], dev, check_finite=True)
-        except NonFiniteValue as e:
-            raise NonFiniteValue(e.row + s0, e.col) from None
-        data = DeviceData(rot.apply(xb), d)
-        ws = Workspace(dev, e0 - s0, k, d, cfg_ws)
+    ws = Workspace(dev, min(batch_rows, max(n, 1)), k, d, cfg_ws)  # reused by every batch
+    for s0, e0, xb in _prefetch_batches(x_full, batch_rows, dev):
+        key = _nonfinite_key(xb, e0 - s0, d)
+        if key != (1 << 64) - 1:
+            raise NonFiniteValue(s0 + key // d, key % d)
+        data = DeviceData(rot.apply(xb, inplace=True), d)
         ws.assign[: e0 - s0].copy_(torch.from_numpy(assign[s0:e0]))
         if pruned:
             ws.counters.zero_()
