@@ -102,18 +102,18 @@ def _run_hier(rank, world, port, q, layout):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", ["shuffled", "sorted"])
-def test_hierarchical_two_ranks_match_single_rank(layout):
-    """Sharded hierarchical fit (BASELINE c5's data-sharded form): meso loop sharded,
+@pytest.mark.parametrize("layout,ranks", [("shuffled", 2), ("sorted", 2), ("sorted", 3)])
+def test_hierarchical_two_ranks_match_single_rank(layout, ranks):
+    """Sharded hierarchical fit (2 and 3 ranks: uneven shards) (BASELINE c5's data-sharded form): meso loop sharded,
     every group fitted as a sharded loop over its members' rank-local rows.  Integer outputs
     equal the single-process fit, centroids up to the cross-rank f64 summation order, replicas
     identical."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     outs = {}
-    for world in (1, 2):
+    for world in (1, ranks):
         q = ctx.Queue()
-        port = 29900 + world + (os.getpid() % 500) + (50 if layout == "sorted" else 0)
+        port = 29900 + world + (os.getpid() % 500) + (50 if layout == "sorted" else 0) + 10 * ranks
         ps = [ctx.Process(target=_run_hier, args=(r, world, port, q, layout)) for r in range(world)]
         for p in ps:
             p.start()
@@ -124,11 +124,12 @@ def test_hierarchical_two_ranks_match_single_rank(layout):
             assert isinstance(v, dict), v
         outs[world] = res
     one = outs[1][0]
-    for r, two in outs[2].items():
+    for r, two in outs[ranks].items():
         assert two["k"] == one["k"]
         assert two["dp"] == one["dp"]
         assert np.array_equal(two["assign"], one["assign"])
         assert two["work"] == one["work"]
         rel = np.linalg.norm(two["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
         assert rel <= 1e-6, rel
-    assert np.array_equal(outs[2][0]["cent"], outs[2][1]["cent"])
+    for r in range(1, ranks):
+        assert np.array_equal(outs[ranks][0]["cent"], outs[ranks][r]["cent"])
