@@ -73,9 +73,9 @@ class DeviceRotation:
         self.d = d
         ld = padded_ld(d)
         r = torch.zeros((d, ld), dtype=torch.float32, device=dev)
-        r[:, :d] = torch.from_numpy(np.ascontiguousarray(rotation.data)).to(dev)
+        r[:, :d].copy_(torch.from_numpy(np.ascontiguousarray(rotation.data, dtype=np.float32)))  # one upload
         rt = torch.zeros((d, ld), dtype=torch.float32, device=dev)
-        rt[:, :d] = torch.from_numpy(np.ascontiguousarray(rotation.data.T)).to(dev)
+        rt[:, :d] = r[:, :d].t()  # transposed on the device
         self.r_hi, self.r_lo = _split(r, d)     # rows of R   -> X @ R^T (unrotate)
         self.rt_hi, self.rt_lo = _split(rt, d)  # rows of R^T -> X @ R   (rotate)
 

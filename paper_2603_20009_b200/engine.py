@@ -680,10 +680,19 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         phase["ground_truth"] = gt_time
     for key in ("gemm", "pruning", "update", "etr"):
         phase[key] = sum(s.timings.get(key, 0.0) for s in stats)
+    # results back through pinned buffers (one DMA each, one sync, no second host copy: the
+    # arrays own the pinned storage)
+    host_c = torch.empty((k, d), dtype=torch.float32, pin_memory=True)
+    host_a = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+    host_t = torch.empty(n_local, dtype=torch.float32, pin_memory=True)
+    host_c.copy_(cents.c[:, :d], non_blocking=True)
+    host_a.copy_(ws.assign[:n_local], non_blocking=True)
+    host_t.copy_(ws.tau[:n_local], non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
     return LoopOutput(
-        centroids_rotated=cents.c[:, :d].cpu().numpy().copy(),
-        assignments=ws.assign[:n_local].cpu().numpy().copy(),
-        best_sq_dist=ws.tau[:n_local].cpu().numpy().copy(),
+        centroids_rotated=host_c.numpy(),
+        assignments=host_a.numpy(),
+        best_sq_dist=host_t.numpy(),
         stats=stats,
         terminated_by=terminated,
         d_prime_final=d_prime,
