@@ -111,6 +111,8 @@ FIT_CASES = {
     "etr": (("blobs", 4000, 128, 60, 21), dict(k=40, max_iters=12, seed=1)),
     "split": (("blobs", 1200, 96, 4, 13), dict(k=40, max_iters=5, seed=0)),
     "etr2": (("blobs", 12000, 128, 200, 3, 4.0), dict(k=100, max_iters=25, seed=1)),
+    # the c2 dimensionality: 24 tail blocks of 64 after d' = 192, R from a 1536 x 1536 QR
+    "wide": (("skewed", 8000, 1536, 128, 17), dict(k=64, max_iters=5, seed=3)),
 }
 
 
@@ -270,6 +272,14 @@ def cli_golden():
 
 
 def main():
+    if "--only-fit" in sys.argv:  # (re)generate one FIT_CASES entry, keep the rest of fits.npz
+        name = sys.argv[sys.argv.index("--only-fit") + 1]
+        path = os.path.join(HERE, "fits.npz")
+        out = {k: v for k, v in np.load(path).items() if not k.startswith(name + "_")}
+        spec, kw = FIT_CASES[name]
+        fit_case(name, make_x(spec), skm.KMeansConfig(**kw), out)
+        np.savez_compressed(path, **out)
+        return
     if "--only-cli" in sys.argv:
         np.savez_compressed(os.path.join(HERE, "cli.npz"), **cli_golden())
         return
