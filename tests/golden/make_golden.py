@@ -113,6 +113,8 @@ FIT_CASES = {
     "etr2": (("blobs", 12000, 128, 200, 3, 4.0), dict(k=100, max_iters=25, seed=1)),
     # the c2 dimensionality: 24 tail blocks of 64 after d' = 192, R from a 1536 x 1536 QR
     "wide": (("skewed", 8000, 1536, 128, 17), dict(k=64, max_iters=5, seed=3)),
+    # the c3 family: d = 1024 with early termination by recall
+    "etr_wide": (("skewed", 10000, 1024, 256, 23), dict(k=128, max_iters=10, seed=4)),
 }
 
 
@@ -277,6 +279,8 @@ def main():
         path = os.path.join(HERE, "fits.npz")
         out = {k: v for k, v in np.load(path).items() if not k.startswith(name + "_")}
         spec, kw = FIT_CASES[name]
+        if name.startswith("etr"):
+            kw = dict(kw, etr=skm.EtrConfig(n_queries=300, top_k=10))
         fit_case(name, make_x(spec), skm.KMeansConfig(**kw), out)
         np.savez_compressed(path, **out)
         return
