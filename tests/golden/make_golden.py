@@ -141,7 +141,18 @@ def fits():
     out["hier_assign"] = h.assignments
     out["hier_k"] = np.array(h.k)
     out["hier_meso_assign_snap"] = np.array(0)
+    out.update(hier_wide())
     return out
+
+
+def hier_wide():
+    """Hierarchical at the c5 dimensionality (d = 1024, skewed blobs)."""
+    x = make_skewed_blobs(*HIER_WIDE[0])
+    h = skm.hierarchical_fit(x, skm.HierarchicalConfig(**HIER_WIDE[1]))
+    return {"hierw_centroids": h.centroids, "hierw_assign": h.assignments, "hierw_k": np.array(h.k)}
+
+
+HIER_WIDE = ((20000, 1024, 300, 29), dict(k_total=400, seed=6))
 
 
 def hostmath():
@@ -282,6 +293,12 @@ def main():
         if name.startswith("etr"):
             kw = dict(kw, etr=skm.EtrConfig(n_queries=300, top_k=10))
         fit_case(name, make_x(spec), skm.KMeansConfig(**kw), out)
+        np.savez_compressed(path, **out)
+        return
+    if "--only-hier-wide" in sys.argv:
+        path = os.path.join(HERE, "fits.npz")
+        out = {k: v for k, v in np.load(path).items() if not k.startswith("hierw_")}
+        out.update(hier_wide())
         np.savez_compressed(path, **out)
         return
     if "--only-cli" in sys.argv:

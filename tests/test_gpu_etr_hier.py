@@ -70,6 +70,20 @@ def test_hierarchical_matches_reference():
     assert rel <= 1e-3, rel
 
 
+def test_hierarchical_wide_matches_reference():
+    """c5 family (d = 1024 skewed blobs, k_total = 400): reference-generated golden."""
+    import paper_2603_20009_b200 as skb
+    from conftest import make_skewed_blobs
+    g = np.load(GOLD)
+    x = make_skewed_blobs(20000, 1024, 300, 29)
+    h = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=400, seed=6))
+    assert h.k == int(g["hierw_k"])
+    agree = float(np.mean(h.assignments == g["hierw_assign"]))
+    assert agree >= 0.999, agree
+    rel = np.linalg.norm(h.centroids - g["hierw_centroids"]) / np.linalg.norm(g["hierw_centroids"])
+    assert rel <= 1e-3, rel
+
+
 def test_hierarchical_concurrent_groups_bitwise_equal_serial(monkeypatch):
     """The fine phase runs its groups on concurrent streams; the result must be bitwise the
     sequential one (groups are independent fits writing disjoint slices)."""
