@@ -115,6 +115,8 @@ FIT_CASES = {
     "wide": (("skewed", 8000, 1536, 128, 17), dict(k=64, max_iters=5, seed=3)),
     # the c3 family: d = 1024 with early termination by recall
     "etr_wide": (("skewed", 10000, 1024, 256, 23), dict(k=128, max_iters=10, seed=4)),
+    # the c4 family: d = 768 (ragged last tail block after d' = 96: 10 x 64 + 32)
+    "mid": (("skewed", 8000, 768, 160, 19), dict(k=96, max_iters=6, seed=8)),
 }
 
 
