@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=1_000_000)
     ap.add_argument("--d", type=int, default=1536)
     ap.add_argument("--k", type=int, default=4096)
     ap.add_argument("--iters", type=int, default=10)
@@ -176,10 +176,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # test-only overrides (tests/test_gpu_multirank.py runs this bench with 2 ranks on one GPU):
+    # SKM_BENCH_DEVICE pins every rank to one device, SKM_DIST_BACKEND=gloo replaces NCCL
+    local = int(os.environ.get("SKM_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SKM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2603_20009_b200 import api, native
     from paper_2603_20009_b200.config import KMeansConfig
     from paper_2603_20009_b200.engine import Comm

@@ -133,3 +133,23 @@ def test_hierarchical_two_ranks_match_single_rank(layout, ranks):
         assert rel <= 1e-6, rel
     for r in range(1, ranks):
         assert np.array_equal(outs[ranks][0]["cent"], outs[ranks][r]["cent"])
+
+
+def test_bench_two_ranks_runs():
+    """bench.py's sharded path end to end under torchrun (2 ranks sharing cuda:0 over gloo):
+    one JSON line from rank 0 with the whole-job metric, e2e and roofline objects."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SKM_BENCH_DEVICE="0", SKM_DIST_BACKEND="gloo")
+    port = 29700 + os.getpid() % 200
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2", "--steps", "1",
+           "--warmup", "3", "--no-cpu-baseline", "--rows", "60000", "--k", "256"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["roofline"]["achieved"] > 0
