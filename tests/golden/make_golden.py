@@ -92,7 +92,12 @@ def fit_case(name, x, cfg, out):
     out[f"{name}_recall"] = np.array(res.recall_history)
     out[f"{name}_snap_assign"] = np.stack([s["assignments"] for s in snaps])
     out[f"{name}_snap_cent"] = np.stack([s["centroids_rotated"] for s in snaps])
-    out[f"{name}_rotation"] = res.rotation.data
+    if res.rotation.dim >= 512:  # large R: pinned by the SHA-256 of its float32 bytes
+        import hashlib
+        out[f"{name}_rotation_sha256"] = np.array(
+            hashlib.sha256(np.ascontiguousarray(res.rotation.data, dtype=np.float32).tobytes()).hexdigest())
+    else:
+        out[f"{name}_rotation"] = res.rotation.data
     if res.sample_indices is not None:
         out[f"{name}_sidx"] = res.sample_indices
     fa = skm.final_assign(x, res, cfg)

@@ -71,7 +71,12 @@ def test_fit_matches_reference_trajectory(name):
     res = skb.fit(x, cfg, inspect=lambda it, ctx: snaps.append(ctx))
     ref_assign = g[f"{name}_snap_assign"]
     assert np.array_equal(res.init_indices, g[f"{name}_init"])
-    assert np.array_equal(res.rotation.data, g[f"{name}_rotation"])  # host QR contract
+    if f"{name}_rotation" in g.files:  # host QR contract
+        assert np.array_equal(res.rotation.data, g[f"{name}_rotation"])
+    else:
+        import hashlib
+        sha = hashlib.sha256(np.ascontiguousarray(res.rotation.data, dtype=np.float32).tobytes()).hexdigest()
+        assert sha == str(g[f"{name}_rotation_sha256"])
     m = min(len(snaps), ref_assign.shape[0])
     all_equal = True
     xr = x if res.sample_indices is None else x[res.sample_indices]
