@@ -93,6 +93,30 @@ class Comm:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
         return t
 
+    @classmethod
+    def local(cls) -> "Comm":
+        """World-size-1 communicator (identity collectives) for work that is rank-local."""
+        c = cls.__new__(cls)
+        c.dist, c.group, c.world, c.rank = None, None, 1, 0
+        return c
+
+    def all_to_all_rows(self, send: torch.Tensor, send_counts: list[int], recv_counts: list[int]) -> torch.Tensor:
+        """Rows [sum(send_counts[:r]), +send_counts[r]) of ``send`` go to rank r; returns the
+        rows received from every rank, in rank order.  NCCL moves device memory directly; other
+        backends (gloo in the one-GPU multi-rank tests) are staged through host memory."""
+        shape = (int(sum(recv_counts)),) + tuple(send.shape[1:])
+        if self.world == 1:
+            return send[:shape[0]].clone()
+        if self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty(shape, dtype=send.dtype, device=send.device)
+            self.dist.all_to_all_single(out, send.contiguous(), output_split_sizes=list(recv_counts),
+                                        input_split_sizes=list(send_counts), group=self.group)
+            return out
+        out = torch.empty(shape, dtype=send.dtype)
+        self.dist.all_to_all_single(out, send.cpu().contiguous(), output_split_sizes=list(recv_counts),
+                                    input_split_sizes=list(send_counts), group=self.group)
+        return out.to(send.device)
+
     def shard(self, n: int) -> tuple[int, int]:
         """Contiguous row range of this rank."""
         per = (n + self.world - 1) // self.world

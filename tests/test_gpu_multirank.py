@@ -79,9 +79,10 @@ def test_two_ranks_match_single_rank(etr):
     assert np.array_equal(two[0]["cent"], two[1]["cent"])  # replicas stay identical
 
 
-def _run_hier(rank, world, port, q, layout):
+def _run_hier(rank, world, port, q, layout, mode="owner"):
     import torch
     import torch.distributed as dist
+    os.environ["SKM_HIER_FINE"] = mode  # read at import
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -102,9 +103,11 @@ def _run_hier(rank, world, port, q, layout):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout,ranks", [("shuffled", 2), ("sorted", 2), ("sorted", 3)])
-def test_hierarchical_two_ranks_match_single_rank(layout, ranks):
-    """Sharded hierarchical fit (2 and 3 ranks: uneven shards) (BASELINE c5's data-sharded form): meso loop sharded,
+@pytest.mark.parametrize("layout,ranks,mode", [("shuffled", 2, "owner"), ("sorted", 3, "owner"),
+                                               ("sorted", 2, "sharded"), ("shuffled", 3, "sharded")])
+def test_hierarchical_two_ranks_match_single_rank(layout, ranks, mode):
+    """Multi-rank hierarchical fit (2 and 3 ranks: uneven shards; fine phase by group owner after
+    one all-to-all, or as sharded loops) (BASELINE c5's data-sharded form): meso loop sharded,
     every group fitted as a sharded loop over its members' rank-local rows.  Integer outputs
     equal the single-process fit, centroids up to the cross-rank f64 summation order, replicas
     identical."""
@@ -113,8 +116,9 @@ def test_hierarchical_two_ranks_match_single_rank(layout, ranks):
     outs = {}
     for world in (1, ranks):
         q = ctx.Queue()
-        port = 29900 + world + (os.getpid() % 500) + (50 if layout == "sorted" else 0) + 10 * ranks
-        ps = [ctx.Process(target=_run_hier, args=(r, world, port, q, layout)) for r in range(world)]
+        port = 29900 + world + (os.getpid() % 400) + (50 if layout == "sorted" else 0) + 10 * ranks + \
+            (100 if mode == "owner" else 0)
+        ps = [ctx.Process(target=_run_hier, args=(r, world, port, q, layout, mode)) for r in range(world)]
         for p in ps:
             p.start()
         res = dict(q.get(timeout=600) for _ in range(world))
@@ -131,6 +135,8 @@ def test_hierarchical_two_ranks_match_single_rank(layout, ranks):
         assert two["work"] == one["work"]
         rel = np.linalg.norm(two["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
         assert rel <= 1e-6, rel
+        if mode == "owner":  # every group fitted on one rank exactly as on one GPU
+            assert np.array_equal(two["cent"], one["cent"])
     for r in range(1, ranks):
         assert np.array_equal(outs[ranks][0]["cent"], outs[ranks][r]["cent"])
 

@@ -59,3 +59,80 @@ def test_group_plans_rebuild_reference_member_lists(world, layout):
             order = states[r][0]
             members.extend((lo + order[p[1]:p[1] + p[2]]).tolist())
         assert members == np.flatnonzero(assign == gi).tolist()
+
+
+def test_group_owners_lpt_deterministic():
+    from paper_2603_20009_b200.hierarchical import group_owners
+    sizes = np.array([5, 1, 9, 3, 0, 7])
+    assert group_owners(sizes, 2).tolist() == [1, 0, 0, 0, 1, 1]
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(0, 1000, 300)
+    for world in (2, 3, 8):
+        own = group_owners(sizes, world)
+        loads = np.bincount(own, weights=sizes, minlength=world)
+        assert loads.max() - loads.min() <= sizes.max()  # LPT bound
+
+
+def _exchange_worker(rank, world, port, q):
+    import os
+    import types
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_20009_b200.engine import Comm
+        from paper_2603_20009_b200.hierarchical import _exchange_groups, group_owners
+        rng = np.random.default_rng(42)
+        n, mk, ld = 997, 23, 8
+        assign = rng.integers(0, mk, n)
+        assign[assign == 4] = 5  # an empty group
+        x = torch.arange(n * ld, dtype=torch.float32).reshape(n, ld)  # row r holds r*ld..
+        comm = Comm()
+        lo, hi = comm.shard(n)
+        a_l = assign[lo:hi]
+        order = torch.as_tensor(np.argsort(a_l, kind="stable").astype(np.int32))
+        counts = np.bincount(a_l, minlength=mk)
+        offs = np.concatenate(([0], np.cumsum(counts)[:-1]))
+        table = np.stack([np.bincount(assign[min(n, r * ((n + world - 1) // world)):
+                                              min(n, (r + 1) * ((n + world - 1) // world))], minlength=mk)
+                          for r in range(world)])
+        owner = group_owners(table.sum(axis=0), world)
+        data = types.SimpleNamespace(x=x[lo:hi], n=hi - lo, ld=ld)
+        rows, gids, goff = _exchange_groups(data, order, offs, table, owner, comm, lo)
+        q.put((rank, {"rows": rows.numpy(), "gids": gids.numpy(), "goff": goff, "owner": owner, "assign": assign,
+                      "x": x.numpy()}))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_groups_gives_owners_their_groups_in_row_order(world):
+    import os
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + world + os.getpid() % 300
+    ps = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    seen = []
+    for r, v in res.items():
+        assert isinstance(v, dict), v
+        assign, owner, x = v["assign"], v["owner"], v["x"]
+        mine = [g for g in range(len(owner)) if owner[g] == r and np.any(assign == g)]
+        assert sorted(v["goff"]) == mine
+        for g in mine:
+            members = np.flatnonzero(assign == g)
+            o = v["goff"][g]
+            assert np.array_equal(v["gids"][o:o + members.size], members)
+            assert np.array_equal(v["rows"][o:o + members.size], x[members])
+        seen.extend(v["gids"].tolist())
+    assert sorted(seen) == list(range(len(res[0]["assign"])))  # every row moved exactly once
