@@ -41,6 +41,9 @@ int skm_abi_version(void);
 
 /* ---- layout / preprocessing --------------------------------------------------------- */
 /* hi = x with the low 13 mantissa bits cleared, lo = x - hi (exact); pad columns -> 0. */
+/* hi may be NULL: lo only.  tcgen05 kind::tf32 truncates raw fp32 operands exactly like the
+ * explicit hi (x & 0xFFFFE000; tools/trunc_probe.py: bit-identical products), so the fp32 rows
+ * themselves serve as the hi operand and only lo needs storing. */
 int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi, float* lo, long long ldo,
                    void* stream);
 /* out[r] = f32(sum_{c<dims} (f64)x[r,c]^2) */

@@ -23,7 +23,7 @@ __global__ void split_hilo_kernel(const float* __restrict__ x, long long ldx, in
     float v = 0.0f;
     if (c < cols) v = x[r * ldx + c];
     const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    hi[idx] = h;
+    if (hi) hi[idx] = h;  // hi == nullptr: lo only (raw fp32 is a valid hi operand)
     lo[idx] = __fsub_rn(v, h);
   }
 }
@@ -48,7 +48,7 @@ __global__ void split_hilo_vec_kernel(const float4* __restrict__ x, long long ld
     h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
     h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
     h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-    hi[r * ldo4 + c4] = h;
+    if (hi) hi[r * ldo4 + c4] = h;
     lo[r * ldo4 + c4] = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z), __fsub_rn(v.w, h.w));
   }
 }

@@ -179,11 +179,13 @@ class DeviceData:
         self.n = xr.shape[0]
         self.d = d
         self.ld = xr.shape[1]
-        self.hi = torch.empty_like(xr)
+        # 3xTF32 operands: the rows themselves are the hi operand (kind::tf32 truncates fp32
+        # inputs bit-identically to the explicit split), only lo = x - trunc(x) is stored
+        self.hi = xr
         self.lo = torch.empty_like(xr)
         if self.n:
-            native.call("skm_split_hilo", ptr(xr), self.ld, self.n, d, ptr(self.hi), ptr(self.lo), self.ld,
-                        stream_handle(), nbytes=12.0 * self.n * self.ld)
+            native.call("skm_split_hilo", ptr(xr), self.ld, self.n, d, None, ptr(self.lo), self.ld,
+                        stream_handle(), nbytes=8.0 * self.n * self.ld)
         self._norms: dict[int, torch.Tensor] = {}
 
     def norms(self, dims: int) -> torch.Tensor:
