@@ -94,7 +94,10 @@ class DeviceRotation:
         b_hi, b_lo = (self.r_hi, self.r_lo) if inverse else (self.rt_hi, self.rt_lo)
         for r0 in range(0, n, chunk_rows):
             m = min(chunk_rows, n - r0)
-            x_hi, x_lo = _split(x_dev[r0:r0 + m], self.d)
+            if inplace:  # the GEMM overwrites these rows: it must read split copies
+                x_hi, x_lo = _split(x_dev[r0:r0 + m], self.d)
+            else:  # raw rows are a bit-identical hi operand (kind::tf32 truncates): store lo only
+                x_hi, x_lo = x_dev[r0:r0 + m], _split_lo(x_dev[r0:r0 + m], self.d)
             _gemm(x_hi, x_lo, b_hi, b_lo, m, self.d, self.d, native.GEMM_STORE, out=out[r0:r0 + m],
                   n_split=_store_split(m, self.d))
             del x_hi, x_lo
@@ -104,6 +107,12 @@ class DeviceRotation:
 def _store_split(m, n):
     from .engine import _l2_split
     return _l2_split(m, n, n, 6)
+
+
+def _split_lo(x: torch.Tensor, cols: int) -> torch.Tensor:
+    lo = torch.empty_like(x)
+    native.call("skm_split_hilo", ptr(x), x.shape[1], x.shape[0], cols, None, ptr(lo), x.shape[1], stream_handle())
+    return lo
 
 
 def _split(x: torch.Tensor, cols: int):
