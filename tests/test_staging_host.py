@@ -45,3 +45,38 @@ def test_staged_gather_rows(staged, n, d, m):
     out = torch.zeros((m, d))
     staged._copy_rows_to_device(x, out, d, idx)
     assert np.array_equal(out.numpy(), x[idx])
+
+
+class _Stream:
+    def wait_event(self, ev):
+        pass
+
+
+@pytest.fixture
+def prefetch(staged, monkeypatch):
+    import contextlib
+    monkeypatch.setattr(torch.cuda, "Stream", lambda dev=None: _Stream())
+    monkeypatch.setattr(torch.cuda, "stream", lambda s: contextlib.nullcontext())
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda dev=None: _Stream())
+    monkeypatch.setattr(torch.Tensor, "record_stream", lambda self, s: None, raising=False)
+    return staged
+
+
+def test_prefetch_batches_cover_rows_in_order(prefetch):
+    x = np.random.default_rng(3).standard_normal((10_501, 19)).astype(np.float32)
+    got = []
+    for s0, e0, xb in prefetch._prefetch_batches(x, 1000, "cpu"):
+        assert xb.shape[0] == e0 - s0
+        got.append((s0, e0, xb[:, :19].numpy().copy()))
+    assert [g[0] for g in got] == list(range(0, 10_501, 1000))
+    assert np.array_equal(np.concatenate([g[2] for g in got]), x)
+
+
+def test_prefetch_batches_early_exit_stops_worker(prefetch):
+    import threading
+    x = np.zeros((50_000, 8), np.float32)
+    before = threading.active_count()
+    for i, _ in enumerate(prefetch._prefetch_batches(x, 100, "cpu")):
+        if i == 2:
+            break  # the consumer raises / stops: the generator's finally must stop and join the worker
+    assert threading.active_count() <= before
