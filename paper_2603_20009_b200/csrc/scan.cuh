@@ -436,11 +436,16 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             }
             ++sb;
           }
+          // the wave's checkpoint thresholds fl(tau * theta[b + 1]) do not depend on the running
+          // sum: load and scale them ahead of the sequential chain (same values, off the chain)
+          float thr_w[SCAN_DEPTH];
+#pragma unroll
+          for (int i = 0; i < SCAN_DEPTH; ++i) thr_w[i] = __fmul_rn(tcur, s_theta[min(snxt + i + 1, nb)]);
 #pragma unroll
           for (int i = 0; i < SCAN_DEPTH; ++i) {
             if (!fin && snxt + i < hi) {
               srun = __fadd_rn(srun, blk[i]);
-              if (srun > __fmul_rn(tcur, s_theta[snxt + i + 1])) {
+              if (srun > thr_w[i]) {
                 fin = ST_PRUNED;
                 W.qpb[qs] = snxt + i;
               }
