@@ -236,6 +236,12 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     } else {
       lrec = a.cand + static_cast<long long>(rl) * a.cap;
     }
+    // candidate records are prefetched one fill batch ahead (their L2 latency then overlaps the
+    // wave that precedes the next fill)
+    int2 pre = make_int2(0, 0);
+    if constexpr (!DENSE) {
+      if (lane < n_src) pre = lrec[lane];
+    }
     cp_async_wait_all();
     __syncwarp();
 
@@ -247,12 +253,15 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         float p = 0.0f;
         bool ok = e < n_src;
         bool cert = false;
+        int2 rec = pre;
+        if constexpr (!DENSE) {
+          if (e + 32 < n_src) pre = lrec[e + 32];
+        }
         if (ok) {
           if constexpr (DENSE) {
             j = e;
             p = dense_row[e];
           } else {
-            const int2 rec = lrec[e];
             j = rec.x;
             p = __int_as_float(rec.y);
             cert = j < 0;  // CAND_CERT0: certified block-0 prune (gemm_tf32x3.cuh)
