@@ -233,3 +233,28 @@ def test_nonfinite_input_rejected_on_device():
     with pytest.raises(skb.NonFiniteValue) as e:
         skb.final_assign(bad, res, cfg, batch_rows=1000)
     assert (e.value.row, e.value.col) == (1700, 5)
+
+
+@pytest.mark.parametrize("d", [96, 256])
+def test_fit_exact_duplicates_vs_oracle(d):
+    """Degenerate data: 60 distinct points each repeated 50 times, k = 80, so Forgy draws
+    duplicate rows -> identical centroid rows -> exact distance ties, which must go to the lowest
+    index (bitwise-identical distances, independent of GEMM rounding): iteration 1 must agree
+    100 % and the empty duplicate clusters must produce the same number of splits.  After a
+    split every member of a duplicated point is exactly equidistant (in exact arithmetic) from
+    the pair r +- delta, so later assignments hinge on ulp-level rounding of the rotated
+    coordinates (3xTF32 vs sgemm) and whole groups of 50 duplicates may legitimately flip, after
+    which the split-heavy dynamics of this data take the two runs to different local optima
+    (observed final WCSS 4002 here vs 5088 for the oracle): only the rounding-independent
+    outcomes are compared."""
+    import paper_2603_20009_b200 as skb
+    from oracle import skm_ref
+    base = make_blobs(60, d, 12, seed=40 + d)
+    x = np.ascontiguousarray(np.repeat(base, 50, axis=0)[np.random.default_rng(d).permutation(3000)])
+    cfg = skb.KMeansConfig(k=80, max_iters=6, seed=9)
+    snaps = []
+    res = skb.fit(x, cfg, inspect=lambda it, ctx: snaps.append(ctx["assignments"]))
+    ref = skm_ref.fit(x, skm_ref.Params(k=80, max_iters=6, seed=9))
+    assert np.array_equal(snaps[0], ref.snapshots[0]["assignments"])
+    assert res.stats[0].n_empty_splits == ref.stats[0].n_empty_splits > 0
+    assert np.isfinite(res.stats[-1].wcss) and len(np.unique(res.assignments)) <= cfg.k

@@ -208,7 +208,8 @@ SCAN_CASES = [
 @pytest.mark.parametrize("seed,n,k,d,dp,sentinel", SCAN_CASES)
 @pytest.mark.parametrize("two_phase,prev_mode,cert", [(False, "random", False), (True, "random", False),
                                                       (True, "nearest", False), (True, "mixed", False),
-                                                      (False, "nearest", True), (False, "mixed", True)])
+                                                      (False, "nearest", True), (False, "mixed", True),
+                                                      (False, "dup", False), (False, "dup", True)])
 def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, prev_mode, cert):
     """Production scan equals the sequential reference scan over all centroids, including the
     survivor/dims counters: the one-phase exact kernel (candidate lists + speculative waves +
@@ -216,7 +217,8 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     change at their previous centroid + exact kernel on the rest).  ``prev_mode`` picks the
     previous assignment: random (most rows re-assign), the nearest centroid (steady state: the
     speculative phase owns almost every row) or 90% nearest.  ``cert``: the gate GEMM also
-    certifies tail-block-0 prunes (ext_k = 64) and the exact scan skips walking them."""
+    certifies tail-block-0 prunes (ext_k = 64) and the exact scan skips walking them.  ``dup``:
+    the second half of the centroids duplicates the first (exact distance ties everywhere)."""
     from oracle import kernels_np as O
     from paper_2603_20009_b200 import native
     from paper_2603_20009_b200.config import pdxify, tail_block_layout
@@ -227,8 +229,10 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     c = x[rng.choice(n, min(k, n), replace=False)] if k <= n else rng.standard_normal((k, d)).astype(np.float32) * 3
     c = np.ascontiguousarray(c[:k], dtype=np.float32)
     k = c.shape[0]
+    if prev_mode == "dup":  # second half duplicates the first: exact ties, the lower index must win
+        c[k // 2:] = c[:k - k // 2]
     prev = rng.integers(0, k, n).astype(np.int32)
-    if prev_mode != "random":
+    if prev_mode not in ("random", "dup"):
         d2 = ((x.astype(np.float64)[:, None, :] - c.astype(np.float64)[None, :, :]) ** 2).sum(-1)
         near = d2.argmin(1).astype(np.int32)
         prev = near if prev_mode == "nearest" else np.where(rng.random(n) < 0.9, near, prev).astype(np.int32)
