@@ -258,3 +258,20 @@ def test_fit_exact_duplicates_vs_oracle(d):
     assert np.array_equal(snaps[0], ref.snapshots[0]["assignments"])
     assert res.stats[0].n_empty_splits == ref.stats[0].n_empty_splits > 0
     assert np.isfinite(res.stats[-1].wcss) and len(np.unique(res.assignments)) <= cfg.k
+
+
+@pytest.mark.parametrize("n,d,k", [(2000, 96, 1), (300, 128, 300), (257, 70, 256)])
+def test_fit_edge_shapes_vs_oracle(n, d, k):
+    """k = 1 (everything in one cluster), n == k (each row its own Forgy centroid: exact zero
+    distances) and n = k + 1: assignments and centroids as the oracle's."""
+    import paper_2603_20009_b200 as skb
+    from oracle import skm_ref
+    x = make_blobs(n, d, max(2, min(k, 40)), seed=n + k)
+    cfg = skb.KMeansConfig(k=k, max_iters=4, seed=2)
+    res = skb.fit(x, cfg)
+    ref = skm_ref.fit(x, skm_ref.Params(k=k, max_iters=4, seed=2))
+    assert float(np.mean(res.assignments == ref.assignments)) >= 0.999
+    assert _rel_l2(res.centroids, ref.centroids) <= 1e-4
+    assert res.terminated_by == ref.terminated_by
+    if k == 1:
+        assert not res.assignments.any()
