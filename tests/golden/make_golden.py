@@ -122,6 +122,10 @@ FIT_CASES = {
     "etr_wide": (("skewed", 10000, 1024, 256, 23), dict(k=128, max_iters=10, seed=4)),
     # the c4 family: d = 768 (ragged last tail block after d' = 96: 10 x 64 + 32)
     "mid": (("skewed", 8000, 768, 160, 19), dict(k=96, max_iters=6, seed=8)),
+    # sampling at d = 1024 (sample drawn before rotation, final_assign over all rows)
+    "sampled_wide": (("skewed", 12000, 1024, 200, 27), dict(k=64, max_iters=6, seed=11, sampling_fraction=0.25)),
+    # sentinel pruning (no seed thresholds) at d = 768
+    "sentinel_wide": (("skewed", 6000, 768, 120, 31), dict(k=48, max_iters=5, seed=12, pruning_sentinel=True)),
 }
 
 
