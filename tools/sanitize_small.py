@@ -1,0 +1,19 @@
+"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck): fit (pruned path with
+certification), sampled fit + final_assign, hierarchical."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import numpy as np  # noqa: E402
+
+from conftest import make_skewed_blobs  # noqa: E402
+import paper_2603_20009_b200 as skb  # noqa: E402
+
+x = make_skewed_blobs(3000, 200, 40, 3)
+r = skb.fit(x, skb.KMeansConfig(k=48, max_iters=4, seed=1))
+cfg = skb.KMeansConfig(k=32, max_iters=3, seed=2, sampling_fraction=0.5)
+r2 = skb.fit(x, cfg)
+a = skb.final_assign(x, r2, cfg)
+h = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=60, seed=3))
+print("ok", r.k, r2.k, int(a.max()), h.k)
