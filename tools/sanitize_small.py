@@ -1,5 +1,6 @@
-"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck): fit (pruned path with
-certification), sampled fit + final_assign, hierarchical."""
+"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck; initcheck takes > 18 min
+once the ETR part runs): fit (pruned path with certification), sampled fit + final_assign,
+hierarchical, ETR fit, IVF probe evaluation."""
 import os
 import sys
 
@@ -16,4 +17,10 @@ cfg = skb.KMeansConfig(k=32, max_iters=3, seed=2, sampling_fraction=0.5)
 r2 = skb.fit(x, cfg)
 a = skb.final_assign(x, r2, cfg)
 h = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=60, seed=3))
-print("ok", r.k, r2.k, int(a.max()), h.k)
+# ETR: device ground truth (GEMM + radix top-k), probe tally every iteration
+r3 = skb.fit(x, skb.KMeansConfig(k=40, max_iters=6, seed=4, etr=skb.EtrConfig(n_queries=200, top_k=10)))
+# IVF probe evaluation (probe ranking + tally with explored sizes)
+q = x[:100]
+gt = skb.brute_force_topk(x, q, 10)
+pe = skb.probe_eval(r.centroids, skb.build_cluster_lists(r.assignments, r.k), x, q, gt, 5, top_ks=(10,))
+print("ok", r.k, r2.k, int(a.max()), h.k, r3.terminated_by, round(pe["recall_at_10"], 3))
