@@ -295,8 +295,15 @@ class Workspace:
         # 128-row gate-GEMM tiles over the SMs (one CTA per SM) so no launch ends on a
         # partial wave except the last
         per_wave = 128 * _sm_count(dev)
-        b = min(cfg.x_batch_device, (16 << 30) // (8 * self.cap))
+        mem_rows = (16 << 30) // (8 * self.cap)
+        b = min(cfg.x_batch_device, mem_rows)
         b = max(per_wave, b // per_wave * per_wave) if b >= per_wave else max(128, b // 128 * 128)
+        if n > b:
+            if n <= b + b // 4 and n <= mem_rows:
+                b = n  # one launch instead of a near-empty tail batch (e.g. 125K-row shards at 8 GPUs)
+            else:  # balance the batches, whole waves each
+                even = -(-n // -(-n // b))
+                b = min(b, -(-even // per_wave) * per_wave if b >= per_wave else max(128, even))
         b = max(128, min(max(n, 1), b))
         self.batch = b
         i32, f32 = torch.int32, torch.float32
