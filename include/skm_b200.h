@@ -104,8 +104,8 @@ typedef struct skm_gemm_params {
   float* out; long long ldo;   /* STORE / DIST */
   const float* xsq;            /* per-row norm (DIST/ARGMIN/GATE) */
   const float* ysq;            /* per-column norm */
-  int* assign; float* tau;     /* ARGMIN, n_split == 1 */
-  unsigned long long* keys;    /* ARGMIN, n_split > 1: pre-filled with ~0ull */
+  int* top;                    /* ARGMIN: int4 records {best bits, best col, second bits, 0} per
+                                * (N split, row): top[4 * (split * M + row)]; skm_argmin_merge */
   const float* thr;            /* GATE: per-row threshold (keep iff dist <= thr) */
   int* cand; int* cand_cnt; int cand_cap;  /* cand: [M][cand_cap] records {index, float bits} */
   long long row_offset;        /* ARGMIN/GATE output row offset */
@@ -115,8 +115,41 @@ typedef struct skm_gemm_params {
   int ext_k; const float* xsq_ext; const float* ysq_ext; const float* thr1; float cert_eps;
 } skm_gemm_params;
 int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream);
-int skm_decode_argmin_keys(const unsigned long long* keys, int n, int* assign, float* tau, void* stream);
-int skm_fill_u64(unsigned long long* p, long long n, unsigned long long v, void* stream);
+/* Merge the ARGMIN top-2 records: assign = lowest index among the smallest distances, tau = its
+ * tensor-core distance; rows whose runner-up lies within the rigorous tensor-core error bound
+ * (kap * (2 (xsq + *ysq_max) + best + second)) are appended to amb_rows (count in *amb_count,
+ * zeroed by the caller) for an exact re-evaluation (core.py:183-190 semantics). */
+int skm_argmin_merge(const int* top, int n_split, int n, const float* xsq, const float* ysq_max, float kap,
+                     int* assign, float* tau, int* amb_rows, unsigned int* amb_count, void* stream);
+/* Exact argmin (lowest column on ties) of dense distance rows; writes assign/tau[row_ids[r]]. */
+int skm_dense_argmin(const float* dist, long long ld, int rows, int cols, const int* row_ids, int* assign,
+                     float* tau, void* stream);
+/* tau[i] = the reference's GEMM + expansion distance of (row i, centroid assign[i]): inner product
+ * chain of skm_chain_gemm (flavour, q) over d, then max(0, fl(fl(-2 ip + xsq_i) + ysq_a)). */
+int skm_exact_pair_dist(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign,
+                        int n, int d, const float* xsq, const float* ysq, int flavour, int q, float* out,
+                        void* stream);
+/* *out = max(v[0..n)) (>= 0), one CTA */
+int skm_max_f32(const float* v, int n, float* out, void* stream);
+
+/* ---- exact-chain fp32 GEMM on the CUDA cores (bitwise the reference's GEMM backends) -------
+ * out[i][j] = chain over t < K of a[i][t] * b[j][t]; flavour 0 = fused multiply-add chain with
+ * OpenBLAS's threaded K blocking (q = 448: blocks restart from +0 and are added to the output),
+ * flavour 1 = separate multiply / add chain (portable_matmul, _kernels.pyx:122-142; q = 0).
+ * mode 0 stores the products, mode 1 the clamped squared distances
+ * max(0, fl(fl(-2 acc + xsq_i) + ysq_j)) (distance.py:66-82 / evaluation.py:42-50).
+ * Replaces: preprocess.py:37-52 (x @ R, C @ R^T), evaluation.py:42-50 (queries @ x.T). */
+typedef struct skm_chain_params {
+  const float* a; long long lda;
+  const float* b; long long ldb;
+  int M, N, K;
+  int flavour;                 /* 0 fma (OpenBLAS sgemm), 1 mul+add (portable) */
+  int q;                       /* K block of the blocked driver (448), 0 = one chain */
+  int mode;                    /* 0 store, 1 distance */
+  float* out; long long ldo;
+  const float* xsq; const float* ysq;
+} skm_chain_params;
+int skm_chain_gemm(const skm_chain_params* p, void* stream);
 
 /* ---- centroid update ------------------------------------------------------------------ */
 /* stable sort of row ids by assignment; counts/offsets int32[k] */
@@ -139,7 +172,11 @@ int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n
 /* ---- production pruning scan (fused gate candidates -> exact sequential-tau scan) ---- */
 /* tails[j][q][b][r] = C[j][d'+64b+4q+r], zero padded; nb = ceil((d-d')/64) */
 int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream);
-int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, void* stream);
+/* thr[i] = fl(tau[i] * f0) (inf when sentinel); with kap > 0 the emission threshold of the tensor-core
+ * gate instead: every candidate whose exact distance may pass fl(tau * f0) is kept,
+ * thr[i] >= (fl(tau f0) + kap (xsq[i] + *ysq_max)) / (1 - kap). */
+int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, const float* xsq,
+                       const float* ysq_max, float kap, void* stream);
 typedef struct skm_scan_params {
   const int* cand; const int* cand_cnt; int cap;  /* list mode: [rows][cap] {index, float bits} */
   const float* dense; long long ld_dense; const int* dense_row; int k;       /* dense mode */
@@ -152,22 +189,16 @@ typedef struct skm_scan_params {
   float* tau; int* assign;                     /* global rows (row0 + local) */
   unsigned long long* counters;                /* += {survivors, dims touched, changed} */
   int dense_mode;
-  unsigned long long* counters_ext;            /* optional diagnostics: += {block sums computed} */
+  unsigned long long* counters_ext;            /* optional diagnostics: += {block sums computed, warp waves,
+                                                  -, candidates re-evaluated with the exact chain} */
   unsigned long long* prune_hist;              /* optional diagnostics: survivors by prune block */
+  /* tensor-core candidate distances (kap > 0): the reference's value lies within
+   * kap * (xsq[row] + *ysq_max + p) of p; unsettled decisions and possible new bests recompute it
+   * with the exact chain over the d' front columns of x and cent (flavour / q as skm_chain_gemm) */
+  float kap; const float* xsq; const float* ysq; const float* ysq_max;
+  const float* cent; long long ldc; int chain_flavour; int chain_q;
 } skm_scan_params;
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
-/* Block-major tails T2[j][b][t] = C[j][d' + 64 b + t] (zero padded), the layout of the
- * speculative pair scan. */
-int skm_build_tails_blk(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream);
-/* Production scan (list mode; same semantics and outputs as skm_pruned_scan): rounds of the
- * speculative pair scan (each row resolved one tau change at a time, exact counters from
- * per-position outcome records), then the exact sequential scan over rows still open.
- * p->work: >= 20 device u32; scratch: skm_scan2_scratch_bytes(n_rows, cap) bytes of device
- * memory; p->counters_ext (optional): 6 u64 diagnostics.
- * Replaces the scan_bank loop of core.py:237-257 (_kernels.pyx:14-82) for a whole batch. */
-long long skm_scan2_scratch_bytes(int n_rows, int cap);
-int skm_pruned_scan2(const skm_scan_params* p, const float* tails_blk, void* scratch, long long scratch_bytes,
-                     void* stream);
 
 /* ---- exact top-k + ETR tally ------------------------------------------------------- */
 /* k smallest of each row by (value, column) ascending, ties to the lower column (stable

@@ -66,7 +66,14 @@ class KMeansResult:
 
 # ------------------------------------------------------------------------------ rotation
 class DeviceRotation:
-    """R resident on device in both operand orientations (split once)."""
+    """R resident on device in both operand orientations; X.R and C.R^T as the exact fma chain of
+    OpenBLAS's threaded sgemm (preprocess.py:37-52; csrc/sgemm_chain.cuh), so the rotated rows --
+    which every later value of the loop depends on -- are bitwise the reference's.
+
+    ``SKM_FAST_ROTATION=1`` selects the 3xTF32 tensor-core GEMM instead (~4x faster, rows differ
+    from the reference at the ulp level; for timing comparisons only)."""
+
+    FAST = os.environ.get("SKM_FAST_ROTATION", "0") == "1"
 
     def __init__(self, rotation: RotationMatrix, dev):
         d = rotation.dim
@@ -76,14 +83,17 @@ class DeviceRotation:
         r[:, :d].copy_(torch.from_numpy(np.ascontiguousarray(rotation.data, dtype=np.float32)))  # one upload
         rt = torch.zeros((d, ld), dtype=torch.float32, device=dev)
         rt[:, :d] = r[:, :d].t()  # transposed on the device
-        self.r_hi, self.r_lo = _split(r, d)     # rows of R   -> X @ R^T (unrotate)
-        self.rt_hi, self.rt_lo = _split(rt, d)  # rows of R^T -> X @ R   (rotate)
+        self.r, self.rt = r, rt   # rows of R -> X @ R^T (unrotate); rows of R^T -> X @ R (rotate)
+        if self.FAST:
+            self.r_hi, self.r_lo = _split(r, d)
+            self.rt_hi, self.rt_lo = _split(rt, d)
 
     def apply(self, x_dev: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = False,
               inplace: bool = False, chunk_rows: int = 1 << 20) -> torch.Tensor:
-        """out = x @ R (or x @ R^T); x_dev (n, ld) padded.  Row chunks are split and multiplied
-        one at a time, so the extra HBM is one chunk's hi/lo operands; ``inplace`` writes each
-        chunk's result over its input rows (the operands are the split copies)."""
+        """out = x @ R (or x @ R^T); x_dev (n, ld) padded.  ``inplace`` writes the result over the
+        input rows, one row chunk at a time through a chunk-sized buffer (the GEMM reads a whole
+        row tile while other CTAs write, so it never runs in place)."""
+        from .engine import GEMM_Q, chain_gemm
         n = x_dev.shape[0]
         if inplace:
             out = x_dev
@@ -91,16 +101,21 @@ class DeviceRotation:
             out = torch.zeros((n, padded_ld(self.d)), dtype=torch.float32, device=x_dev.device)
         if n == 0:
             return out
-        b_hi, b_lo = (self.r_hi, self.r_lo) if inverse else (self.rt_hi, self.rt_lo)
+        tmp = torch.empty((min(n, chunk_rows), out.shape[1]), dtype=torch.float32, device=x_dev.device) \
+            if inplace else None
         for r0 in range(0, n, chunk_rows):
             m = min(chunk_rows, n - r0)
-            if inplace:  # the GEMM overwrites these rows: it must read split copies
-                x_hi, x_lo = _split(x_dev[r0:r0 + m], self.d)
-            else:  # raw rows are a bit-identical hi operand (kind::tf32 truncates): store lo only
+            dst = tmp[:m] if inplace else out[r0:r0 + m]
+            if self.FAST:
+                b_hi, b_lo = (self.r_hi, self.r_lo) if inverse else (self.rt_hi, self.rt_lo)
                 x_hi, x_lo = x_dev[r0:r0 + m], _split_lo(x_dev[r0:r0 + m], self.d)
-            _gemm(x_hi, x_lo, b_hi, b_lo, m, self.d, self.d, native.GEMM_STORE, out=out[r0:r0 + m],
-                  n_split=_store_split(m, self.d))
-            del x_hi, x_lo
+                _gemm(x_hi, x_lo, b_hi, b_lo, m, self.d, self.d, native.GEMM_STORE, out=dst,
+                      n_split=_store_split(m, self.d))
+                del x_lo
+            else:
+                chain_gemm(x_dev[r0:r0 + m], self.r if inverse else self.rt, m, self.d, self.d, dst, 0, GEMM_Q)
+            if inplace:
+                out[r0:r0 + m].copy_(dst)
         return out
 
 
@@ -362,30 +377,8 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
     dev = x_dev.device
     timer = _Timer()
     ws = None
-    first_pass_done = False
-    n_local0 = x_dev.shape[0]
     if isinstance(rotation, _RotationJob):
-        if comm.world == 1 and cfg.etr is None and 0 < n_local0 and not (cfg.k > n_local0):
-            # The host QR of R is still running.  Iteration 1 is a full argmin and squared
-            # distances are rotation invariant, so it runs on the unrotated rows against the
-            # unrotated Forgy rows now (same assignments up to distance near-ties, like any
-            # GEMM-vs-OpenBLAS difference); the loop then starts from its result.
-            from .engine import Centroids, Workspace, full_assign_pass
-            from .hostmath import init_indices as _ii
-            timer.start("gemm")
-            d0 = DeviceData(x_dev, d)
-            idx0 = torch.tensor(_ii(n_local0, cfg.k, [cfg.seed, 2]), dtype=torch.int64, device=dev)
-            rows0 = torch.zeros((cfg.k, d0.ld), dtype=torch.float32, device=dev)
-            native.call("skm_gather_rows", ptr(d0.x), d0.ld, ptr(idx0), cfg.k, d0.ld, ptr(rows0), d0.ld,
-                        stream_handle())
-            c0 = Centroids(rows0, d)
-            c0.refresh(d, None)
-            ws = Workspace(dev, n_local0, cfg.k, d, cfg)
-            full_assign_pass(d0, c0, ws)
-            del d0, c0, rows0
-            first_pass_done = True
-            timer.stop("gemm")
-        rotation = rotation.get()
+        rotation = rotation.get()  # the host QR ran beside the H2D copy
     timer.start("rotation")
     rot = DeviceRotation(rotation, dev)
     xr = rot.apply(x_dev, inplace=consume_input)  # consume_input: x_dev is a private copy
@@ -404,8 +397,8 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
         etr = EtrState(cfg)
     phase = dict(timer.collect())
     out = fit_rotated_device(data, cfg, inspect=inspect, comm=comm, n_global=n, row_lo=row_lo, init_rows=init_rows,
-                             init_idx=init_idx, etr=etr, timer=timer, ws=ws, first_pass_done=first_pass_done)
-    for key, v in out.phase_seconds.items():  # "gemm" may hold iteration 1 on the unrotated rows
+                             init_idx=init_idx, etr=etr, timer=timer, ws=ws)
+    for key, v in out.phase_seconds.items():
         phase[key] = phase.get(key, 0.0) + v
     timer.start("unrotate")
     cent = rot.apply(out.centroids_dev, inverse=True)
@@ -495,7 +488,7 @@ def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, b
     else:
         cents.refresh(d, None)
         plan = None
-    cfg_ws = KMeansConfig(k=k, x_batch_device=cfg.x_batch_device, cand_cap=cfg.cand_cap)
+    cfg_ws = KMeansConfig(k=k, x_batch_device=cfg.x_batch_device, cand_cap=cfg.cand_cap, gemm_backend=cfg.gemm_backend)
     ws = Workspace(dev, min(batch_rows, max(n, 1)), k, d, cfg_ws)  # reused by every batch
     for s0, e0, xb in _prefetch_batches(x_full, batch_rows, dev):
         key = _nonfinite_key(xb, e0 - s0, d)

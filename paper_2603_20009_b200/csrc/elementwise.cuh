@@ -2,6 +2,7 @@
 // threshold seeding, bit-exact bank scan (parity ABI), portable matmul (parity ABI),
 // assignment statistics, split application.
 #pragma once
+#include "sgemm_chain.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -289,10 +290,17 @@ __global__ void __launch_bounds__(SEED_ROWS)
 // running sum, so the result is bitwise the d-column chain.  Needs 16-byte aligned rows.
 constexpr int SEEDA_LD = 36;  // padded row (floats): LDS.128 quarter-warps hit 8 distinct bank groups
 constexpr int SEEDA_SMEM = 2 * 2 * SEED_ROWS * SEEDA_LD * 4;
+// PAIR = 0: seed_thresholds (sub / mul / add chain, _kernels.pyx:97-103).
+// PAIR = 1 / 2: the exact squared distance the reference's GEMM + expansion gives the pair
+// (row, assign[row]) (distance.py:58-82): the fma (OpenBLAS, K blocks of q) or mul+add
+// (portable) inner-product chain of sgemm_chain.cuh, then max(0, fl(fl(-2 ip + xsq) + ysq)).
+// Used after the tensor-core argmin of a full pass to give tau its reference bits.
+template <int PAIR>
 __global__ void __launch_bounds__(SEED_ROWS)
     seed_thresholds_async_kernel(const float* __restrict__ x, long long ldx, const float* __restrict__ cent,
                                  long long ldc, const int* __restrict__ assign, int n, int d,
-                                 float* __restrict__ out) {
+                                 float* __restrict__ out, const float* __restrict__ xsq = nullptr,
+                                 const float* __restrict__ ysq = nullptr, int kq = 0) {
   extern __shared__ __align__(16) float seed_smem[];  // [buf][x|c][row][SEEDA_LD], 73.7 KB
   auto tile = reinterpret_cast<float(*)[2][SEED_ROWS][SEEDA_LD]>(seed_smem);
   const int r0 = blockIdx.x * SEED_ROWS;
@@ -324,6 +332,8 @@ __global__ void __launch_bounds__(SEED_ROWS)
   };
   const int nchunk = (d + 31) / 32;
   float acc = 0.0f;
+  float tot = 0.0f;                                   // PAIR: finished K blocks
+  int next_b = PAIR == 1 ? chain_next_boundary(0, d, kq) : d;  // PAIR 1: next K-block boundary
   issue(0, 0);
   for (int ch = 0; ch < nchunk; ++ch) {
     const int buf = ch & 1;
@@ -336,21 +346,130 @@ __global__ void __launch_bounds__(SEED_ROWS)
     __syncthreads();
     const float4* xr = reinterpret_cast<const float4*>(&tile[buf][0][tid][0]);
     const float4* cr = reinterpret_cast<const float4*>(&tile[buf][1][tid][0]);
+    if constexpr (PAIR == 0) {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const float4 a = xr[v], c = cr[v];
-      float df = __fsub_rn(a.x, c.x);
-      acc = __fadd_rn(acc, __fmul_rn(df, df));
-      df = __fsub_rn(a.y, c.y);
-      acc = __fadd_rn(acc, __fmul_rn(df, df));
-      df = __fsub_rn(a.z, c.z);
-      acc = __fadd_rn(acc, __fmul_rn(df, df));
-      df = __fsub_rn(a.w, c.w);
-      acc = __fadd_rn(acc, __fmul_rn(df, df));
+      for (int v = 0; v < 8; ++v) {
+        const float4 a = xr[v], c = cr[v];
+        float df = __fsub_rn(a.x, c.x);
+        acc = __fadd_rn(acc, __fmul_rn(df, df));
+        df = __fsub_rn(a.y, c.y);
+        acc = __fadd_rn(acc, __fmul_rn(df, df));
+        df = __fsub_rn(a.z, c.z);
+        acc = __fadd_rn(acc, __fmul_rn(df, df));
+        df = __fsub_rn(a.w, c.w);
+        acc = __fadd_rn(acc, __fmul_rn(df, df));
+      }
+    } else {
+      const int t0 = 32 * ch;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const float4 a = xr[v], c = cr[v];
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if constexpr (PAIR == 1) {
+            if (t0 + 4 * v + u == next_b) {  // block boundary (uniform across the CTA)
+              tot = __fadd_rn(tot, acc);
+              acc = 0.0f;
+              next_b = chain_next_boundary(next_b, d, kq);
+            }
+          }
+          // columns past d are zero-filled: fma(0, 0, acc) == acc (acc is never -0)
+          acc = chain_scalar_step<PAIR == 1 ? CHAIN_FMA : CHAIN_MULADD>(av[u], cv[u], acc);
+        }
+      }
     }
     __syncthreads();  // buf is refilled by the next iteration's issue
   }
-  if (r0 + tid < n) out[r0 + tid] = acc;
+  if (r0 + tid < n) {
+    if constexpr (PAIR == 0) {
+      out[r0 + tid] = acc;
+    } else {
+      const float ip = __fadd_rn(tot, acc);
+      const float e = __fadd_rn(__fadd_rn(__fmul_rn(ip, -2.0f), xsq[r0 + tid]), ysq[__ldg(assign + r0 + tid)]);
+      out[r0 + tid] = e > 0.0f ? e : 0.0f;
+    }
+  }
+}
+
+// Merge of the ARGMIN epilogue's per-split top-2 records (gemm_tf32x3.cuh): assign = lowest
+// column among the smallest tensor-core distances; the row is flagged for an exact re-evaluation
+// when the runner-up is within the rigorous error bound of both tensor-core values
+// (|p_tc - p_exact| <= kap * (xsq + ysq_max + p)), i.e. when the exact
+// chain-based distances could order differently or tie.
+__global__ void argmin_merge_kernel(const int4* __restrict__ top, int n_split, int n, const float* __restrict__ xsq,
+                                    const float* __restrict__ ysq_max, float kap, int* __restrict__ assign,
+                                    float* __restrict__ tau, int* __restrict__ amb_rows,
+                                    unsigned int* __restrict__ amb_count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 t = top[i];
+  float best = __int_as_float(t.x), second = __int_as_float(t.z);
+  int bj = t.y;
+  for (int s = 1; s < n_split; ++s) {
+    const int4 u = top[static_cast<long long>(s) * n + i];
+    const float b1 = __int_as_float(u.x), s1 = __int_as_float(u.z);
+    if (b1 < best || (b1 == best && u.y < bj)) {
+      second = fminf(best, s1);
+      best = b1;
+      bj = u.y;
+    } else {
+      second = fminf(second, b1);
+    }
+  }
+  assign[i] = bj;
+  tau[i] = best;
+  if (isfinite(second)) {
+    const float base = xsq[i] + *ysq_max;
+    const float margin = kap * (2.0f * base + best + second);
+    if (second - best <= margin) amb_rows[atomicAdd(amb_count, 1u)] = i;
+  }
+}
+
+// Exact argmin of dense distance rows (lowest column on ties): one warp per row.
+__global__ void dense_argmin_kernel(const float* __restrict__ dist, long long ld, int rows, int cols,
+                                    const int* __restrict__ row_ids, int* __restrict__ assign,
+                                    float* __restrict__ tau) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * (blockDim.x >> 5)) {
+    const float* p = dist + r * ld;
+    float bv = __int_as_float(0x7f800000);
+    int bj = 0x7fffffff;
+    for (int j = lane; j < cols; j += 32) {
+      const float v = p[j];
+      if (v < bv) { bv = v; bj = j; }  // ascending j per lane: first occurrence kept
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+    }
+    if (lane == 0) {
+      const int g = row_ids[r];
+      assign[g] = bj;
+      tau[g] = bv;
+    }
+  }
+}
+
+// max over the column norms (one CTA)
+__global__ void max_f32_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  __shared__ float red[32];
+  float m = 0.0f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *out = m;
+  }
 }
 
 __device__ __forceinline__ void warp_add_u64(unsigned long long v, unsigned long long* dst) {
@@ -429,20 +548,6 @@ __global__ void portable_matmul_kernel(const float* __restrict__ a, long long ld
 }
 
 // keys (dist_bits << 32 | col) -> assign / tau
-__global__ void decode_argmin_keys_kernel(const unsigned long long* __restrict__ keys, int n, int* __restrict__ assign,
-                                          float* __restrict__ tau) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const unsigned long long k = keys[i];
-  assign[i] = static_cast<int>(k & 0xffffffffu);
-  tau[i] = __uint_as_float(static_cast<unsigned int>(k >> 32));
-}
-
-__global__ void fill_u64_kernel(unsigned long long* p, long long n, unsigned long long v) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = v;
-}
-
 // Per-block partials of sum(tau) (f64) and count(assign != prev); fixed-order final pass.
 constexpr int STAT_THREADS = 256;
 __global__ void __launch_bounds__(STAT_THREADS)
@@ -475,16 +580,87 @@ __global__ void __launch_bounds__(STAT_THREADS)
   }
 }
 
-__global__ void assign_stats_final_kernel(const double* __restrict__ part_sum,
+// wcss = float(np.sum(tau, dtype=np.float64)) (core.py:344), bitwise: NumPy reduces the f32 array
+// through 8192-element cast buffers, adding each buffer's pairwise sum (DOUBLE_pairwise_sum:
+// blocks of <= 128 with 8 interleaved accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// larger spans halved at a multiple of 8) to the running result in buffer order
+// (tools/blas_order_probe.py checks this model against np.sum).
+constexpr int NP_SUM_BUF = 8192;
+__device__ __forceinline__ double np_pairwise_leaf(const float* __restrict__ a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, static_cast<double>(a[i]));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], static_cast<double>(a[i + j]));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, static_cast<double>(a[i]));
+  return res;
+}
+
+// the recursion pairwise(a, n) = pairwise(a, n2) + pairwise(a + n2, n - n2) for n > 128, evaluated
+// with an explicit stack (device recursion overflowed the default per-thread stack)
+__device__ double np_pairwise_f32(const float* __restrict__ a, int n) {
+  int lo_s[16], n_s[16], stage[16];
+  double left[16];
+  int top = 0;
+  lo_s[0] = 0;
+  n_s[0] = n;
+  stage[0] = 0;
+  double ret = 0.0;
+  while (top >= 0) {
+    const int m = n_s[top];
+    if (m <= 128) {
+      ret = np_pairwise_leaf(a + lo_s[top], m);
+      --top;
+      continue;
+    }
+    int m2 = m / 2;
+    m2 -= m2 % 8;
+    if (stage[top] == 0) {  // descend left
+      stage[top] = 1;
+      lo_s[top + 1] = lo_s[top];
+      n_s[top + 1] = m2;
+      stage[top + 1] = 0;
+      ++top;
+    } else if (stage[top] == 1) {  // left done: descend right
+      left[top] = ret;
+      stage[top] = 2;
+      lo_s[top + 1] = lo_s[top] + m2;
+      n_s[top + 1] = m - m2;
+      stage[top + 1] = 0;
+      ++top;
+    } else {  // both done
+      ret = __dadd_rn(left[top], ret);
+      --top;
+    }
+  }
+  return ret;
+}
+
+__global__ void np_sum_chunks_kernel(const float* __restrict__ v, long long n, double* __restrict__ part) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long lo = c * NP_SUM_BUF;
+  if (lo >= n) return;
+  part[c] = np_pairwise_f32(v + lo, static_cast<int>(min((long long)NP_SUM_BUF, n - lo)));
+}
+
+__global__ void assign_stats_final_kernel(const double* __restrict__ chunk_sum, int chunks,
                                           const unsigned long long* __restrict__ part_cnt, int parts,
                                           double* __restrict__ out_sum, unsigned long long* __restrict__ out_cnt) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
+    for (int p = 0; p < chunks; ++p) s = __dadd_rn(s, chunk_sum[p]);
     unsigned long long c = 0;
-    for (int p = 0; p < parts; ++p) {
-      s += part_sum[p];
-      c += part_cnt[p];
-    }
+    for (int p = 0; p < parts; ++p) c += part_cnt[p];
     *out_sum = s;
     *out_cnt = c;
   }

@@ -28,7 +28,7 @@ namespace skm {
 enum GemmMode : int {
   GEMM_STORE = 0,    // out = A.B^T (fp32)
   GEMM_DIST = 1,     // out = max(0, fl(fl(-2 acc + xsq_i) + ysq_j))   (distance.py:77-80)
-  GEMM_ARGMIN = 2,   // running (min dist, lowest col) per row        (core.py:183-190)
+  GEMM_ARGMIN = 2,   // running (min dist, lowest col) + second-smallest dist per row (core.py:183-190)
   GEMM_GATE = 3,     // emit (col, dist) for dist <= thr_i in ascending col order
 };
 
@@ -41,9 +41,8 @@ struct GemmArgs {
   long long ldo;
   const float* xsq;           // DIST / ARGMIN / GATE: per-row norm term
   const float* ysq;           // per-column norm term
-  int* assign;                // ARGMIN (grid.y == 1)
-  float* tau;
-  unsigned long long* keys;   // ARGMIN (grid.y > 1): atomicMin((dist_bits<<32)|col)
+  int4* top;                  // ARGMIN: per (N split, row) {best bits, best col, second bits, 0},
+                              // top[split * M + row]; merged by argmin_merge_kernel
   const float* thr;           // GATE: per-row threshold
   int2* cand;                 // GATE: per-row candidate slab [M][cap] of {index, float bits}
   int* cand_cnt;              // GATE: per-row count (may exceed cap -> overflow)
@@ -268,6 +267,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (t_begin < t_end) load_norms(t_begin);
     }
     float best = __int_as_float(0x7f800000);
+    float second = __int_as_float(0x7f800000);  // ARGMIN: smallest distance other than the best
     int best_j = 0x7fffffff;
     int cnt = 0;
     const long long out_row = static_cast<long long>(row) + args.row_offset;
@@ -344,13 +344,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       } else if constexpr (MODE == GEMM_ARGMIN) {
         if (row_ok) {
           const int lim = args.N - col0;  // valid columns in this slice
-          float bv = best;
+          float bv = best, sv = second;
           int bl = -1;
 #pragma unroll
           for (int j = 0; j < HALF; ++j) {
             const float dv = expand_dist(acc[j], xs, ys_tile[j]);
-            if (j < lim && dv < bv) { bv = dv; bl = j; }
+            if (j < lim) {
+              // ascending columns: a strictly smaller value takes over (lowest index on ties);
+              // every other value, ties included, competes for the second place
+              sv = fminf(sv, dv < bv ? bv : dv);
+              if (dv < bv) { bv = dv; bl = j; }
+            }
           }
+          second = sv;
           if (bl >= 0) { best = bv; best_j = col0 + bl; }
         }
       } else if constexpr (MODE == GEMM_GATE) {
@@ -466,28 +472,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if constexpr (MODE == GEMM_ARGMIN) {
       // combine the column slices lexicographically on (dist, col)
+      // (the exchange area holds 2 * GEMM_PARTS * GEMM_BM ints: best | col, then seconds in the
+      // column-norm area behind it, which is no longer read)
       float* xf = reinterpret_cast<float*>(xchg);
+      float* xs2 = reinterpret_cast<float*>(xchg + 2 * GEMM_PARTS * GEMM_BM);
+      epi_bar_sync();  // the last tile's column norms have been consumed by every slice
       xf[half * GEMM_BM + r_local] = best;
       xchg[(GEMM_PARTS + half) * GEMM_BM + r_local] = best_j;
+      xs2[half * GEMM_BM + r_local] = second;
       epi_bar_sync();
       if (half == 0 && row_ok && t_begin < t_end) {
 #pragma unroll
         for (int q = 1; q < GEMM_PARTS; ++q) {
           const float b1 = xf[q * GEMM_BM + r_local];
           const int j1 = xchg[(GEMM_PARTS + q) * GEMM_BM + r_local];
+          const float s1 = xs2[q * GEMM_BM + r_local];
           if (b1 < best || (b1 == best && j1 < best_j)) {
+            second = fminf(best, s1);  // the old best is now a runner-up (second >= best)
             best = b1;
             best_j = j1;
+          } else {
+            second = fminf(second, b1);  // s1 >= b1
           }
         }
-        if (args.n_split == 1) {
-          args.assign[out_row] = best_j;
-          args.tau[out_row] = best;
-        } else {
-          const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(best)) << 32) |
-                                         static_cast<unsigned int>(best_j);
-          atomicMin(args.keys + out_row, key);
-        }
+        const int split = blockIdx.x % args.n_split;
+        args.top[static_cast<long long>(split) * args.M + row] =
+            make_int4(__float_as_int(best), best_j, __float_as_int(second), 0);
       }
     }
     if constexpr (MODE == GEMM_GATE) {

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
+#include "sgemm_chain.cuh"
 
 namespace skm {
 
@@ -42,7 +43,8 @@ namespace skm {
 constexpr int SCAN_DEPTH = SKM_SCAN_DEPTH;     // consecutive blocks per candidate per wave
 constexpr int SCAN_SLOTS = 32 / SCAN_DEPTH;    // candidates in flight per wave
 constexpr int SCAN_WINDOW = SKM_SCAN_WINDOW;   // in-flight queue positions per warp
-constexpr int SCAN_NB_MAX = 40;                // tail blocks supported (d - d' <= 2560)
+constexpr int SCAN_NB_MAX = 104;               // tail blocks supported (d - d' <= 6656): 4 warps x
+                                               // 512 B per block of x tail + records fit in 227 KB
 constexpr int SCAN_WARPS = SKM_SCAN_WARPS;     // warps per CTA
 
 struct ScanArgs {
@@ -72,12 +74,20 @@ struct ScanArgs {
   int* assign;             // global rows, in/out
   unsigned long long* counters;  // [0] survivors, [1] dims touched, [2] changed
   unsigned long long* counters_ext;  // optional diagnostics: [0] 64-dim block sums computed
-  // two-phase scan (spec_scan.cuh)
-  const float4* tails_blk;       // [k][nb][16] float4: block-major tails
-  int* cx_rows;                  // complex rows (batch-local) appended by the speculative phase
-  unsigned int* cx_count;
-  const unsigned int* n_rows_dev;  // exact phase: row count read on device (overrides n_rows)
   unsigned long long* prune_hist;  // optional diagnostics: survivors by prune block (nb = complete)
+  // Exact re-evaluation of tensor-core partial distances.  kap > 0: a candidate's distance p~
+  // comes from the 3xTF32 GEMM and the reference's (chain) value lies in [p~ - D, p~ + D],
+  // D = kap * (xsq[row] + *ysq_max + p~).  Decisions are taken on that
+  // interval; a decision it cannot settle, and every candidate that may replace the current best
+  // (its running sum becomes tau), recomputes p with the reference's chain (exact_dot) first.
+  float kap;
+  const float* xsq;        // global rows: squared norm over the d' front columns
+  const float* ysq;        // centroids: squared norm over d'
+  const float* ysq_max;    // device scalar: max_j ysq[j]
+  const float* cent;       // centroid rows, row-major (front columns for the exact chain)
+  long long ldc;
+  int chain_flavour;       // 0 fma chain with K blocks of chain_q (OpenBLAS), 1 mul+add (portable)
+  int chain_q;
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -97,11 +107,27 @@ __global__ void build_tails_kernel(const float* __restrict__ cent, long long ldc
   }
 }
 
-// thr_i = sentinel ? inf : fl(tau_i * F0)
+// thr_i = sentinel ? inf : fl(tau_i * F0); kap > 0: the tensor-core gate's emission threshold,
+// a rigorous upper end for every p~ whose exact value may pass fl(tau_i * F0):
+// p~ - kap (xsq_i + ysq_max + p~) <= thr  <=>  p~ <= (thr + kap (xsq_i + ysq_max)) / (1 - kap),
+// evaluated in f64 and rounded up (plus 2^-20 relative) so no fp32 rounding can drop a candidate.
 __global__ void gate_threshold_kernel(const float* __restrict__ tau, int n, float f0, int sentinel,
-                                      float* __restrict__ thr) {
+                                      float* __restrict__ thr, const float* __restrict__ xsq,
+                                      const float* __restrict__ ysq_max, float kap) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) thr[i] = sentinel ? __int_as_float(0x7f800000) : __fmul_rn(tau[i], f0);
+  if (i >= n) return;
+  if (sentinel) {
+    thr[i] = __int_as_float(0x7f800000);
+    return;
+  }
+  const float t0 = __fmul_rn(tau[i], f0);
+  if (kap > 0.0f) {
+    const double k = kap;
+    const double t = (static_cast<double>(t0) + k * (static_cast<double>(xsq[i]) + *ysq_max)) / (1.0 - k);
+    thr[i] = __double2float_ru(t * (1.0 + 0x1p-20));
+  } else {
+    thr[i] = t0;
+  }
 }
 
 struct ScanWarpSmem {
@@ -113,6 +139,8 @@ struct ScanWarpSmem {
   int qpb[SCAN_WINDOW];
   float qrun[SCAN_WINDOW];
   int qver[SCAN_WINDOW];    // tau version the outcome was decided under
+  float qdl[SCAN_WINDOW];   // error bound of qp (0: exact)
+  float qrunhi[SCAN_WINDOW];  // upper end of the final running sum (COMPLETE)
   int sel[32];              // dispatch: lane of the r-th taken position
 };
 
@@ -126,31 +154,58 @@ __device__ __forceinline__ float2 sq_diff2(float2 a, float2 b) {
   return make_float2(__uint_as_float(static_cast<unsigned>(q)), __uint_as_float(static_cast<unsigned>(q >> 32)));
 }
 
-enum : int { ST_PENDING = 0, ST_NOTSURV = 1, ST_PRUNED = 2, ST_COMPLETE = 3 };
+// ST_AMBIG: the interval of a tensor-core distance cannot settle the outcome -> exact p needed
+#ifndef SKM_EXF
+#define SKM_EXF exact_front_dist
+#endif
+enum : int { ST_PENDING = 0, ST_NOTSURV = 1, ST_PRUNED = 2, ST_COMPLETE = 3, ST_AMBIG = 4 };
 
-// Exact walk of one recorded candidate under threshold tcur (blocks < nd are available).
-// Returns the status; ST_PENDING if it needs a block that has not been computed yet.
-__device__ __forceinline__ int walk_exact(float p, const float* rec_row, int nd, int nb, float tcur, float f0,
-                                          const float* theta, int& pb, float& run) {
-  if (p > __fmul_rn(tcur, f0)) return ST_NOTSURV;
+// Walk of one recorded candidate under threshold tcur (blocks < nd are available) with its
+// distance known to lie in [p - dl, p + dl] (dl == 0: exact).  Adding a block sum is monotone
+// under round-to-nearest, so the running sums of the two ends bracket the exact one: a checkpoint
+// prunes for certain when the low end exceeds it, and continues for certain when the high end
+// does not.  Returns the exact status (NOTSURV / PRUNED at pb / COMPLETE with run in
+// [run, run_hi]), ST_AMBIG if some checkpoint was not settled, or ST_PENDING if a block that has
+// not been computed yet is needed.  The low-end walk never prunes later than the exact walk
+// would, so the blocks recorded for it cover the exact walk.
+__device__ __forceinline__ int walk_interval(float p, float dl, const float* rec_row, int nd, int nb, float tcur,
+                                             float f0, const float* theta, int& pb, float& run, float& run_hi) {
+  const float thr0 = __fmul_rn(tcur, f0);
+  if (__fsub_rn(p, dl) > thr0) return ST_NOTSURV;
+  bool amb = __fadd_rn(p, dl) > thr0;
   if (nd < 0) {  // GEMM-certified: pruned at block 0 under any tau <= the seed tau
     pb = 0;
-    return ST_PRUNED;
+    return amb ? ST_AMBIG : ST_PRUNED;
   }
-  run = p;
+  float lo = fmaxf(__fsub_rn(p, dl), 0.0f), hi = __fadd_rn(p, dl);
   for (int b = 0; b < nb; ++b) {
     if (b >= nd) return ST_PENDING;
-    run = __fadd_rn(run, rec_row[b]);
-    if (run > __fmul_rn(tcur, theta[b + 1])) {
+    lo = __fadd_rn(lo, rec_row[b]);
+    hi = __fadd_rn(hi, rec_row[b]);
+    const float thr = __fmul_rn(tcur, theta[b + 1]);
+    if (lo > thr) {
       pb = b;
-      return ST_PRUNED;
+      run = lo;
+      return amb ? ST_AMBIG : ST_PRUNED;
     }
+    amb = amb || hi > thr;
   }
-  return ST_COMPLETE;
+  run = lo;
+  run_hi = hi;
+  return amb ? ST_AMBIG : ST_COMPLETE;
+}
+
+// The reference's partial distance of (row, j): chain inner product over the d' front columns
+// (OpenBLAS / portable bits, sgemm_chain.cuh) + expansion (distance.py:66-82).
+__device__ __noinline__ float exact_front_dist(const float* __restrict__ xr, const float* __restrict__ cr, int dp,
+                                               int flavour, int q, float xs, float ys) {
+  const float ip = flavour == 0 ? exact_dot<CHAIN_FMA>(xr, cr, dp, q) : exact_dot<CHAIN_MULADD>(xr, cr, dp, 0);
+  const float e = __fadd_rn(__fadd_rn(__fmul_rn(ip, -2.0f), xs), ys);
+  return e > 0.0f ? e : 0.0f;
 }
 
 #ifndef SKM_SCAN_MINB
-#define SKM_SCAN_MINB 1
+#define SKM_SCAN_MINB 3  // 12 warps per SM: caps registers at 168 (the exact-chain call site raised it to 231)
 #endif
 template <bool DENSE>
 __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
@@ -186,10 +241,8 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
   const unsigned leader_mask = (SCAN_DEPTH == 4) ? 0x11111111u : (SCAN_DEPTH == 8) ? 0x01010101u
                               : (SCAN_DEPTH == 2) ? 0x55555555u : 0xffffffffu;  // slot leader lanes
 
-  unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0;
-  const int n_rows = a.n_rows_dev ? static_cast<int>(*a.n_rows_dev) : a.n_rows;
-  if (a.counters_ext && a.n_rows_dev && blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd(&a.counters_ext[2], static_cast<unsigned long long>(n_rows));  // rows routed here
+  unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0, exact_acc = 0;
+  const int n_rows = a.n_rows;
   while (true) {
     // rows are handed out in order from a global counter: warps running concurrently work on
     // neighbouring (cluster-sorted) rows, so their candidate centroids' tails stay L2-hot
@@ -223,12 +276,16 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     }
     float tcur = a.tau[row];
     int best = a.assign[row];
+    // error-bound base of this row's tensor-core distances: D = kap * (dl_base + p)
+    const float dl_base = a.kap > 0.0f ? __ldg(a.xsq + row) + *a.ysq_max : 0.0f;
+    const float xs_row = a.kap > 0.0f ? __ldg(a.xsq + row) : 0.0f;
     const int best0 = best;
     int ver = 0;  // bumped whenever tau tightens
     int src = 0, F = 0, D = 0, R = 0;
     // slot state: all lanes of a slot hold spos/snxt; the leader also walks (srun, sb, sver)
     int spos = -1, snxt = 0, sb = 0, sver = -1;
-    float srun = 0.0f;
+    float srun = 0.0f, srun_hi = 0.0f;
+    bool samb = false;
     const float* dense_row = nullptr;
     const int2* lrec = nullptr;
     if constexpr (DENSE) {
@@ -267,13 +324,15 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             cert = j < 0;  // CAND_CERT0: certified block-0 prune (gemm_tf32x3.cuh)
             j &= 0x7fffffff;
           }
-          ok = !(p > __fmul_rn(tcur, f0));
         }
+        const float dl = a.kap * (dl_base + p);
+        if (ok) ok = !(__fsub_rn(p, dl) > __fmul_rn(tcur, f0));
         const unsigned m = __ballot_sync(FULL, ok);
         if (ok) {
           const int qs = (F + __popc(m & ((1u << lane) - 1u))) % SCAN_WINDOW;
           W.qj[qs] = j;
           W.qp[qs] = p;
+          W.qdl[qs] = dl;
           W.qdone[qs] = cert ? -1 : 0;  // -1 marks a certified entry: never takes a slot
           W.qstat[qs] = ST_PENDING;
           W.qver[qs] = -1;
@@ -292,9 +351,12 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         while (nfree > 0 && D < F && D < R + SCAN_WINDOW) {
           const int lim = min(min(F, R + SCAN_WINDOW) - D, 32);
           const int pp = D + lane;
-          bool pass = false, gate = false, cert = false;
+          bool pass = false, gate = false, gate_hi = false, cert = false;
           if (lane < lim) {
-            gate = !(W.qp[pp % SCAN_WINDOW] > __fmul_rn(tcur, f0));
+            const float qp = W.qp[pp % SCAN_WINDOW], qd = W.qdl[pp % SCAN_WINDOW];
+            const float thr0 = __fmul_rn(tcur, f0);
+            gate = !(__fsub_rn(qp, qd) > thr0);      // may pass
+            gate_hi = !(__fadd_rn(qp, qd) > thr0);   // passes for certain
             cert = W.qdone[pp % SCAN_WINDOW] < 0;
             pass = gate && !cert;
           }
@@ -307,7 +369,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           }
           if (lane < cut && !pass) {  // decided on the spot: not a survivor, or certified prune
             const int qs = pp % SCAN_WINDOW;
-            W.qstat[qs] = (cert && gate) ? ST_PRUNED : ST_NOTSURV;
+            W.qstat[qs] = !gate ? ST_NOTSURV : (gate_hi ? ST_PRUNED : ST_AMBIG);  // !gate or certified
             W.qpb[qs] = 0;
             W.qver[qs] = ver;
           }
@@ -352,7 +414,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
       while (R < D) {
         const int p = R + lane;
         int st = ST_NOTSURV;  // lanes beyond D: neutral
-        float run = 0.0f;
+        float run = 0.0f, run_hi = 0.0f;
         int pb = 0, j = 0;
         if (p < D) {
           const int qs = p % SCAN_WINDOW;
@@ -360,16 +422,37 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           j = W.qj[qs];
           if (st != ST_PENDING) {
             if (W.qver[qs] != ver) {
-              st = walk_exact(W.qp[qs], rec + qs * nb, W.qdone[qs], nb, tcur, f0, s_theta, pb, run);
+              st = walk_interval(W.qp[qs], W.qdl[qs], rec + qs * nb, W.qdone[qs], nb, tcur, f0, s_theta, pb, run,
+                                 run_hi);
               if (st != ST_PENDING) {
                 W.qstat[qs] = st;
                 W.qpb[qs] = pb;
                 W.qrun[qs] = run;
+                W.qrunhi[qs] = run_hi;
                 W.qver[qs] = ver;
               }
             } else {
               pb = W.qpb[qs];
               run = W.qrun[qs];
+              run_hi = W.qrunhi[qs];
+            }
+            // an unsettled outcome, or an inexact candidate that may replace the best (its
+            // running sum would become tau): recompute p with the reference's chain, walk exactly
+            const bool may_improve = st == ST_COMPLETE && (run < tcur || (run == tcur && j < best));
+            if (st == ST_AMBIG || (may_improve && W.qdl[qs] > 0.0f)) {
+              const float pe = SKM_EXF(a.x + row * a.ldx, a.cent + static_cast<long long>(j) * a.ldc,
+                                                a.d_prime, a.chain_flavour, a.chain_q, xs_row, __ldg(a.ysq + j));
+              W.qp[qs] = pe;
+              W.qdl[qs] = 0.0f;
+              st = walk_interval(pe, 0.0f, rec + qs * nb, W.qdone[qs], nb, tcur, f0, s_theta, pb, run, run_hi);
+              if (st != ST_PENDING) {
+                W.qstat[qs] = st;
+                W.qpb[qs] = pb;
+                W.qrun[qs] = run;
+                W.qrunhi[qs] = run;
+                W.qver[qs] = ver;
+              }
+              ++exact_acc;
             }
           }
         }
@@ -432,17 +515,24 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           if (sver != ver) {  // tau tightened since this walk started: restart from the records
             sver = ver;
             sb = 0;
-            srun = W.qp[qs];
-            if (srun > __fmul_rn(tcur, f0)) fin = ST_NOTSURV;
+            const float qp = W.qp[qs], qd = W.qdl[qs];
+            const float thr0 = __fmul_rn(tcur, f0);
+            srun = fmaxf(__fsub_rn(qp, qd), 0.0f);  // low end: prunes only for certain
+            srun_hi = __fadd_rn(qp, qd);
+            samb = srun_hi > thr0;
+            if (__fsub_rn(qp, qd) > thr0) fin = ST_NOTSURV;
           }
           // blocks recorded in earlier waves (only after a restart), then this wave's
           // blocks straight from registers (static indices)
           while (!fin && sb < snxt) {
             srun = __fadd_rn(srun, rec[qs * nb + sb]);
-            if (srun > __fmul_rn(tcur, s_theta[sb + 1])) {
-              fin = ST_PRUNED;
+            srun_hi = __fadd_rn(srun_hi, rec[qs * nb + sb]);
+            const float thr = __fmul_rn(tcur, s_theta[sb + 1]);
+            if (srun > thr) {
+              fin = samb ? ST_AMBIG : ST_PRUNED;
               W.qpb[qs] = sb;
             }
+            samb = samb || srun_hi > thr;
             ++sb;
           }
           // the wave's checkpoint thresholds fl(tau * theta[b + 1]) do not depend on the running
@@ -454,16 +544,19 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           for (int i = 0; i < SCAN_DEPTH; ++i) {
             if (!fin && snxt + i < hi) {
               srun = __fadd_rn(srun, blk[i]);
+              srun_hi = __fadd_rn(srun_hi, blk[i]);
               if (srun > thr_w[i]) {
-                fin = ST_PRUNED;
+                fin = samb ? ST_AMBIG : ST_PRUNED;
                 W.qpb[qs] = snxt + i;
               }
+              samb = samb || srun_hi > thr_w[i];
               ++sb;
             }
           }
-          if (!fin && sb >= nb) fin = ST_COMPLETE;
+          if (!fin && sb >= nb) fin = samb ? ST_AMBIG : ST_COMPLETE;
           if (fin) {
             W.qrun[qs] = srun;
+            W.qrunhi[qs] = srun_hi;
             W.qver[qs] = ver;
             W.qstat[qs] = fin;
           }
@@ -492,6 +585,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
   if (a.counters_ext) {
     warp_add_u64(blocks_acc, &a.counters_ext[0]);  // speculative block sums computed
     if (lane == 0 && waves_acc) atomicAdd(&a.counters_ext[1], waves_acc);  // warp waves executed
+    warp_add_u64(exact_acc, &a.counters_ext[3]);  // candidates re-evaluated with the exact chain
   }
 }
 

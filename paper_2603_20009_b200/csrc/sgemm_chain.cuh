@@ -1,0 +1,308 @@
+// Exact-chain fp32 GEMM on the CUDA cores: out[i][j] = chain_t A[i][t] * B[j][t], bitwise equal to
+// the reference's GEMM backends.
+//
+// The reference computes every contraction with NumPy `@` -> OpenBLAS sgemm (distance.py:58-59,
+// preprocess.py:43,52, evaluation.py:45) or, with gemm_backend="portable", with the Cython
+// portable_matmul (_kernels.pyx:122-142).  Measured on the survey container (OpenBLAS 0.3.30,
+// SkylakeX kernel, threaded driver; tools/blas_order_probe.py):
+//   * each output element is ONE sequential fused-multiply-add chain over ascending t, starting
+//     from +0 (the AVX-512 micro-kernel keeps one accumulator per output);
+//   * K is blocked by the threaded level-3 driver with GEMM_Q = 448: while more than 2Q remain a
+//     block of Q is taken, a remainder in (Q, 2Q) is halved as ceil(m/2), and every block's chain
+//     restarts from +0 and is added to the running output with one fp32 add (C += alpha * acc);
+//   * portable_matmul: one chain per output with separate rounded multiply and add (the
+//     extension is built with -ffp-contract=off), no K blocking.
+// A tensor-core product cannot reproduce those roundings (every step rounds the running sum), so
+// the contractions whose every output bit matters downstream -- the rotation X.R and C.R^T, the
+// ETR distance blocks -- run here; the large distance GEMMs of the Lloyd loop stay on the tensor
+// cores and only their decisions near a tie are re-evaluated with the same chain (exact_dot below).
+//
+// Tiling: 128x128 output tile per 256-thread CTA, 16-deep k tiles double buffered through shared
+// memory (A stored as duplicated pairs (a, a) so one 64-bit load feeds a packed f32x2 operand),
+// 8x8 outputs per thread as 32 packed pairs: one fma.rn.f32x2 (FFMA2) computes two outputs' chain
+// steps, each lane-exact IEEE fma (measured 74 TFLOP/s peak for FFMA2 on B200,
+// tools/micro/ffma2_bench.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace skm {
+
+constexpr int CH_BM = 128;
+constexpr int CH_BN = 128;
+constexpr int CH_BK = 16;
+constexpr int CH_THREADS = 256;
+constexpr int CH_Q = 448;  // OpenBLAS SkylakeX SGEMM_DEFAULT_Q (threaded driver K blocking)
+
+enum ChainFlavour : int { CHAIN_FMA = 0, CHAIN_MULADD = 1 };
+enum ChainMode : int { CHAIN_STORE = 0, CHAIN_DIST = 1 };
+
+struct ChainArgs {
+  const float* a;
+  long long lda;
+  const float* b;
+  long long ldb;
+  int M, N, K;
+  int q;  // K block size of the blocked driver (0: one chain over all of K)
+  float* out;
+  long long ldo;
+  const float* xsq;  // DIST: per-row norm term
+  const float* ysq;  // DIST: per-column norm term
+};
+
+// next K-block boundary after `k0` under the threaded OpenBLAS rule (q == 0: no blocking)
+__host__ __device__ __forceinline__ int chain_next_boundary(int k0, int K, int q) {
+  if (q <= 0) return K;
+  const int m = K - k0;
+  if (m >= 2 * q) return k0 + q;
+  if (m > q) return k0 + (m + 1) / 2;
+  return K;
+}
+
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  return static_cast<unsigned long long>(__float_as_uint(lo)) |
+         (static_cast<unsigned long long>(__float_as_uint(hi)) << 32);
+}
+__device__ __forceinline__ float f2_lo(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v)); }
+__device__ __forceinline__ float f2_hi(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v >> 32)); }
+
+template <int FLAVOUR>
+__device__ __forceinline__ unsigned long long chain_step2(unsigned long long a, unsigned long long b,
+                                                          unsigned long long c) {
+  unsigned long long d;
+  if constexpr (FLAVOUR == CHAIN_FMA) {
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  } else {
+    // scalar mul.rn / add.rn: ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (observed in
+    // the SASS), which would silently turn the portable chain into the fma chain
+    d = f2_pack(__fadd_rn(f2_lo(c), __fmul_rn(f2_lo(a), f2_lo(b))),
+                __fadd_rn(f2_hi(c), __fmul_rn(f2_hi(a), f2_hi(b))));
+  }
+  return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// One output's chain, scalar: used to re-evaluate single (row, centroid) pairs exactly.
+template <int FLAVOUR>
+__device__ __forceinline__ float chain_scalar_step(float a, float b, float c) {
+  if constexpr (FLAVOUR == CHAIN_FMA) return __fmaf_rn(a, b, c);
+  return __fadd_rn(c, __fmul_rn(a, b));
+}
+
+template <int FLAVOUR>
+__device__ float exact_dot(const float* __restrict__ x, const float* __restrict__ y, int K, int q) {
+  float tot = 0.0f;
+  int k0 = 0;
+  while (k0 < K) {
+    const int k1 = chain_next_boundary(k0, K, q);
+    float acc = 0.0f;
+    int t = k0;
+    if ((((reinterpret_cast<uintptr_t>(x + t) | reinterpret_cast<uintptr_t>(y + t)) & 15) == 0)) {
+      for (; t + 4 <= k1; t += 4) {
+        const float4 u = *reinterpret_cast<const float4*>(x + t);
+        const float4 v = *reinterpret_cast<const float4*>(y + t);
+        acc = chain_scalar_step<FLAVOUR>(u.x, v.x, acc);
+        acc = chain_scalar_step<FLAVOUR>(u.y, v.y, acc);
+        acc = chain_scalar_step<FLAVOUR>(u.z, v.z, acc);
+        acc = chain_scalar_step<FLAVOUR>(u.w, v.w, acc);
+      }
+    }
+    for (; t < k1; ++t) acc = chain_scalar_step<FLAVOUR>(x[t], y[t], acc);
+    tot = __fadd_rn(tot, acc);  // first block: +0 + acc == acc (acc is never -0)
+    k0 = k1;
+  }
+  return tot;
+}
+
+template <int FLAVOUR, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(const ChainArgs g) {
+  extern __shared__ __align__(16) uint8_t ch_smem[];
+  // As2[buf][k][m] = (a, a) pairs, Bs[buf][k][n]
+  unsigned long long* As2 = reinterpret_cast<unsigned long long*>(ch_smem);
+  float* Bs = reinterpret_cast<float*>(ch_smem + 2 * CH_BK * CH_BM * 8);
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * CH_BM, n0 = blockIdx.x * CH_BN;
+  const bool vec = ((g.lda | g.ldb) & 3) == 0 && (g.K & 3) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(g.a) | reinterpret_cast<uintptr_t>(g.b)) & 15) == 0;
+  // global -> register staging: thread loads 8 k-values of one A row and one B row
+  const int lr = tid >> 1, lk = (tid & 1) * 8;
+  const long long arow = m0 + lr, brow = n0 + lr;
+  float ra[8], rb[8];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = k0 + lk + 4 * h;
+      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+      if (vec) {
+        if (arow < g.M && kk < g.K) va = __ldg(reinterpret_cast<const float4*>(g.a + arow * g.lda + kk));
+        if (brow < g.N && kk < g.K) vb = __ldg(reinterpret_cast<const float4*>(g.b + brow * g.ldb + kk));
+      } else {
+        float* pa = &va.x;
+        float* pb = &vb.x;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (arow < g.M && kk + u < g.K) pa[u] = g.a[arow * g.lda + kk + u];
+          if (brow < g.N && kk + u < g.K) pb[u] = g.b[brow * g.ldb + kk + u];
+        }
+      }
+      ra[4 * h + 0] = va.x; ra[4 * h + 1] = va.y; ra[4 * h + 2] = va.z; ra[4 * h + 3] = va.w;
+      rb[4 * h + 0] = vb.x; rb[4 * h + 1] = vb.y; rb[4 * h + 2] = vb.z; rb[4 * h + 3] = vb.w;
+    }
+  };
+  auto sstore = [&](int buf) {
+    unsigned long long* A = As2 + buf * CH_BK * CH_BM;
+    float* B = Bs + buf * CH_BK * CH_BN;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      A[(lk + u) * CH_BM + lr] = f2_pack(ra[u], ra[u]);
+      B[(lk + u) * CH_BN + lr] = rb[u];
+    }
+  };
+
+  unsigned long long acc[8][4];
+  unsigned long long tot[SPLIT ? 8 : 1][SPLIT ? 4 : 1];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+  if constexpr (SPLIT) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tot[i][j] = 0ull;
+  }
+  int next_b = SPLIT ? chain_next_boundary(0, g.K, g.q) : g.K;
+
+  const int ntile = (g.K + CH_BK - 1) / CH_BK;
+  if (ntile > 0) {
+    gload(0);
+    sstore(0);
+  }
+  __syncthreads();
+  for (int kt = 0; kt < ntile; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ntile) gload((kt + 1) * CH_BK);
+    const unsigned long long* A = As2 + buf * CH_BK * CH_BM;
+    const float* B = Bs + buf * CH_BK * CH_BN;
+    const int kbase = kt * CH_BK;
+#pragma unroll
+    for (int kk = 0; kk < CH_BK; ++kk) {
+      if constexpr (SPLIT) {
+        if (kbase + kk == next_b) {  // K-block boundary: fold the block's chains into the output
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              tot[i][j] = add2(tot[i][j], acc[i][j]);
+              acc[i][j] = 0ull;
+            }
+          next_b = chain_next_boundary(next_b, g.K, g.q);
+        }
+      }
+      const ulonglong2* Ak = reinterpret_cast<const ulonglong2*>(A + kk * CH_BM);
+      const ulonglong2 a01 = Ak[ty * 2], a23 = Ak[ty * 2 + 1];
+      const ulonglong2 a45 = Ak[32 + ty * 2], a67 = Ak[32 + ty * 2 + 1];
+      const unsigned long long av[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+      const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
+      const ulonglong2 b47 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + 64 + tx * 4);
+      const unsigned long long bv[4] = {b03.x, b03.y, b47.x, b47.y};
+      if (kbase + kk < g.K) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step2<FLAVOUR>(av[i], bv[j], acc[i][j]);
+      }
+    }
+    if (kt + 1 < ntile) sstore(buf ^ 1);
+    __syncthreads();
+  }
+  if constexpr (SPLIT) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = add2(tot[i][j], acc[i][j]);
+  }
+  // epilogue: rows ty*4 + {0..3}, 64 + ty*4 + {0..3}; columns tx*4 + {0..3}, 64 + tx*4 + {0..3}
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const long long r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (r >= g.M) continue;
+    float xs = 0.0f;
+    if constexpr (MODE == CHAIN_DIST) xs = g.xsq[r];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c0 = n0 + h * 64 + tx * 4;
+      float v[4] = {f2_lo(acc[i][2 * h]), f2_hi(acc[i][2 * h]), f2_lo(acc[i][2 * h + 1]), f2_hi(acc[i][2 * h + 1])};
+      if constexpr (MODE == CHAIN_DIST) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c0 + u < g.N) {
+            const float e = __fadd_rn(__fadd_rn(__fmul_rn(v[u], -2.0f), xs), g.ysq[c0 + u]);
+            v[u] = e > 0.0f ? e : 0.0f;
+          }
+        }
+      }
+      float* o = g.out + r * g.ldo + c0;
+      if (c0 + 4 <= g.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u < g.N) o[u] = v[u];
+      }
+    }
+  }
+}
+
+inline size_t chain_smem_bytes() { return 2 * CH_BK * CH_BM * 8 + 2 * CH_BK * CH_BN * 4; }
+
+// Squared row norms over the leading `dims` columns, bitwise equal to the reference's
+// np.einsum("ij,ij->i", m, m, dtype=np.float64).astype(np.float32) (preprocess.py:95-101).
+// NumPy's einsum inner loop for two contiguous f64 operands and a 0-stride output
+// (sum_of_products_contig_contig_outstride0_two, baseline SSE build: 2 f64 lanes) keeps one
+// 2-lane accumulator; its 4x-unrolled body adds the pairs of each 8-element group in the order
+// (6,7), (4,5), (2,3), (0,1); the remainder is added pair by pair (zero-padded), and the lanes
+// are summed last.  Products of fp32 values are exact in f64, so only the summation order
+// matters (verified bitwise on 3000 x {7..1536} random rows and strided column views,
+// tools/blas_order_probe.py).  One thread per row; the two lanes are independent chains.
+__global__ void row_sq_norms_einsum_kernel(const float* __restrict__ x, long long ldx, int rows, int dims,
+                                           float* __restrict__ out) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const float* p = x + r * ldx;
+    double l0 = 0.0, l1 = 0.0;
+    int t = 0;
+    const bool al = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+    for (; t + 8 <= dims; t += 8) {
+      float v[8];
+      if (al) {
+        const float4 u = __ldg(reinterpret_cast<const float4*>(p + t));
+        const float4 w = __ldg(reinterpret_cast<const float4*>(p + t + 4));
+        v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = p[t + u];
+      }
+#pragma unroll
+      for (int pr = 3; pr >= 0; --pr) {
+        const double e0 = v[2 * pr], e1 = v[2 * pr + 1];
+        l0 = __dadd_rn(l0, e0 * e0);
+        l1 = __dadd_rn(l1, e1 * e1);
+      }
+    }
+    for (; t < dims; t += 2) {
+      const double e0 = p[t];
+      const double e1 = (t + 1 < dims) ? static_cast<double>(p[t + 1]) : 0.0;
+      l0 = __dadd_rn(l0, e0 * e0);
+      l1 = __dadd_rn(l1, e1 * e1);
+    }
+    out[r] = static_cast<float>(__dadd_rn(l0, l1));
+  }
+}
+
+}  // namespace skm

@@ -13,7 +13,7 @@
 #include "gemm_tf32x3.cuh"
 #include "update.cuh"
 #include "scan.cuh"
-#include "spec_scan.cuh"
+#include "sgemm_chain.cuh"
 #include "topk.cuh"
 
 namespace {
@@ -117,9 +117,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   a.ldo = p->ldo;
   a.xsq = p->xsq;
   a.ysq = p->ysq;
-  a.assign = p->assign;
-  a.tau = p->tau;
-  a.keys = p->keys;
+  a.top = reinterpret_cast<int4*>(p->top);
   a.thr = p->thr;
   a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
   a.cand_cnt = p->cand_cnt;
@@ -135,7 +133,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
     if (dbg < 0) { const char* e = getenv("SKM_GEMM_DBG"); dbg = e ? atoi(e) : 0; }
     a.dbg = dbg;
   }
-  if (MODE == skm::GEMM_ARGMIN && split > 1 && !p->keys) return fail(SKM_E_ARG, "ARGMIN with n_split>1 needs keys");
+  if (MODE == skm::GEMM_ARGMIN && !p->top) return fail(SKM_E_ARG, "ARGMIN needs the top-2 record buffer");
   if (MODE == skm::GEMM_GATE && split > 1) return fail(SKM_E_ARG, "GATE requires n_split == 1");
   const long long blocks = static_cast<long long>((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM) * split;
   if (blocks > 0x7fffffffLL) return fail(SKM_E_ARG, "gemm: grid too large");
@@ -146,6 +144,59 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- exact-chain GEMM
+namespace {
+template <int FL, int MODE, bool SPLIT>
+int launch_chain(const skm::ChainArgs& g, cudaStream_t st) {
+  auto kern = skm::sgemm_chain_kernel<FL, MODE, SPLIT>;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(skm::chain_smem_bytes()));
+    if (e != cudaSuccess) return cuda_fail(e, "chain_gemm smem attribute");
+    attr_dev = dev;
+  }
+  dim3 grid((g.N + skm::CH_BN - 1) / skm::CH_BN, (g.M + skm::CH_BM - 1) / skm::CH_BM);
+  if (grid.y > 65535) return fail(SKM_E_ARG, "chain_gemm: too many row tiles for one launch");
+  kern<<<grid, skm::CH_THREADS, skm::chain_smem_bytes(), st>>>(g);
+  SKM_LAUNCH_CHECK("chain_gemm launch");
+  return SKM_OK;
+}
+}  // namespace
+
+extern "C" int skm_chain_gemm(const skm_chain_params* p, void* stream) {
+  if (!p || p->M < 0 || p->N < 0 || p->K < 0) return fail(SKM_E_ARG, "chain_gemm: bad shape");
+  if ((long long)p->M * p->N == 0) return SKM_OK;
+  if (p->mode == 1 && (!p->xsq || !p->ysq)) return fail(SKM_E_ARG, "chain_gemm: distance mode needs xsq/ysq");
+  skm::ChainArgs g{};
+  g.a = p->a; g.lda = p->lda; g.b = p->b; g.ldb = p->ldb;
+  g.M = p->M; g.N = p->N; g.K = p->K; g.q = p->q;
+  g.out = p->out; g.ldo = p->ldo; g.xsq = p->xsq; g.ysq = p->ysq;
+  const bool split = p->q > 0 && p->K > p->q;
+  cudaStream_t st = as_stream(stream);
+  // rows beyond 65535 tiles: consecutive launches over row ranges
+  const int rows_per = 65535 * skm::CH_BM;
+  for (int r0 = 0; r0 < p->M; r0 += rows_per) {
+    skm::ChainArgs h = g;
+    h.M = std::min(rows_per, p->M - r0);
+    h.a = p->a + (long long)r0 * p->lda;
+    h.out = p->out + (long long)r0 * p->ldo;
+    if (h.xsq) h.xsq = p->xsq + r0;
+    int rc;
+    if (p->flavour == 0) {
+      if (p->mode == 0) rc = split ? launch_chain<0, 0, true>(h, st) : launch_chain<0, 0, false>(h, st);
+      else rc = split ? launch_chain<0, 1, true>(h, st) : launch_chain<0, 1, false>(h, st);
+    } else {
+      if (p->mode == 0) rc = split ? launch_chain<1, 0, true>(h, st) : launch_chain<1, 0, false>(h, st);
+      else rc = split ? launch_chain<1, 1, true>(h, st) : launch_chain<1, 1, false>(h, st);
+    }
+    if (rc) return rc;
+  }
+  return SKM_OK;
+}
 
 extern "C" {
 
@@ -174,8 +225,8 @@ int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi,
 
 int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* out, void* stream) {
   if (rows <= 0) return SKM_OK;
-  skm::row_sq_norms_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, dims,
-                                                                                             out);
+  skm::row_sq_norms_einsum_kernel<<<grid_for(rows, 128, 148 * 64), 128, 0, as_stream(stream)>>>(x, ldx, rows, dims,
+                                                                                                out);
   SKM_LAUNCH_CHECK("row_sq_norms");
   return SKM_OK;
 }
@@ -269,12 +320,12 @@ int skm_seed_thresholds(const float* x, long long ldx, const float* centroids, l
   if (aligned) {
     static bool set = false;
     if (!set) {
-      cudaError_t e = cudaFuncSetAttribute(skm::seed_thresholds_async_kernel,
+      cudaError_t e = cudaFuncSetAttribute(skm::seed_thresholds_async_kernel<0>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "seed_thresholds smem attribute");
       set = true;
     }
-    skm::seed_thresholds_async_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, skm::SEEDA_SMEM,
+    skm::seed_thresholds_async_kernel<0><<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, skm::SEEDA_SMEM,
                                         as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out);
   } else {
     skm::seed_thresholds_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, 0, as_stream(stream)>>>(
@@ -432,18 +483,24 @@ int skm_apply_splits(float* centroids, long long ldc, int d, const int* empties,
   return SKM_OK;
 }
 
-long long skm_stats_workspace_bytes(int n) { return 2 * align256(16LL * 1024); }
+long long skm_stats_workspace_bytes(int n) {
+  const long long chunks = (std::max(n, 1) + skm::NP_SUM_BUF - 1) / skm::NP_SUM_BUF;
+  return 2 * align256(16LL * 1024) + align256(8 * chunks);
+}
 
 int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n, double* out_sum,
                      unsigned long long* out_changed, void* workspace, long long workspace_bytes, void* stream) {
   if (workspace_bytes < skm_stats_workspace_bytes(n)) return fail(SKM_E_WORKSPACE, "assign_stats: workspace too small");
   const int parts = std::max(1, std::min(1024, (n + 4095) / 4096));
+  const int chunks = (n + skm::NP_SUM_BUF - 1) / skm::NP_SUM_BUF;
   char* ws = static_cast<char*>(workspace);
   double* ps = reinterpret_cast<double*>(ws);
   unsigned long long* pc = reinterpret_cast<unsigned long long*>(ws + align256(16LL * 1024));
+  double* cs = reinterpret_cast<double*>(ws + 2 * align256(16LL * 1024));
   cudaStream_t st = as_stream(stream);
   skm::assign_stats_partial_kernel<<<parts, skm::STAT_THREADS, 0, st>>>(tau, assign, prev, n, ps, pc);
-  skm::assign_stats_final_kernel<<<1, 32, 0, st>>>(ps, pc, parts, out_sum, out_changed);
+  if (chunks > 0) skm::np_sum_chunks_kernel<<<(chunks + 127) / 128, 128, 0, st>>>(tau, n, cs);
+  skm::assign_stats_final_kernel<<<1, 32, 0, st>>>(cs, chunks, pc, parts, out_sum, out_changed);
   SKM_LAUNCH_CHECK("assign_stats");
   return SKM_OK;
 }
@@ -463,19 +520,59 @@ int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream) {
   }
 }
 
-int skm_decode_argmin_keys(const unsigned long long* keys, int n, int* assign, float* tau, void* stream) {
+int skm_argmin_merge(const int* top, int n_split, int n, const float* xsq, const float* ysq_max, float kap,
+                     int* assign, float* tau, int* amb_rows, unsigned int* amb_count, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::decode_argmin_keys_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(keys, n, assign, tau);
-  SKM_LAUNCH_CHECK("decode_argmin_keys");
+  skm::argmin_merge_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const int4*>(top), n_split, n, xsq, ysq_max, kap, assign, tau, amb_rows, amb_count);
+  SKM_LAUNCH_CHECK("argmin_merge");
   return SKM_OK;
 }
 
-int skm_fill_u64(unsigned long long* p, long long n, unsigned long long v, void* stream) {
-  if (n <= 0) return SKM_OK;
-  skm::fill_u64_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, v);
-  SKM_LAUNCH_CHECK("fill_u64");
+int skm_dense_argmin(const float* dist, long long ld, int rows, int cols, const int* row_ids, int* assign,
+                     float* tau, void* stream) {
+  if (rows <= 0) return SKM_OK;
+  skm::dense_argmin_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(dist, ld, rows, cols,
+                                                                                             row_ids, assign, tau);
+  SKM_LAUNCH_CHECK("dense_argmin");
   return SKM_OK;
 }
+
+int skm_max_f32(const float* v, int n, float* out, void* stream) {
+  skm::max_f32_kernel<<<1, 1024, 0, as_stream(stream)>>>(v, n, out);
+  SKM_LAUNCH_CHECK("max_f32");
+  return SKM_OK;
+}
+
+int skm_exact_pair_dist(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign,
+                        int n, int d, const float* xsq, const float* ysq, int flavour, int q, float* out,
+                        void* stream) {
+  if (n <= 0) return SKM_OK;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(centroids)) & 15) == 0 &&
+                       ldx % 4 == 0 && ldc % 4 == 0;
+  if (!aligned) return fail(SKM_E_ARG, "exact_pair_dist: needs 16-byte aligned rows");
+  auto k1 = skm::seed_thresholds_async_kernel<1>;
+  auto k2 = skm::seed_thresholds_async_kernel<2>;
+  static int set_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "exact_pair_dist smem attribute");
+    set_dev = dev;
+  }
+  const int grid = (n + skm::SEED_ROWS - 1) / skm::SEED_ROWS;
+  if (flavour == 0)
+    k1<<<grid, skm::SEED_ROWS, skm::SEEDA_SMEM, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out, xsq,
+                                                                     ysq, q);
+  else
+    k2<<<grid, skm::SEED_ROWS, skm::SEEDA_SMEM, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out, xsq,
+                                                                     ysq, 0);
+  SKM_LAUNCH_CHECK("exact_pair_dist");
+  return SKM_OK;
+}
+
 
 // ---------------------------------------------------------------- pruning scan
 int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream) {
@@ -487,9 +584,12 @@ int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_p
   return SKM_OK;
 }
 
-int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, void* stream) {
+int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* thr, const float* xsq,
+                       const float* ysq_max, float kap, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::gate_threshold_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(tau, n, f0, sentinel, thr);
+  if (kap > 0.0f && (!xsq || !ysq_max)) return fail(SKM_E_ARG, "gate_threshold: kap needs xsq and ysq_max");
+  skm::gate_threshold_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(tau, n, f0, sentinel, thr, xsq, ysq_max,
+                                                                             kap);
   SKM_LAUNCH_CHECK("gate_threshold");
   return SKM_OK;
 }
@@ -530,6 +630,16 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.counters = p->counters;
   a.counters_ext = p->counters_ext;
   a.prune_hist = p->prune_hist;
+  a.kap = p->kap;
+  a.xsq = p->xsq;
+  a.ysq = p->ysq;
+  a.ysq_max = p->ysq_max;
+  a.cent = p->cent;
+  a.ldc = p->ldc;
+  a.chain_flavour = p->chain_flavour;
+  a.chain_q = p->chain_q;
+  if (a.kap > 0.0f && (!a.xsq || !a.ysq || !a.ysq_max || !a.cent))
+    return fail(SKM_E_ARG, "pruned_scan: kap > 0 needs xsq, ysq, ysq_max and cent");
   const size_t smem = skm::scan_dyn_smem(p->nb);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -542,12 +652,17 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (p->dense_mode) {
     static bool set = false;
-    if (!set) { cudaFuncSetAttribute(skm::pruned_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); set = true; }
+    if (!set) {
+      cudaFuncSetAttribute(skm::pruned_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(skm::scan_dyn_smem(skm::SCAN_NB_MAX)));
+      set = true;
+    }
     skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   } else {
     static bool set = false;
     if (!set) {
-      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(skm::scan_dyn_smem(skm::SCAN_NB_MAX)));
       const char* cv = getenv("SKM_SCAN_CARVEOUT");
       if (cv) cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
       set = true;
@@ -558,164 +673,6 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   return SKM_OK;
 }
 
-int skm_build_tails_blk(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream) {
-  const int nb = (d - d_prime + 63) / 64;
-  if (k <= 0 || nb <= 0) return SKM_OK;
-  skm::build_tails_blk_kernel<<<grid_for((long long)k * 64 * nb, 256), 256, 0, as_stream(stream)>>>(
-      centroids, ldc, k, d, d_prime, nb, tails);
-  SKM_LAUNCH_CHECK("build_tails_blk");
-  return SKM_OK;
-}
-
-// Production scan (list mode): SPEC_ROUNDS rounds of [row_prep_kernel -> spec_scan_kernel]
-// (spec_scan.cuh) -- round 0 over every row of the batch, round r over the rows frozen in
-// round r-1 -- then the exact sequential kernel over any row still open.  All counts stay on
-// the device (no host synchronisation).  p->work: >= 20 device u32; scratch: see
-// skm_scan2_scratch_bytes.  counters_ext (optional, 6 u64): spec blocks, spec waves, exact
-// blocks, exact waves, exact rows, rows of rounds >= 1.
-long long skm_scan2_scratch_bytes(int n_rows, int cap) {
-  const long long n = std::max(n_rows, 1);
-  return (5 * n + n * static_cast<long long>(cap)) * 4 + n * static_cast<long long>(sizeof(skm::RowDesc)) + 256;
-}
-
-int skm_pruned_scan2(const skm_scan_params* p, const float* tails_blk, void* scratch, long long scratch_bytes,
-                     void* stream) {
-  if (!p) return fail(SKM_E_ARG, "pruned_scan2: null params");
-  if (p->n_rows <= 0) return SKM_OK;
-  if (p->dense_mode) return fail(SKM_E_ARG, "pruned_scan2: list mode only");
-  if (p->nb <= 0 || p->nb > skm::SCAN_NB_MAX) return fail(SKM_E_ARG, "pruned_scan2: tail block count out of range");
-  if (!p->work || !tails_blk || !scratch) return fail(SKM_E_ARG, "pruned_scan2: work, tails_blk and scratch required");
-  if (scratch_bytes < skm_scan2_scratch_bytes(p->n_rows, p->cap)) return fail(SKM_E_ARG, "pruned_scan2: scratch too small");
-  if ((reinterpret_cast<uintptr_t>(tails_blk) & 15) != 0) return fail(SKM_E_ARG, "pruned_scan2: tails_blk must be 16-byte aligned");
-  cudaStream_t st = as_stream(stream);
-  unsigned int* work = reinterpret_cast<unsigned int*>(p->work);
-  {
-    cudaError_t e = cudaMemsetAsync(work, 0, 20 * sizeof(unsigned int), st);
-    if (e != cudaSuccess) return cuda_fail(e, "pruned_scan2 work reset");
-  }
-  const long long n = p->n_rows;
-  int* lists[2] = {reinterpret_cast<int*>(scratch), reinterpret_cast<int*>(scratch) + n};
-  int* st_pos = lists[1] + n;
-  float* st_tau = reinterpret_cast<float*>(st_pos + n);
-  int* st_best = reinterpret_cast<int*>(st_tau + n);
-  int* outcome = st_best + n;
-  skm::RowDesc* desc = reinterpret_cast<skm::RowDesc*>(
-      (reinterpret_cast<uintptr_t>(outcome + n * static_cast<long long>(p->cap)) + 63) & ~uintptr_t(63));
-
-  skm::ScanArgs a{};
-  a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
-  a.cand_cnt = p->cand_cnt;
-  a.cap = p->cap;
-  a.k = p->k;
-  a.rows = p->rows;
-  a.n_rows = p->n_rows;
-  a.row0 = p->row0;
-  a.row_map = p->row_map;
-  a.x = p->x;
-  a.ldx = p->ldx;
-  a.tails = reinterpret_cast<const float4*>(p->tails);
-  a.tails_blk = reinterpret_cast<const float4*>(tails_blk);
-  a.nb = p->nb;
-  a.d_prime = p->d_prime;
-  a.theta = p->theta;
-  a.block_dims = p->block_dims;
-  a.tau = p->tau;
-  a.assign = p->assign;
-  a.counters = p->counters;
-  a.counters_ext = p->counters_ext;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  {
-    // kernel shape (SKM_SPEC_CFG overrides for experiments): "P<K>" = pair_scan_kernel<K>
-    // (lane-local inner loop of K blocks), "<G>x<P>" = spec_scan_kernel<G, P>
-    static char cfg[8] = "P2";
-    static bool cfg_read = false;
-    if (!cfg_read) {
-      const char* c = getenv("SKM_SPEC_CFG");
-      if (c && strlen(c) >= 2 && strlen(c) < 8) strcpy(cfg, c);
-      cfg_read = true;
-    }
-    const void* kfn = nullptr;
-    int cfg_g = 0, cfg_p = 0;
-    if (cfg[0] == 'P') {
-      const int K = cfg[1] - '0';
-      if (K == 1) kfn = reinterpret_cast<const void*>(skm::pair_scan_kernel<1>);
-      else if (K == 4) kfn = reinterpret_cast<const void*>(skm::pair_scan_kernel<4>);
-      else kfn = reinterpret_cast<const void*>(skm::pair_scan_kernel<2>);
-    } else {
-      cfg_g = cfg[0] - '0';
-      cfg_p = cfg[2] - '0';
-      if (cfg_g == 2 && cfg_p == 1) kfn = reinterpret_cast<const void*>(skm::spec_scan_kernel<2, 1>);
-      else if (cfg_g == 1 && cfg_p == 2) kfn = reinterpret_cast<const void*>(skm::spec_scan_kernel<1, 2>);
-      else { cfg_g = 2; cfg_p = 2; kfn = reinterpret_cast<const void*>(skm::spec_scan_kernel<2, 2>); }
-    }
-    // as many warps per CTA (one CTA per SM) as shared memory allows
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, kfn);
-    int optin = 232448;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const size_t per_warp = cfg_g ? skm::spec_dyn_smem(p->nb, 1, cfg_g, cfg_p) : skm::pair_dyn_smem(p->nb, 1);
-    const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 256;
-    const int warps = static_cast<int>(std::min<size_t>(skm::SPEC_WARPS, budget / per_warp));
-    if (warps < 1) return fail(SKM_E_ARG, "pruned_scan2: tail too long for the staging budget");
-    const size_t smem = cfg_g ? skm::spec_dyn_smem(p->nb, warps, cfg_g, cfg_p) : skm::pair_dyn_smem(p->nb, warps);
-    const size_t psmem = skm::prep_dyn_smem(p->nb);
-    {
-      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (e != cudaSuccess) return cuda_fail(e, "spec_scan smem attribute");
-    }
-    static size_t set_psmem = 0;
-    if (set_psmem < psmem) {
-      cudaError_t e = cudaFuncSetAttribute(skm::row_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(psmem));
-      if (e != cudaSuccess) return cuda_fail(e, "row_prep smem attribute");
-      set_psmem = psmem;
-    }
-    for (int r = 0; r < skm::SPEC_ROUNDS; ++r) {
-      skm::SpecRound R{};
-      R.round = r;
-      R.in_rows = r ? lists[(r - 1) & 1] : nullptr;
-      R.in_cnt = r ? work + 8 + (r - 1) : nullptr;
-      R.out_rows = lists[r & 1];
-      R.out_cnt = work + 8 + r;
-      R.st_pos = st_pos;
-      R.st_tau = st_tau;
-      R.st_best = st_best;
-      R.outcome = outcome;
-      a.work = work + r;
-      const int pblocks = std::max(1, std::min(static_cast<int>((n + skm::PREP_WARPS - 1) / skm::PREP_WARPS),
-                                               r == 0 ? 8 * sms : 2 * sms));
-      skm::row_prep_kernel<<<pblocks, skm::PREP_WARPS * 32, psmem, st>>>(a, R, desc);
-      SKM_LAUNCH_CHECK("row_prep");
-      const int blocks = std::max(1, std::min(static_cast<int>((n + warps - 1) / warps), sms));
-      void* args[] = {&a, &R, &desc};
-      {
-        cudaError_t e = cudaLaunchKernel(kfn, dim3(blocks), dim3(warps * 32), args, smem, st);
-        if (e != cudaSuccess) return cuda_fail(e, "spec_scan launch");
-      }
-      SKM_LAUNCH_CHECK("spec_scan");
-    }
-  }
-  {
-    // rows still open after the speculative rounds: exact sequential kernel (count on device)
-    skm::ScanArgs e = a;
-    e.rows = lists[(skm::SPEC_ROUNDS - 1) & 1];
-    e.n_rows_dev = work + 8 + skm::SPEC_ROUNDS - 1;
-    e.work = work + 16;
-    e.counters_ext = p->counters_ext ? p->counters_ext + 2 : nullptr;
-    const size_t smem = skm::scan_dyn_smem(p->nb);
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      set = true;
-    }
-    const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms));
-    skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(e);
-    SKM_LAUNCH_CHECK("pruned_scan(exact fallback)");
-  }
-  return SKM_OK;
-}
 
 // ---------------------------------------------------------------- top-k / ETR
 int skm_topk_rows(const float* d, long long ld, int rows, int cols, int k, int* out_idx, float* out_val,

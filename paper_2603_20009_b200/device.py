@@ -65,7 +65,7 @@ def row_sq_norms(x: torch.Tensor, dims: int, out: torch.Tensor | None = None) ->
 
 
 def gemm(a_hi, a_lo, b_hi, b_lo, M: int, N: int, K: int, mode: int, *, out=None, xsq=None, ysq=None,
-         assign=None, tau=None, keys=None, thr=None, cand=None, cand_cnt=None,
+         top=None, thr=None, cand=None, cand_cnt=None,
          cand_cap: int = 0, n_split: int = 1, row_offset: int = 0, ext_k: int = 0, xsq_ext=None, ysq_ext=None,
          thr1=None, cert_eps: float = 0.0) -> None:
     p = native.GemmParams()
@@ -74,7 +74,7 @@ def gemm(a_hi, a_lo, b_hi, b_lo, M: int, N: int, K: int, mode: int, *, out=None,
     p.M, p.N, p.K, p.mode, p.n_split = M, N, K, mode, n_split
     if out is not None:
         p.out, p.ldo = out.data_ptr(), out.stride(0)
-    for name, t in (("xsq", xsq), ("ysq", ysq), ("assign", assign), ("tau", tau), ("keys", keys),
+    for name, t in (("xsq", xsq), ("ysq", ysq), ("top", top),
                     ("thr", thr), ("cand", cand), ("cand_cnt", cand_cnt),
                     ("xsq_ext", xsq_ext), ("ysq_ext", ysq_ext), ("thr1", thr1)):
         if t is not None:

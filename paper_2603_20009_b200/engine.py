@@ -48,21 +48,79 @@ from .hostmath import (
     threshold_factors,
 )
 
-# Scan selection.  Default: the exact sequential kernel (scan.cuh), the fastest measured on
-# B200.  SKM_SCAN=spec selects the multi-round speculative pair scan (spec_scan.cuh, same
-# results bit for bit; see DESIGN.md section 3 for why it is not the default).
-TWO_PHASE_SCAN = os.environ.get("SKM_SCAN", "exact") == "spec"
 PRUNE_HIST = None  # diagnostics (tools/): device u64[nb + 1] histogram of prune blocks
 COLLECT_DIAG = os.environ.get("SKM_DIAG", "0") == "1"  # read scan diagnostics back every iteration
 # GEMM-certified tail-block-0 prunes (gemm_tf32x3.cuh, GATE ext_k): the gate GEMM also sums
 # the first 64 tail dimensions and flags candidates whose distance there exceeds fl(tau F1)
-# by more than CERT_EPS * (|x|^2 + |c|^2) over those dimensions -- far above the 3xTF32 +
-# expansion error -- so the exact scan counts them (survivor, 64 dims) without walking them.
+# by more than cert_eps(K) * (|x|^2 + |c|^2) over those dimensions -- the rigorous bound of
+# both the tensor-core value and the reference's own rounding of that running sum (cert_eps) --
+# so the scan counts them (survivor, 64 dims) without walking them.
 # (a prefix of tail block 0 lower-bounds its running sum, so any ext <= 64 is a valid certificate)
 CERT_EXT = int(os.environ.get("SKM_CERT_EXT", "64")) if os.environ.get("SKM_CERT", "1") != "0" else 0
-CERT_EPS = 3e-5
 
-_U64_MAX = (1 << 64) - 1
+
+def cert_eps(k_dim: int) -> float:
+    """Margin of the block-0 certificate over k_dim = d' + ext columns, relative to xsq + ysq
+    there: the tensor-core distance D~ and the reference's running sum fl(p + block sum) each lie
+    within tc_kappa * (xsq + ysq + D) <= 3 tc_kappa * (xsq + ysq) of the exact distance (D <=
+    2 (xsq + ysq)), so 6 tc_kappa separates them from the threshold for certain."""
+    return 6.0 * tc_kappa(k_dim)
+
+
+# ---------------------------------------------------------------- exact-chain policy
+# The reference's contractions are OpenBLAS sgemm (one fma chain per output, K blocked by 448 in
+# the threaded driver) or, with gemm_backend="portable", the Cython mul+add chain (no blocking);
+# see csrc/sgemm_chain.cuh.  Contractions whose every output bit propagates (the rotation, the
+# un-rotation, the ETR distance blocks) run as that chain on the CUDA cores; the Lloyd loop's
+# large distance GEMMs run on the tensor cores (3xTF32) and every decision that could depend on
+# their rounding is re-evaluated with the chain (argmin near-ties, gate / prune checkpoints and
+# winners in the scan), so the loop reproduces the reference bit for bit.
+GEMM_Q = 448
+_U = 2.0 ** -24
+
+
+def resolve_gemm_backend(backend: str = "auto") -> str:
+    """distance.py:33-43 (env SUPERKMEANS_GEMM when "auto")."""
+    if backend == "auto":
+        env = os.environ.get("SUPERKMEANS_GEMM", "").strip().lower()
+        if env in ("blas", "portable"):
+            return env
+        if env:
+            raise ValueError(f"unknown SUPERKMEANS_GEMM value {env!r}")
+        return "blas"
+    if backend not in ("blas", "portable"):
+        raise ValueError(f"unknown gemm backend {backend!r}")
+    return backend
+
+
+def chain_policy(backend: str = "auto") -> tuple[int, int]:
+    """(flavour, q) of the distance chain: blas -> (fma, 448), portable -> (mul+add, none)."""
+    return (1, 0) if resolve_gemm_backend(backend) == "portable" else (0, GEMM_Q)
+
+
+def tc_kappa(k_dim: int) -> float:
+    """Rigorous bound coefficient for |p_tensor_core - p_chain| <= kappa * (xsq + ysq + p) of a
+    squared distance over k_dim columns: the chain's own error
+    gamma_K = K u / (1 - K u) plus the 3xTF32 error (dropped lo*lo and tf32 truncation of lo:
+    3 * 2^-20 per product, accumulator truncation of the 12 MMAs of a 32-wide k-block, fp32 adds
+    of the k-block partials), with a factor 2 of slack, plus 16 u for the expansion's roundings."""
+    g = k_dim * _U / (1.0 - k_dim * _U)
+    return 2.0 * (g + 2.0 ** -17) + 16.0 * _U
+
+
+def chain_gemm(a: torch.Tensor, b: torch.Tensor, M: int, N: int, K: int, out: torch.Tensor, flavour: int = 0,
+               q: int = GEMM_Q, xsq: torch.Tensor | None = None, ysq: torch.Tensor | None = None) -> None:
+    """out = the reference's sgemm (flavour 0) / portable_matmul (1) bits of a[:, :K] . b[:, :K]^T,
+    or (with xsq / ysq) the clamped squared distances of distance.expand_to_sq_l2."""
+    p = native.ChainParams()
+    p.a, p.lda, p.b, p.ldb = a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0)
+    p.M, p.N, p.K, p.flavour, p.q = M, N, K, flavour, q
+    p.mode = 1 if xsq is not None else 0
+    p.out, p.ldo = out.data_ptr(), out.stride(0)
+    if xsq is not None:
+        p.xsq, p.ysq = xsq.data_ptr(), ysq.data_ptr()
+    native.call("skm_chain_gemm", C.byref(p), stream_handle(), flops=2.0 * M * N * K,
+                tag="chain_dist" if xsq is not None else "chain_gemm")
 
 
 def _i64(t: torch.Tensor) -> int:
@@ -213,14 +271,15 @@ class Centroids:
         self.lo = torch.empty_like(c)
         self.ysq = torch.empty(self.k, dtype=torch.float32, device=c.device)
         self.tails = None
-        self.tails_blk = None
         self.ysq_ext = None
+        self.ysq_max = torch.zeros(1, dtype=torch.float32, device=c.device)  # max_j ysq (error bounds)
 
     def refresh(self, dims: int, d_prime: int | None):
         """Recompute split + norms over `dims` (+ tails at d_prime) after an update."""
         native.call("skm_split_hilo", ptr(self.c), self.ld, self.k, self.d, ptr(self.hi), ptr(self.lo), self.ld,
                     stream_handle())
         native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, dims, ptr(self.ysq), stream_handle())
+        native.call("skm_max_f32", ptr(self.ysq), self.k, ptr(self.ysq_max), stream_handle())
         if d_prime is not None:
             if self.ysq_ext is None:
                 self.ysq_ext = torch.empty(self.k, dtype=torch.float32, device=self.c.device)
@@ -232,11 +291,6 @@ class Centroids:
                 self.tails = torch.empty(need, dtype=torch.float32, device=self.c.device)
             native.call("skm_build_tails", ptr(self.c), self.ld, self.k, self.d, d_prime, ptr(self.tails),
                         stream_handle())
-            if TWO_PHASE_SCAN:
-                if self.tails_blk is None or self.tails_blk.numel() < need:
-                    self.tails_blk = torch.empty(need, dtype=torch.float32, device=self.c.device)
-                native.call("skm_build_tails_blk", ptr(self.c), self.ld, self.k, self.d, d_prime,
-                            ptr(self.tails_blk), stream_handle())
 
 
 def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
@@ -245,6 +299,9 @@ def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
     p.b_hi, p.b_lo, p.ldb = b_hi.data_ptr(), b_lo.data_ptr(), b_hi.stride(0)
     p.M, p.N, p.K, p.mode = M, N, K, mode
     p.n_split = kw.pop("n_split", 1)
+    top = kw.pop("top", None)
+    if top is not None:
+        p.top = top.data_ptr()
     out = kw.pop("out", None)
     if out is not None:
         p.out, p.ldo = out.data_ptr(), out.stride(0)
@@ -312,17 +369,16 @@ class Workspace:
         self.prev = torch.zeros(nn, dtype=i32, device=dev)
         self.tau = torch.full((nn,), float("inf"), dtype=f32, device=dev)
         self.thr = torch.empty(nn, dtype=f32, device=dev)
-        self.keys = None
+        self.top = None
+        self.amb_rows = torch.empty(nn, dtype=i32, device=dev)
+        self.amb_count = torch.zeros(1, dtype=i32, device=dev)
+        self.chain_flavour, self.chain_q = chain_policy(cfg.gemm_backend)
         self.cand = torch.empty((b, self.cap, 2), dtype=i32, device=dev)  # {index, float bits} records
         self.cand_cnt = torch.empty(b, dtype=i32, device=dev)
         self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
         self.work = torch.zeros(256, dtype=torch.int32, device=dev)  # per-SM scan row queues
         # scan diagnostics: spec blocks, spec waves, exact blocks, exact waves, rows routed to the exact phase
         self.diag = torch.zeros(8, dtype=torch.int64, device=dev)
-        self.scan_scratch = None
-        if TWO_PHASE_SCAN:
-            nbytes = int(native.load().skm_scan2_scratch_bytes(self.batch, self.cap))
-            self.scan_scratch = torch.empty((nbytes + 3) // 4, dtype=torch.int32, device=dev)
         self.bx = torch.empty(b, dtype=f32, device=dev)
         self.bthr = torch.empty(b, dtype=f32, device=dev)
         self.thr1 = torch.empty(nn, dtype=f32, device=dev)
@@ -345,33 +401,66 @@ class Workspace:
                            torch.empty((self.batch, fld), dtype=torch.float32, device=self.dev))
         return self._front[0][:, :fld], self._front[1][:, :fld]
 
-    def argmin_keys(self, n):
-        if self.keys is None or self.keys.numel() < n:
-            self.keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
-        return self.keys
+    def top_records(self, n):
+        """ARGMIN top-2 records, int4 per (N split, row)."""
+        if self.top is None or self.top.numel() < 4 * n:
+            self.top = torch.empty(4 * max(n, 1), dtype=torch.int32, device=self.dev)
+        return self.top
 
 
 # ------------------------------------------------------------------------------ passes
 def full_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, row0: int = 0, rows: int | None = None):
-    """Exact argmin over all centroids (lowest index on ties) -> ws.assign / ws.tau."""
+    """Exact argmin over all centroids (lowest index on ties) -> ws.assign / ws.tau, bitwise the
+    reference's batched sgemm + expansion + argmin (core.py:169-192).
+
+    The tensor-core ARGMIN GEMM keeps each row's best and runner-up distances; its argmin is the
+    reference's whenever the runner-up is outside the rigorous error bound of both values (the
+    common case).  tau is then recomputed as the reference's own chain distance of that pair, and
+    the few rows with a runner-up inside the bound get the whole distance row from the chain GEMM
+    (the reference's exact bits, ties to the lowest index)."""
     n = data.n if rows is None else rows
     if n == 0:
         return
-    d = data.d
-    xsq = data.norms(d)
-    split = _l2_split(n, cents.k, d, 4)
-    a_hi = data.hi[row0:row0 + n]
-    a_lo = data.lo[row0:row0 + n]
-    if split == 1:
-        _gemm(a_hi, a_lo, cents.hi, cents.lo, n, cents.k, d, native.GEMM_ARGMIN, xsq=xsq[row0:row0 + n],
-              ysq=cents.ysq, assign=ws.assign[row0:row0 + n], tau=ws.tau[row0:row0 + n])
-    else:
-        keys = ws.argmin_keys(n)
-        native.call("skm_fill_u64", ptr(keys), n, C.c_ulonglong(_U64_MAX), stream_handle())
-        _gemm(a_hi, a_lo, cents.hi, cents.lo, n, cents.k, d, native.GEMM_ARGMIN, xsq=xsq[row0:row0 + n],
-              ysq=cents.ysq, keys=keys, n_split=split)
-        native.call("skm_decode_argmin_keys", ptr(keys), n, ptr(ws.assign[row0:row0 + n]),
-                    ptr(ws.tau[row0:row0 + n]), stream_handle())
+    d, k = data.d, cents.k
+    st = stream_handle()
+    xsq = data.norms(d)[row0:row0 + n]
+    n_tiles = (k + 255) // 256  # ARGMIN tile width 256
+    split = max(1, min(_l2_split(n, k, d, 4), n_tiles))
+    split = -(-n_tiles // -(-n_tiles // split))  # the launcher's effective split (whole tile ranges)
+    top = ws.top_records(split * n)
+    _gemm(data.hi[row0:row0 + n], data.lo[row0:row0 + n], cents.hi, cents.lo, n, k, d, native.GEMM_ARGMIN,
+          xsq=xsq, ysq=cents.ysq, top=top, n_split=split)
+    assign, tau = ws.assign[row0:row0 + n], ws.tau[row0:row0 + n]
+    ws.amb_count.zero_()
+    native.call("skm_argmin_merge", ptr(top), split, n, ptr(xsq), ptr(cents.ysq_max), float(tc_kappa(d)),
+                ptr(assign), ptr(tau), ptr(ws.amb_rows), ptr(ws.amb_count), st)
+    native.call("skm_exact_pair_dist", ptr(data.x[row0:row0 + n]), data.ld, ptr(cents.c), cents.ld, ptr(assign), n,
+                d, ptr(xsq), ptr(cents.ysq), ws.chain_flavour, ws.chain_q, ptr(tau), st, nbytes=4.0 * n * d)
+    n_amb = int(ws.amb_count.item())
+    if n_amb:
+        exact_rows_argmin(data, cents, ws, ws.amb_rows[:n_amb], row0, xsq)
+
+
+def exact_rows_argmin(data: DeviceData, cents: Centroids, ws: Workspace, rows_local: torch.Tensor, row0: int,
+                      xsq: torch.Tensor) -> None:
+    """Full chain-GEMM distance rows (the reference's bits) + exact argmin for the given rows
+    (indices relative to row0)."""
+    dev = data.x.device
+    st = stream_handle()
+    d, k = data.d, cents.k
+    m = int(rows_local.numel())
+    chunk = max(1, min(m, (1 << 28) // max(k, 1)))  # <= 1 GiB of distances per chunk
+    for c0 in range(0, m, chunk):
+        cn = min(chunk, m - c0)
+        ids = rows_local[c0:c0 + cn]
+        glob = (ids + row0).contiguous()
+        xa = torch.empty((cn, data.ld), dtype=torch.float32, device=dev)
+        native.call("skm_gather_rows_i32", ptr(data.x), data.ld, ptr(glob), cn, data.ld, ptr(xa), data.ld, st)
+        xs = xsq[ids.to(torch.int64)].contiguous()
+        dense = torch.empty((cn, padded_ld(k)), dtype=torch.float32, device=dev)
+        chain_gemm(xa, cents.c, cn, k, d, dense, ws.chain_flavour, ws.chain_q, xsq=xs, ysq=cents.ysq)
+        native.call("skm_dense_argmin", ptr(dense), dense.stride(0), cn, k, ptr(ids), ptr(ws.assign[row0:]),
+                    ptr(ws.tau[row0:]), st)
 
 
 class PrunePlan:
@@ -412,15 +501,18 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
     elif seed_tau:
         native.call("skm_seed_thresholds", ptr(x_rows), data.ld, ptr(cents.c), cents.ld, ptr(assign), n, d,
                     ptr(tau), st, nbytes=4.0 * n * d + 8.0 * n)
-    native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
-                ptr(ws.thr[row0:row0 + n]), st)
-    # certification (exact scan only; the speculative scan does not decode the flag)
-    ext = CERT_EXT if (not TWO_PHASE_SCAN and not plan.sentinel and dp % 4 == 0 and dp + CERT_EXT <= d
-                       and plan.widths[0] == 64) else 0
-    if ext:
-        native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(ws.thr1[row0:row0 + n]), st)
-        xsq_ext = data.norms(dp + ext)
     xsq = data.norms(dp)
+    kap = tc_kappa(dp)
+    # emission threshold of the tensor-core gate: a superset of the candidates whose exact
+    # (chain) distance may pass fl(tau F0); the scan settles every decision exactly
+    native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
+                ptr(ws.thr[row0:row0 + n]), ptr(xsq[row0:row0 + n]), ptr(cents.ysq_max), float(kap), st)
+    ext = CERT_EXT if (not plan.sentinel and dp % 4 == 0 and dp + CERT_EXT <= d and plan.widths[0] == 64) else 0
+    if ext:
+        native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(ws.thr1[row0:row0 + n]),
+                    None, None, 0.0, st)
+        xsq_ext = data.norms(dp + ext)
+        ceps = cert_eps(dp + ext)
     k = cents.k
     ordered = order is not None and row0 == 0 and n == data.n
     if ordered:
@@ -439,14 +531,14 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
                         ptr(ws.bx_ext) if ext else None, ptr(ws.bthr1) if ext else None, st,
                         nbytes=16.0 * bn * (dp + ext) + 24.0 * bn)
             cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=cents.ysq_ext, thr1=ws.bthr1[:bn],
-                        cert_eps=CERT_EPS) if ext else {}
+                        cert_eps=ceps) if ext else {}
             _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
                   ysq=cents.ysq, thr=ws.bthr[:bn], cand=ws.cand, cand_cnt=ws.cand_cnt,
                   cand_cap=ws.cap, **cert)
             sp.row_map = rmap.data_ptr()
         else:
             cert = dict(ext_k=ext, xsq_ext=xsq_ext[r:r + bn], ysq_ext=cents.ysq_ext, thr1=ws.thr1[r:r + bn],
-                        cert_eps=CERT_EPS) if ext else {}
+                        cert_eps=ceps) if ext else {}
             _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE,
                   xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand=ws.cand,
                   cand_cnt=ws.cand_cnt, cand_cap=ws.cap, **cert)
@@ -460,12 +552,8 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         sp.counters_ext = ws.diag.data_ptr()
         if PRUNE_HIST is not None:
             sp.prune_hist = PRUNE_HIST.data_ptr()
-        if TWO_PHASE_SCAN:
-            native.call("skm_pruned_scan2", C.byref(sp), ptr(cents.tails_blk), ptr(ws.scan_scratch),
-                        ws.scan_scratch.numel() * 4, st, tag="pruned_scan",
-                        nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
-        else:
-            native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        _scan_exact_args(sp, data, cents, ws, xsq, kap)
+        native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
         if ws.cap < k:
             # rows whose candidate list overflowed the slab: dense distance rows, same kernel
             over = torch.nonzero(ws.cand_cnt[:bn] > ws.cap).flatten()
@@ -506,7 +594,16 @@ def _dense_overflow(data, cents, ws, plan, glob_rows, n_over, xsq):
         sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
         sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
         sp.dense_mode = 1
+        _scan_exact_args(sp, data, cents, ws, xsq, tc_kappa(plan.d_prime))
         native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan_dense", nbytes=4.0 * cn * k)
+
+
+def _scan_exact_args(sp, data: DeviceData, cents: Centroids, ws: Workspace, xsq: torch.Tensor, kap: float) -> None:
+    """Interval decisions on tensor-core distances + the exact chain for the unsettled ones."""
+    sp.kap = kap
+    sp.xsq, sp.ysq, sp.ysq_max = xsq.data_ptr(), cents.ysq.data_ptr(), cents.ysq_max.data_ptr()
+    sp.cent, sp.ldc = cents.c.data_ptr(), cents.ld
+    sp.chain_flavour, sp.chain_q = ws.chain_flavour, ws.chain_q
 
 
 def update_centroids_device(data: DeviceData, cents: Centroids, ws: Workspace, comm: Comm,

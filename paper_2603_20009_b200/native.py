@@ -36,12 +36,22 @@ class GemmParams(C.Structure):
         ("mode", _i), ("n_split", _i),
         ("out", _vp), ("ldo", _ll),
         ("xsq", _vp), ("ysq", _vp),
-        ("assign", _vp), ("tau", _vp),
-        ("keys", _vp),
+        ("top", _vp),
         ("thr", _vp),
         ("cand", _vp), ("cand_cnt", _vp), ("cand_cap", _i),
         ("row_offset", _ll),
         ("ext_k", _i), ("xsq_ext", _vp), ("ysq_ext", _vp), ("thr1", _vp), ("cert_eps", _f),
+    ]
+
+
+class ChainParams(C.Structure):
+    _fields_ = [
+        ("a", _vp), ("lda", _ll),
+        ("b", _vp), ("ldb", _ll),
+        ("M", _i), ("N", _i), ("K", _i),
+        ("flavour", _i), ("q", _i), ("mode", _i),
+        ("out", _vp), ("ldo", _ll),
+        ("xsq", _vp), ("ysq", _vp),
     ]
 
 
@@ -59,6 +69,8 @@ class ScanParams(C.Structure):
         ("dense_mode", _i),
         ("counters_ext", _vp),
         ("prune_hist", _vp),
+        ("kap", _f), ("xsq", _vp), ("ysq", _vp), ("ysq_max", _vp),
+        ("cent", _vp), ("ldc", _ll), ("chain_flavour", _i), ("chain_q", _i),
     ]
 
 
@@ -79,8 +91,11 @@ _SIGS = {
     "skm_accumulate_centroid_sums": ([_vp, _ll, _vp, _i, _i, _i, _vp, _vp, _vp, _ll, _vp], _i),
     "skm_portable_matmul": ([_vp, _ll, _vp, _ll, _i, _i, _i, _vp, _ll, _vp], _i),
     "skm_gemm_tf32x3": ([C.POINTER(GemmParams), _vp], _i),
-    "skm_decode_argmin_keys": ([_vp, _i, _vp, _vp, _vp], _i),
-    "skm_fill_u64": ([_vp, _ll, C.c_ulonglong, _vp], _i),
+    "skm_argmin_merge": ([_vp, _i, _i, _vp, _vp, _f, _vp, _vp, _vp, _vp, _vp], _i),
+    "skm_dense_argmin": ([_vp, _ll, _i, _i, _vp, _vp, _vp, _vp], _i),
+    "skm_exact_pair_dist": ([_vp, _ll, _vp, _ll, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _vp], _i),
+    "skm_max_f32": ([_vp, _i, _vp, _vp], _i),
+    "skm_chain_gemm": ([C.POINTER(ChainParams), _vp], _i),
     "skm_cluster_sort": ([_vp, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp], _i),
     "skm_cluster_sums": ([_vp, _ll, _vp, _vp, _vp, _i, _i, _vp, _i, _vp, _ll, _i, _vp], _i),
     "skm_finalize_centroids": ([_vp, _vp, _i, _i, _vp, _ll, _vp], _i),
@@ -89,7 +104,7 @@ _SIGS = {
     "skm_stats_workspace_bytes": ([_i], _ll),
     "skm_assign_stats": ([_vp, _vp, _vp, _i, _vp, _vp, _vp, _ll, _vp], _i),
     "skm_build_tails": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
-    "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp], _i),
+    "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp, _vp, _f, _vp], _i),
     "skm_pruned_scan": ([C.POINTER(ScanParams), _vp], _i),
     "skm_first_nonfinite": ([_vp, _ll, _ll, _i, _vp, _vp], _i),
     "skm_wcss_workspace_bytes": ([], _ll),
@@ -97,9 +112,6 @@ _SIGS = {
     "skm_ingest_records": ([_vp, _ll, _i, _i, _i, _ll, _vp, _ll, _vp, _vp, _vp], _i),
     "skm_gather_front": ([_vp, _vp, _ll, _vp, _i, _i, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
                          _i),
-    "skm_build_tails_blk": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
-    "skm_scan2_scratch_bytes": ([_i, _i], _ll),
-    "skm_pruned_scan2": ([C.POINTER(ScanParams), _vp, _vp, _ll, _vp], _i),
     "skm_topk_rows": ([_vp, _ll, _i, _i, _i, _vp, _vp, _ll, _i, _vp], _i),
     "skm_topk_merge": ([_vp, _vp, _i, _i, _i, _vp, _vp, _vp], _i),
     "skm_etr_hits": ([_vp, _i, _i, _vp, _i, _i, _vp, _ll, _ll, _i, _i, _vp, _vp], _i),

@@ -91,20 +91,29 @@ def test_gemm_dist_argmin_gate_consistent():
     M, N = 3000, 300
     D = torch.empty((M, dev.padded_ld(N)), dtype=torch.float32, device="cuda")
     dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_DIST, out=D, xsq=xs, ysq=cs)
-    a = torch.empty(M, dtype=torch.int32, device="cuda")
-    t = torch.empty(M, dtype=torch.float32, device="cuda")
-    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_ARGMIN, xsq=xs, ysq=cs, assign=a, tau=t)
     Dn = D[:, :N].cpu().numpy()
-    assert np.array_equal(a.cpu().numpy(), np.argmin(Dn, axis=1))
-    assert np.array_equal(t.cpu().numpy(), Dn.min(axis=1))
-    # multi-CTA split along N goes through packed atomicMin keys
-    keys = torch.full((M,), -1, dtype=torch.int64, device="cuda")
-    dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_ARGMIN, xsq=xs, ysq=cs, keys=keys, n_split=2)
-    a2 = torch.empty_like(a)
-    t2 = torch.empty_like(t)
-    native.call("skm_decode_argmin_keys", dev.ptr(keys), M, dev.ptr(a2), dev.ptr(t2), dev.stream_handle())
-    assert np.array_equal(a2.cpu().numpy(), a.cpu().numpy())
-    assert np.array_equal(t2.cpu().numpy(), t.cpu().numpy())
+    srt = np.sort(Dn, axis=1)
+    for split in (1, 2):  # top-2 records per N split, merged on the device
+        top = torch.empty(4 * M * split, dtype=torch.int32, device="cuda")
+        dev.gemm(xh, xl, ch, cl, M, N, K, native.GEMM_ARGMIN, xsq=xs, ysq=cs, top=top, n_split=split)
+        a = torch.empty(M, dtype=torch.int32, device="cuda")
+        t = torch.empty(M, dtype=torch.float32, device="cuda")
+        amb = torch.empty(M, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ymax = torch.tensor([float(cs.max().item())], device="cuda")
+        native.call("skm_argmin_merge", dev.ptr(top), split, M, dev.ptr(xs), dev.ptr(ymax), 0.0, dev.ptr(a),
+                    dev.ptr(t), dev.ptr(amb), dev.ptr(cnt), dev.stream_handle())
+        assert np.array_equal(a.cpu().numpy(), np.argmin(Dn, axis=1))
+        assert np.array_equal(t.cpu().numpy(), Dn.min(axis=1))
+        rec = top.view(split, M, 4).cpu().numpy()
+        second = rec[..., 2].view(np.float32).min(axis=0)
+        best = rec[..., 0].view(np.float32)
+        # the global runner-up is the smaller of the splits' seconds and the losing splits' bests
+        run_up = np.sort(np.concatenate([best, rec[..., 2].view(np.float32)], axis=0), axis=0)[1]
+        assert np.array_equal(run_up, srt[:, 1])
+        # kap = 0: a row is flagged only on an exact tie of the two smallest values
+        assert int(cnt.item()) == int(np.count_nonzero(srt[:, 1] == srt[:, 0]))
+        del second
     # gate
     thr = torch.tensor(np.quantile(Dn, 0.05, axis=1).astype(np.float32), device="cuda")
     cap = 64
@@ -206,19 +215,23 @@ SCAN_CASES = [
 
 
 @pytest.mark.parametrize("seed,n,k,d,dp,sentinel", SCAN_CASES)
-@pytest.mark.parametrize("two_phase,prev_mode,cert", [(False, "random", False), (True, "random", False),
-                                                      (True, "nearest", False), (True, "mixed", False),
-                                                      (False, "nearest", True), (False, "mixed", True),
-                                                      (False, "dup", False), (False, "dup", True)])
-def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, prev_mode, cert):
+@pytest.mark.parametrize("exact,prev_mode,cert", [(False, "random", False), (True, "random", False),
+                                                  (True, "nearest", False), (True, "mixed", False),
+                                                  (True, "nearest", True), (False, "mixed", True),
+                                                  (True, "mixed", True), (True, "dup", False),
+                                                  (True, "dup", True)])
+def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_mode, cert):
     """Production scan equals the sequential reference scan over all centroids, including the
-    survivor/dims counters: the one-phase exact kernel (candidate lists + speculative waves +
-    in-order resolve) and the two-phase scan (speculative pair scan for rows whose tau can only
-    change at their previous centroid + exact kernel on the rest).  ``prev_mode`` picks the
-    previous assignment: random (most rows re-assign), the nearest centroid (steady state: the
-    speculative phase owns almost every row) or 90% nearest.  ``cert``: the gate GEMM also
-    certifies tail-block-0 prunes (ext_k = 64) and the exact scan skips walking them.  ``dup``:
-    the second half of the centroids duplicates the first (exact distance ties everywhere)."""
+    survivor/dims counters.  ``exact``: the oracle scans the reference's own partial distances
+    (the exact fma chain of OpenBLAS sgemm, computed here by the device chain GEMM) while the
+    device gates on 3xTF32 tensor-core distances and settles every decision on their rigorous
+    error interval, recomputing the chain where the interval cannot decide -- the production
+    configuration; otherwise both sides see the tensor-core values (kap = 0).  ``prev_mode``
+    picks the previous assignment: random (most rows re-assign), the nearest centroid (steady
+    state) or 90% nearest.  ``cert``: the gate GEMM also certifies tail-block-0 prunes (ext_k =
+    64) and the scan skips walking them.  ``dup``: the second half of the centroids duplicates
+    the first (exact distance ties everywhere)."""
+    from paper_2603_20009_b200.engine import cert_eps, chain_gemm, tc_kappa
     from oracle import kernels_np as O
     from paper_2603_20009_b200 import native
     from paper_2603_20009_b200.config import pdxify, tail_block_layout
@@ -244,7 +257,16 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     cs = dev.row_sq_norms(Cm, dp)
     D = torch.empty((n, dev.padded_ld(k)), dtype=torch.float32, device="cuda")
     dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_DIST, out=D, xsq=xs, ysq=cs)
-    vals = np.ascontiguousarray(D[:, :k].cpu().numpy())
+    if exact:  # the reference's bits: sgemm's fma chain + expansion
+        DE = torch.empty_like(D)
+        chain_gemm(X, Cm, n, k, dp, DE, 0, 448, xsq=xs, ysq=cs)
+        vals = np.ascontiguousarray(DE[:, :k].cpu().numpy())
+        tc = D[:, :k].cpu().numpy()
+        print("tensor-core vs chain distances: %d of %d differ" % (np.count_nonzero(tc != vals), tc.size))
+    else:
+        vals = np.ascontiguousarray(D[:, :k].cpu().numpy())
+    kap = tc_kappa(dp) if exact else 0.0
+    ymax = torch.tensor([float(cs.max().item())], device="cuda")
     widths, bounds = tail_block_layout(d, dp)
     f = threshold_factors(d, dp, bounds, 2.1)
     fs = sentinel_factors(f) if sentinel else f
@@ -268,7 +290,8 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     if sentinel:
         tau.fill_(float("inf"))
     thr = torch.empty(n, dtype=torch.float32, device="cuda")
-    native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[0]), int(sentinel), dev.ptr(thr), dev.stream_handle())
+    native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[0]), int(sentinel), dev.ptr(thr), dev.ptr(xs),
+                dev.ptr(ymax), float(kap), dev.stream_handle())
     cap = 128
     rec = torch.empty((n, cap, 2), dtype=torch.int32, device="cuda")  # {index, float bits}
     ci = rec[..., 0]
@@ -280,9 +303,10 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     kw = {}
     if ext:
         thr1 = torch.empty(n, dtype=torch.float32, device="cuda")
-        native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[1]), 0, dev.ptr(thr1), dev.stream_handle())
+        native.call("skm_gate_threshold", dev.ptr(tau), n, float(fs[1]), 0, dev.ptr(thr1), None, None, 0.0,
+                    dev.stream_handle())
         kw = dict(ext_k=ext, xsq_ext=dev.row_sq_norms(X, dp + ext), ysq_ext=dev.row_sq_norms(Cm, dp + ext), thr1=thr1,
-                  cert_eps=3e-5)
+                  cert_eps=cert_eps(dp + ext))
     dev.gemm(xh, xl, ch, cl, n, k, dp, native.GEMM_GATE, xsq=xs, ysq=cs, thr=thr, cand=rec,
              cand_cnt=cc, cand_cap=cap, **kw)
     if ext:
@@ -308,23 +332,13 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
     p.tau, p.assign, p.counters = tau.data_ptr(), assign.data_ptr(), counters.data_ptr()
     work = torch.zeros(256, dtype=torch.int32, device="cuda")
     p.work = work.data_ptr()
+    diag = torch.zeros(8, dtype=torch.int64, device="cuda")
+    p.counters_ext = diag.data_ptr()
+    p.kap = kap
+    p.xsq, p.ysq, p.ysq_max = xs.data_ptr(), cs.data_ptr(), ymax.data_ptr()
+    p.cent, p.ldc, p.chain_flavour, p.chain_q = Cm.data_ptr(), Cm.stride(0), 0, 448
     import ctypes
-    if two_phase:
-        tails_blk = torch.empty(k * 64 * nb, dtype=torch.float32, device="cuda")
-        native.call("skm_build_tails_blk", dev.ptr(Cm), Cm.stride(0), k, d, dp, dev.ptr(tails_blk),
-                    dev.stream_handle())
-        nbytes = int(native.load().skm_scan2_scratch_bytes(n, cap))
-        scratch = torch.empty((nbytes + 3) // 4, dtype=torch.int32, device="cuda")
-        diag = torch.zeros(8, dtype=torch.int64, device="cuda")
-        p.counters_ext = diag.data_ptr()
-        native.check(native.load().skm_pruned_scan2(ctypes.byref(p), dev.ptr(tails_blk), dev.ptr(scratch), nbytes,
-                                                    dev.stream_handle()), "scan2")
-        p.counters_ext = None
-        if prev_mode == "nearest" and not sentinel:
-            # steady state: round 0 of the speculative scan finishes most rows itself
-            assert int(diag[5].item()) < n // 2
-    else:
-        native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
+    native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
     # overflow rows -> dense pass over their full distance rows
     over = torch.nonzero(cc > cap).flatten().to(torch.int32)
     if over.numel():
@@ -336,6 +350,8 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, two_phase, p
         p2.dense_row = ident.data_ptr()
         native.check(native.load().skm_pruned_scan(ctypes.byref(p2), dev.stream_handle()), "scan dense")
     torch.cuda.synchronize()
+    if exact:
+        print("candidates re-evaluated with the exact chain:", int(diag[3].item()))
     sv, td, ch_ = counters.cpu().tolist()
     assert np.array_equal(assign.cpu().numpy(), a_o)
     assert np.array_equal(tau.cpu().numpy(), tau_o)

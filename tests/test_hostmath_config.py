@@ -139,3 +139,11 @@ def test_sub_seed_and_reconcile():
     from paper_2603_20009_b200.hierarchical import _fine_k, reconcile_k
     assert _fine_k(1) == 1 and _fine_k(100) == 10 and _fine_k(42) == round(np.sqrt(42))
     assert reconcile_k(238, 120) == {"requested_k": 120, "achieved_k": 238}
+
+
+def test_chunked_generators_bitwise_reference_generators():
+    """synth.py (row-chunked) == the reference's one-shot generators (conftest restatement)."""
+    from conftest import make_blobs as mb, make_skewed_blobs as msb
+    from paper_2603_20009_b200 import synth
+    assert np.array_equal(synth.make_blobs(5000, 37, 11, 3, chunk_rows=777), mb(5000, 37, 11, 3))
+    assert np.array_equal(synth.make_skewed_blobs(4000, 96, 64, 0, chunk_rows=1000), msb(4000, 96, 64, 0))
