@@ -2,13 +2,18 @@
 """Benchmark: SuperKMeans fit of 1M x 1536 fp32 into k=4096 for 10 fixed iterations
 (BASELINE.json configs[1]) on 1..8 B200, one process per GPU.
 
-A step = one complete fit of the north-star hot path on device-resident data: rotation GEMM
-(tcgen05 3xTF32), iteration 1 full-distance GEMM + argmin, 9 pruned iterations (fused gate GEMM
-+ exact pruning scan), ordered centroid update (+ NCCL allreduce at N>1), un-rotation.
-Rows are sharded across ranks (strong scaling: the 1M rows are fixed, split over N GPUs).
+Data: the reference's own generator, make_skewed_blobs(1_000_000, 1536, 8192, seed=0)
+(pkg/tests/conftest.py:16-20, restated bit-exactly in paper_2603_20009_b200/synth.py), i.e. the
+input of tests/golden/full_c2.npz: the timed trajectory is compared with the real reference's
+(d', survivors, n_changed, wcss) and reported in "parity".
 
-  python bench.py [--gpus N --steps K --warmup W]           # our B200 path
-  python bench.py --impl reference ...                      # reference CPU path (oracle/) on host cores
+A step = one complete fit of the north-star hot path on device-resident rows: exact-chain rotation,
+iteration 1 (tensor-core argmin + exact fix-up), 9 pruned iterations (tensor-core gate + exact
+interval scan), ordered centroid update (+ NCCL allreduce at N>1), un-rotation.  Rows are sharded
+across ranks (strong scaling: the 1M rows are fixed, split over N GPUs).
+
+  python bench.py [--gpus N --steps K --warmup W]     # our B200 path
+  python bench.py --impl reference ...                # the real reference (baseline/_ref) on host cores
 
 Prints ONE JSON line on rank 0.
 """
@@ -30,6 +35,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "kmeans fit throughput (Lloyd iterations/s incl. rotation), 1M x 1536 fp32, k=4096, 10 iterations"
 UNIT = "iter/s"
+GOLDEN_C2 = os.path.join(ROOT, "tests", "golden", "full_c2.npz")
+
+# secondary BASELINE configs measured after the headline (N=1): (generator, n, d, centres, k, iters, etr)
+EXTRA = {
+    "c1": ("blobs", 100_000, 128, 256, 256, 10, None),
+    "c3": ("skewed", 1_000_000, 1024, 32768, 16384, 25, (1000, 10)),
+    "c4_k1024": ("skewed", 1_000_000, 768, 2048, 1024, 10, None),
+    "c4_k4096": ("skewed", 1_000_000, 768, 8192, 4096, 10, None),
+    "c4_k16384": ("skewed", 1_000_000, 768, 32768, 16384, 10, None),
+}
 
 
 def parse():
@@ -46,9 +61,16 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=0,
-                    help="rows in the bounded CPU sample (default n/16: ~10-30 s of CPU work)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs (c1, c3, c4 sweep)")
+    ap.add_argument("--extra", default=",".join(EXTRA), help="secondary configs to measure at N=1")
     return ap.parse_args()
+
+
+def workload(args) -> dict:
+    return {"workload": f"c2: make_skewed_blobs({args.n}, {args.d}, {args.centers}, seed={args.seed}) fp32, "
+                        f"k={args.k}, {args.iters} fixed iterations (the reference's generator and fit config)",
+            "n": args.n, "d": args.d, "k": args.k, "iterations": args.iters,
+            "l2": "inputs (6 GB) exceed the 126 MB L2 between steps"}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -96,73 +118,146 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- data
-def make_shard_device(n, d, centers, lo, hi, seed, dev):
-    """Skewed-blob rows [lo, hi) generated on the GPU (same distribution as the reference's
-    make_skewed_blobs: centres ~ N(0, 1.5^2), unit noise, per-dim scale 0.995^t)."""
-    import torch
-    from paper_2603_20009_b200.device import padded_ld
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-    cen = torch.randn((centers, d), generator=g, device=dev) * 1.5
-    scale = (0.995 ** torch.arange(d, device=dev, dtype=torch.float64)).to(torch.float32)
-    ld = padded_ld(d)
-    x = torch.zeros((hi - lo, ld), dtype=torch.float32, device=dev)
-    chunk = 1 << 16
-    for s in range(lo, hi, chunk):
-        e = min(hi, s + chunk)
-        gg = torch.Generator(device=dev)
-        gg.manual_seed(seed * 1_000_003 + s)
-        which = torch.randint(0, centers, (e - s,), generator=gg, device=dev)
-        x[s - lo:e - lo, :d] = (cen[which] + torch.randn((e - s, d), generator=gg, device=dev)) * scale
-    return x
+def make_rows(gen: str, n: int, d: int, centers: int, seed: int, hi: int | None = None) -> np.ndarray:
+    """Rows [0, hi) of the reference generator's matrix (the RNG stream is sequential, so a shard
+    needs every row before it drawn; rows past hi are not generated)."""
+    from paper_2603_20009_b200 import synth
+    hi = n if hi is None else hi
+    if gen == "blobs":
+        return synth.make_blobs(n, d, centers, seed, out_rows=hi) if hi != n else synth.make_blobs(n, d, centers, seed)
+    return synth.make_skewed_blobs(n, d, centers, seed, out_rows=hi) if hi != n else \
+        synth.make_skewed_blobs(n, d, centers, seed)
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    from paper_2603_20009_b200.engine import shard_bounds
+    return shard_bounds(n, world, rank)
 
 
 # ----------------------------------------------------------------------------- reference arm
-def cpu_reference_sample(args, sample_rows, iters=10):
-    """Reference CPU path (oracle/ restatement of core.fit) on a bounded sample of the same
-    workload: returns (iterations/s scaled to the full n, seconds, description)."""
-    from oracle import skm_ref
-    rng = np.random.default_rng(args.seed)
-    centers = (rng.standard_normal((args.centers, args.d)) * 1.5).astype(np.float32)
-    which = rng.integers(0, args.centers, sample_rows)
-    x = (centers[which] + rng.standard_normal((sample_rows, args.d)).astype(np.float32))
-    x *= (0.995 ** np.arange(args.d)).astype(np.float32)
-    k = min(args.k, sample_rows // 2)
-    t0 = time.perf_counter()
-    skm_ref.fit(x, skm_ref.Params(k=k, max_iters=iters, seed=args.seed), inspect=False)
-    dt = time.perf_counter() - t0
-    # per-iteration cost is linear in rows x centroids for this loop
-    per_iter_full = (dt / iters) * (args.n / sample_rows) * (args.k / k)
-    desc = (f"oracle/skm_ref fit of {sample_rows} skewed-blob rows x {args.d}, k={k}, {iters} iterations "
-            f"({dt:.1f}s); iteration time scaled by (n/rows)*(k_full/k) to {args.n}x{args.d}, k={args.k}")
-    return 1.0 / per_iter_full, dt, desc
+def _reference_module():
+    """The unmodified reference package installed from /root/reference/pkg into baseline/_ref
+    (pip --target, its own setup.py builds the compiled kernels)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import superkmeans
+    from superkmeans import kernels
+    return superkmeans, bool(kernels.HAS_COMPILED)
 
 
 def run_reference(args, rank, world):
+    """The reference's own fit (compiled Cython kernels, OpenBLAS, all host cores) on the full c2
+    workload.  A step is one Lloyd iteration of its loop, timed between consecutive `inspect`
+    callbacks (rotation + iteration 1 make the first step of each fit; the last update and the
+    un-rotation are charged to the next fit's first step): fits run back to back until W + K
+    iterations are covered and the K after the warm-up are timed."""
     if rank != 0:
         return
+    try:
+        skm, compiled = _reference_module()
+    except Exception as e:  # pragma: no cover - box without the install
+        print(json.dumps({"impl": "reference", "unavailable": f"baseline/_ref not importable: {e}"}), flush=True)
+        return
     cores = os.cpu_count() or 1
-    per_step = []
-    desc = ""
-    n_warm, n_steps = args.warmup, args.steps
-    # each step is a bounded sample (n/16 rows x all iterations, ~10-15 s of CPU work on the GPU
-    # boxes' host cores), shrunk when many steps are asked for so the run stays within minutes
-    rows = args.cpu_sample or max(args.n // 64, int(args.n // 16 * min(1.0, 10.0 / max(1, n_warm + n_steps))))
-    for i in range(n_warm + n_steps):
-        v, dt, desc = cpu_reference_sample(args, rows, iters=args.iters)
-        if i >= n_warm:
-            per_step.append(v)
-    value = float(np.median(per_step))
+    x = make_rows("skewed", args.n, args.d, args.centers, args.seed)
+    cfg = skm.KMeansConfig(k=args.k, max_iters=args.iters, seed=args.seed)
+    need = args.warmup + args.steps
+    stamps = [time.perf_counter()]
+    traj = []
+    while len(stamps) - 1 < need:
+        res = skm.fit(x, cfg, inspect=lambda it, ctx: stamps.append(time.perf_counter()))
+        traj = [s.d_prime for s in res.stats]
+    steps_s = np.diff(np.array(stamps))[args.warmup:need]
+    total = float(steps_s.sum())
+    value = args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": n_steps, "warmup": n_warm, "ms_per_step": 1e3 * args.iters / value,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"c2: {args.n}x{args.d} fp32 skewed blobs, k={args.k}, {args.iters} fixed iterations",
-                   "sample": f"bounded CPU sample per step: {desc}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "config": workload(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"the reference's fit on the full workload, {args.steps} timed Lloyd iterations "
+                                   f"after {args.warmup} warm-up iterations (compiled kernels: {compiled})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference": {"package": "baseline/_ref/superkmeans (unmodified, pip --target from /root/reference/pkg)",
+                      "step_seconds": [round(float(v), 3) for v in steps_s], "d_prime": traj},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(args, x: np.ndarray) -> dict | None:
+    """Bounded sample of the reference on this box's host cores: its fit with max_iters=1 on the full
+    c2 rows (rotation + iteration 1, the full-distance pass), ~10-30 s.  The pruned iterations are
+    timed by the --impl reference arm (all 10 iterations, same data)."""
+    try:
+        skm, compiled = _reference_module()
+    except Exception:
+        return None
+    cfg = skm.KMeansConfig(k=args.k, max_iters=1, seed=args.seed)
+    t0 = time.perf_counter()
+    skm.fit(x, cfg)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"reference fit (baseline/_ref, compiled kernels: {compiled}) with max_iters=1 on the full "
+                      f"{args.n}x{args.d} rows: rotation + the iteration-1 full-distance pass, {dt:.1f} s; the "
+                      f"--impl reference arm times all iterations"}
+
+
+# ----------------------------------------------------------------------------- roofline
+def roofline(prof, steps: int, args, stats, n_local: int) -> dict:
+    from paper_2603_20009_b200 import profiling
+    agg = prof.summary()
+    pk = profiling.peaks()
+    total_ms = sum(v["ms"] for v in agg.values())
+    tf32 = pk["bf16_tflops"] / 2.0
+    fp32 = profiling.fp32_peak()
+    l2 = profiling.l2_peak()
+    pruned = [s for s in stats if s.d_prime is not None]
+    n, d, k = args.n, args.d, args.k
+    # SURVEY 8(d): algorithmic HBM bytes of a pruned iteration (one X read: seed tau needs all d dims,
+    # the tail scan the same rows; assign/tau read+write; the centroids)
+    hbm_bytes = steps * sum(4.0 * n * d + 16.0 * n + 4.0 * k * d for _ in pruned) * n_local / n
+    # bytes the scan reads from L2/L1: x tails + 4 B per touched (row, centroid, dim)
+    l2_bytes = steps * sum(4.0 * n * (d - s.d_prime) + 4.0 * s.tail_dims_touched for s in pruned) * n_local / n
+    kernels = {}
+    for name, v in sorted(agg.items(), key=lambda kv: -kv[1]["ms"])[:10]:
+        e = {"ms_per_step": round(v["ms"] / steps, 3), "share": round(v["ms"] / total_ms, 4),
+             "launches_per_step": v["launches"] / steps}
+        sec = v["ms"] * 1e-3
+        if name.startswith("gemm_"):  # 3xTF32: 3 TF32 MMAs per fp32-accurate product
+            ex = 3.0 * v["flops"] / sec / 1e12
+            e.update(bound="tensor", achieved=round(ex, 1), peak=tf32, unit="TFLOP/s", frac=round(ex / tf32, 3))
+        elif name.startswith("chain_"):
+            a = v["flops"] / sec / 1e12
+            e.update(bound="fp32 (CUDA-core fma chain)", achieved=round(a, 1), peak=fp32, unit="TFLOP/s",
+                     frac=round(a / fp32, 3))
+        elif v["bytes"] > 0 and name != "pruned_scan":
+            a = v["bytes"] / sec / 1e9
+            e.update(bound="hbm", achieved=round(a, 1), peak=pk["hbm_gbs"], unit="GB/s", frac=round(a / pk["hbm_gbs"], 3))
+        kernels[name] = e
+    scan = agg.get("pruned_scan")
+    out = {"kernels": kernels, "peak_source": pk["source"]}
+    if scan:
+        sec = scan["ms"] * 1e-3
+        per_launch_ms = scan["ms"] / scan["launches"]
+        a_hbm = hbm_bytes / sec / 1e9
+        a_l2 = l2_bytes / sec / 1e9
+        out.update({
+            "kernel": "pruned_scan", "share_of_kernel_time": round(scan["ms"] / total_ms, 4),
+            "launches": scan["launches"], "avg_launch_ms": round(per_launch_ms, 4),
+            "bound": "hbm", "achieved": round(a_hbm, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(a_hbm / pk["hbm_gbs"], 4),
+            "traffic": profiling.traffic_per_launch("pruned_scan", n_local * len(pruned) * steps / scan["launches"]),
+            "algorithmic_bytes_per_launch": hbm_bytes / scan["launches"],
+            "l2": {"bytes_per_launch": l2_bytes / scan["launches"], "achieved": round(a_l2, 1), "peak": l2["gbs"],
+                   "unit": "GB/s", "frac": round(a_l2 / l2["gbs"], 4), "peak_source": l2["source"]},
+            "limiter": "not HBM: the scan reads the L2-resident centroid tails row by row (LSU / L1 wavefronts "
+                       "and the sequential-tau bookkeeping; ncu in profiles/)",
+            "note": "achieved = SURVEY 8(d) algorithmic HBM bytes of the pruned iterations (4Nd + 16N + 4kd each) / "
+                    "scan time; l2 = x tails + 4 B per touched (row, centroid, dim) from the exact counter",
+        })
+    return out
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -187,17 +282,19 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    from paper_2603_20009_b200 import api, native
-    from paper_2603_20009_b200.config import KMeansConfig
+    from paper_2603_20009_b200 import api, native, profiling
+    from paper_2603_20009_b200.config import EtrConfig, KMeansConfig
+    from paper_2603_20009_b200.device import to_device_matrix
     from paper_2603_20009_b200.engine import Comm
-    from paper_2603_20009_b200 import profiling
     from paper_2603_20009_b200.hostmath import generate_rotation
 
     native.load()
     comm = Comm()
-    per = (args.n + world - 1) // world
-    lo, hi = min(args.n, rank * per), min(args.n, (rank + 1) * per)
-    x = make_shard_device(args.n, args.d, args.centers, lo, hi, args.seed, dev)
+    lo, hi = shard_range(args.n, world, rank)
+    t_gen = time.perf_counter()
+    x_host = make_rows("skewed", args.n, args.d, args.centers, args.seed, hi=hi)[lo:hi]
+    gen_s = time.perf_counter() - t_gen
+    x = to_device_matrix(x_host, device=dev)
     cfg = KMeansConfig(k=args.k, max_iters=args.iters, seed=args.seed)
     t_qr = time.perf_counter()
     rotation = generate_rotation(args.d, args.seed)
@@ -240,62 +337,118 @@ def main():
     value = iters_done / elapsed
     ms_per_step = 1e3 * elapsed / args.steps
     launches = prof.launches
-    # algorithmic bytes of the pruning scan per timed region: the x tail rows it streams from HBM
-    # plus the centroid tail values it evaluates (4 B per touched (vector, centroid, dim), from
-    # the exact dims-touched counter; these are served from the L2-resident PDX tails)
-    st_last = res.loop.stats
-    scan_bytes = args.steps * sum(4.0 * args.n * (args.d - s.d_prime) + 4.0 * s.tail_dims_touched
-                                  for s in st_last if s.d_prime is not None)
-    scan_launches = prof.summary().get("pruned_scan", {}).get("launches", 0)
-    scan_rows = args.steps * (hi - lo) * sum(1 for s in st_last if s.d_prime is not None)
-    roof = prof.roofline(args.steps, bytes_override={"pruned_scan": scan_bytes},
-                         rows_per_launch={"pruned_scan": scan_rows / max(1, scan_launches)})
+    st = res.loop.stats
+    roof = roofline(prof, args.steps, args, st, hi - lo)
 
-    # ---- end to end through the public entry with host (pinned) input ----
+    # ---- parity of the timed trajectory with the real reference's (tests/golden/full_c2.npz) ----
+    parity = None
+    if os.path.exists(GOLDEN_C2) and (args.n, args.d, args.k, args.iters, args.centers, args.seed) == \
+            (1_000_000, 1536, 4096, 10, 8192, 0):
+        g = np.load(GOLDEN_C2)
+        checks = {
+            "d_prime": [-1 if s.d_prime is None else s.d_prime for s in st] == g["dp"].tolist(),
+            "survivors": [s.survivors for s in st] == g["surv"].tolist(),
+            "tail_dims": [s.tail_dims_touched for s in st] == g["tail"].tolist(),
+            "n_changed": [-1 if s.n_changed is None else s.n_changed for s in st] == g["changed"].tolist(),
+            "wcss": [s.wcss for s in st] == g["wcss"].tolist(),
+        }
+        parity = {"golden": "tests/golden/full_c2.npz (the real reference, 632.7 s on 8 cores)",
+                  "bitwise_equal": checks, "all": all(checks.values())}
+
+    # ---- end to end through the public entry (api.fit) with pinned host input ----
     e2e = None
     if not args.no_e2e:
         host = torch.empty((hi - lo, args.d), dtype=torch.float32, pin_memory=True)
-        host.copy_(x[:, :args.d].cpu())
-        xe = torch.zeros_like(x)
+        host.numpy()[:] = x_host
         ee0 = torch.cuda.Event(enable_timing=True)
         ee1 = torch.cuda.Event(enable_timing=True)
         barrier()
         ee0.record()
         d2h = 0
+        iters_e2e = 0
         for _ in range(args.steps):
-            job = api._RotationJob(args.d, args.seed)          # host QR overlapped with the copy ...
-            xe[:, :args.d].copy_(host, non_blocking=True)
-            # ... and (1 GPU) with iteration 1's argmin on the unrotated rows
-            r = api.fit_device(xe, args.d, cfg, job, comm=comm, n_global=args.n, row_lo=lo)
-            cent = r.centroids_dev[:, :args.d].cpu()
-            d2h = cent.numel() * 4 + r.loop.assignments.nbytes  # assignments already copied by the loop
+            if world == 1:
+                r = api.fit(host, cfg)  # H2D (one DMA) + host QR beside it + fit + D2H of the result
+                d2h = r.centroids.nbytes + r.assignments.nbytes + r.centroids_rotated.nbytes
+                iters_e2e += len(r.stats)
+            else:
+                job = api._RotationJob(args.d, args.seed)
+                xe = torch.zeros_like(x)
+                xe[:, :args.d].copy_(host, non_blocking=True)
+                r = api.fit_device(xe, args.d, cfg, job, comm=comm, n_global=args.n, row_lo=lo, consume_input=True)
+                cent = r.centroids_dev[:, :args.d].cpu()
+                d2h = cent.numel() * 4 + r.loop.assignments.nbytes
+                iters_e2e += len(r.loop.stats)
         ee1.record()
         barrier()
         e2e_s = max_over_ranks(ee0.elapsed_time(ee1) / 1e3)
-        e2e = {"value": args.iters * args.steps / e2e_s, "unit": UNIT,
+        e2e = {"value": iters_e2e / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(host.numel() * 4) * world, "d2h_bytes_per_step": int(d2h) * world,
-               "note": "host pinned input -> H2D -> host QR (overlapped with the copy and iteration 1) -> fit -> "
-                       "D2H centroids+assignments"}
+               "note": "api.fit on a pinned host matrix: H2D (one DMA), host QR of R (LAPACK, the persisted-model "
+                       "contract) beside the copy, fit, D2H of centroids + assignments" if world == 1 else
+                       "per rank: H2D of the shard, host QR beside it, sharded fit, D2H of centroids + assignments"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc = cpu_reference_sample(args, args.cpu_sample or args.n // 16, iters=args.iters)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": desc}
+        cpu = cpu_baseline_sample(args, x_host)
+
+    extra = None
+    if world == 1 and not args.no_extra:
+        extra = {}
+        for name in [c for c in args.extra.split(",") if c in EXTRA]:
+            gen, n, d, centers, k, iters, etr = EXTRA[name]
+            t0 = time.perf_counter()
+            xh = make_rows(gen, n, d, centers, 0)
+            xd = to_device_matrix(xh, device=dev)
+            del xh
+            gs = time.perf_counter() - t0
+            ccfg = KMeansConfig(k=k, max_iters=iters, seed=0,
+                                etr=EtrConfig(n_queries=etr[0], top_k=etr[1]) if etr else None)
+            rot = generate_rotation(d, 0)
+            r = api.fit_device(xd, d, ccfg, rot)  # warm-up
+            torch.cuda.synchronize()
+            times = []
+            for _ in range(2):
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record()
+                r = api.fit_device(xd, d, ccfg, rot)
+                a1.record()
+                torch.cuda.synchronize()
+                times.append(a0.elapsed_time(a1))
+            s2 = r.loop.stats
+            ms = float(np.median(times))
+            extra[name] = {
+                "workload": f"{'make_blobs' if gen == 'blobs' else 'make_skewed_blobs'}({n}, {d}, {centers}, seed=0), "
+                            f"k={k}, max_iters={iters}" + (f", ETR(n_queries={etr[0]}, top_k={etr[1]})" if etr else ""),
+                "ms_per_fit": round(ms, 2), "iterations": len(s2), "iter_per_s": round(len(s2) / (ms * 1e-3), 2),
+                "terminated_by": r.loop.terminated_by, "d_prime": [s.d_prime for s in s2],
+                "prune_rate": [None if s.prune_rate_after_gemm is None else round(s.prune_rate_after_gemm, 5)
+                               for s in s2],
+                "pruned_dim_fraction": [None if s.d_prime is None else
+                                        round(1.0 - s.tail_dims_touched / (n * k * (d - s.d_prime)), 6) for s in s2],
+                "recall_history": [round(v, 4) for v in r.loop.recall_history], "data_gen_s": round(gs, 1),
+            }
+            del xd
 
     if rank == 0:
-        st = res.loop.stats
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMM, fp32 scan)", "data": "synthetic",
-            "config": {"workload": f"c2: {args.n}x{args.d} fp32 skewed blobs ({args.centers} centres), k={args.k}, "
-                                   f"{args.iters} fixed iterations, rows sharded over {world} GPU(s)",
-                       "l2": "inputs (6 GB) exceed the 126 MB L2 between steps",
-                       "rotation_qr_host_ms": round(qr_s * 1e3, 1),
-                       "d_prime": [s.d_prime for s in st], "prune_rate": [s.prune_rate_after_gemm for s in st],
-                       "phase_ms_last_step": {k: round(v * 1e3, 2) for k, v in res.phase.items()}},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "vs_baseline": None, "dtype": "f32 (reference-exact: fp32 fma-chain rotation, 3xTF32 tensor-core "
+                                          "distances settled by the fp32 chain, fp32 scan)",
+            "data": "synthetic (the reference's make_skewed_blobs generator)",
+            "config": dict(workload(args), **{
+                "rows_per_gpu": hi - lo, "data_gen_s": round(gen_s, 1), "rotation_qr_host_ms": round(qr_s * 1e3, 1),
+                "d_prime": [s.d_prime for s in st],
+                "prune_rate": [None if s.prune_rate_after_gemm is None else round(s.prune_rate_after_gemm, 6)
+                               for s in st],
+                "pruned_dim_fraction": [None if s.d_prime is None else
+                                        round(1.0 - s.tail_dims_touched / (args.n * args.k * (args.d - s.d_prime)), 6)
+                                        for s in st],
+                "phase_ms_last_step": {k_: round(v_ * 1e3, 2) for k_, v_ in res.phase.items()}}),
+            "parity": parity, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(), "configs": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -129,6 +129,16 @@ int skm_dense_argmin(const float* dist, long long ld, int rows, int cols, const 
 int skm_exact_pair_dist(const float* x, long long ldx, const float* centroids, long long ldc, const int* assign,
                         int n, int d, const float* xsq, const float* ysq, int flavour, int q, float* out,
                         void* stream);
+/* Ambiguous argmin rows (global indices rows[0..n_rows)): thr[r] = GATE threshold keeping every
+ * column whose exact distance may be <= the exact best (tau holds the tensor-core best), xs_out[r] =
+ * xsq[rows[r]]; then skm_cand_exact_argmin: exact chain distance of every candidate (cand lists in
+ * GATE layout [n_rows][cap]), lowest column among the smallest, into assign/tau[rows[r]]
+ * (rows with cand_cnt > cap are skipped: the caller re-evaluates them whole). */
+int skm_argmin_candidates(const int* rows, int n_rows, const float* tau, const float* xsq, const float* ysq_max,
+                          float kap, float* thr, float* xs_out, void* stream);
+int skm_cand_exact_argmin(const int* rows, int n_rows, const int* cand, const int* cand_cnt, int cap, const float* x,
+                          long long ldx, const float* centroids, long long ldc, int d, const float* xsq,
+                          const float* ysq, int flavour, int q, int* assign, float* tau, void* stream);
 /* *out = max(v[0..n)) (>= 0), one CTA */
 int skm_max_f32(const float* v, int n, float* out, void* stream);
 

@@ -183,7 +183,16 @@ def _copy_rows_to_device(x: np.ndarray, out: torch.Tensor, d: int, idx: np.ndarr
             e.synchronize()  # the ring is released when the function returns
 
 
-def _h2d(x: np.ndarray, dev, check_finite: bool = False, idx: np.ndarray | None = None) -> torch.Tensor:
+def _pinned_source(x) -> torch.Tensor | None:
+    """A 2-D float32 C-contiguous CPU tensor in pinned memory can be copied by one DMA."""
+    if isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.dim() == 2 and x.dtype == torch.float32 \
+            and x.is_contiguous() and x.is_pinned():
+        return x
+    return None
+
+
+def _h2d(x: np.ndarray, dev, check_finite: bool = False, idx: np.ndarray | None = None,
+         src: torch.Tensor | None = None) -> torch.Tensor:
     """(n, ld) device copy of x (or of the rows x[idx]) with zero pad columns.  ``check_finite``:
     validate_vector_set's NaN/Inf check (model.py:84-87) on the device after the copy -- the
     host scan costs ~0.3 s per GB, more than the fit -- raising the same NonFiniteValue(first
@@ -192,7 +201,10 @@ def _h2d(x: np.ndarray, dev, check_finite: bool = False, idx: np.ndarray | None 
     d = x.shape[1]
     out = torch.zeros((n, padded_ld(d)), dtype=torch.float32, device=dev)
     if n:
-        _copy_rows_to_device(x, out, d, idx)
+        if src is not None and idx is None:
+            out[:, :d].copy_(src, non_blocking=True)  # pinned host rows: one DMA
+        else:
+            _copy_rows_to_device(x, out, d, idx)
         if check_finite:
             first = torch.empty(1, dtype=torch.int64, device=dev)
             native.call("skm_first_nonfinite", ptr(out), out.shape[1], n, d, ptr(first), stream_handle())
@@ -411,13 +423,18 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
 
 
 def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
-    """Sample, rotate, cluster and un-rotate on the B200 (core.py:417-460)."""
+    """Sample, rotate, cluster and un-rotate on the B200 (core.py:417-460).  ``x``: any 2-D
+    array-like (a pinned float32 CPU tensor is copied with a single DMA)."""
+    src = _pinned_source(x)
     x = validate_vector_set(x, check_finite=False)  # finiteness: on the device, below
     dev = require_cuda(device)
     n_total, d = x.shape
     job = _RotationJob(d, cfg.seed)       # host PCG64 + LAPACK QR (persisted-model contract) ...
     if cfg.sampling_fraction == 1:
-        x_dev = _h2d(x, dev, check_finite=True)  # ... overlapped with the copy and iteration 1
+        x_dev = _h2d(x, dev, check_finite=True, src=src)  # ... overlapped with the copy
+        # validate_vector_set, then sample_training_set's EmptySample (core.py:419-425,
+        # preprocess.py:68-70), before init_centroids' KTooLarge
+        sample_indices(n_total, 1.0, [cfg.seed, 1], k=cfg.k)
         sidx = None
         res = fit_device(x_dev, d, cfg, job, inspect=inspect, consume_input=True)
     else:

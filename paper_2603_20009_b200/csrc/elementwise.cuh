@@ -646,11 +646,77 @@ __device__ double np_pairwise_f32(const float* __restrict__ a, int n) {
   return ret;
 }
 
+// one CTA of 64 threads per 8192-element buffer: a full buffer's recursion is the balanced tree over
+// 64 leaves of 128 (every split is an exact half, a multiple of 8), combined left + right level by
+// level; a ragged last buffer takes the general recursion on one thread
 __global__ void np_sum_chunks_kernel(const float* __restrict__ v, long long n, double* __restrict__ part) {
-  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  __shared__ double leaf[64];
+  const long long c = blockIdx.x;
   const long long lo = c * NP_SUM_BUF;
-  if (lo >= n) return;
-  part[c] = np_pairwise_f32(v + lo, static_cast<int>(min((long long)NP_SUM_BUF, n - lo)));
+  const int len = static_cast<int>(min((long long)NP_SUM_BUF, n - lo));
+  const int t = threadIdx.x;
+  if (len == NP_SUM_BUF) {
+    leaf[t] = np_pairwise_leaf(v + lo + 128 * t, 128);
+    __syncthreads();
+    for (int w = 1; w < 64; w *= 2) {
+      if ((t & (2 * w - 1)) == 0) leaf[t] = __dadd_rn(leaf[t], leaf[t + w]);
+      __syncthreads();
+    }
+    if (t == 0) part[c] = leaf[0];
+  } else if (t == 0) {
+    part[c] = np_pairwise_f32(v + lo, len);
+  }
+}
+
+// Exact argmin over a row's candidate list (ascending columns, from a tensor-core GATE pass that
+// kept every column whose exact distance may tie the best): the reference's chain distance of
+// each candidate, smallest value, lowest column on ties.  One warp per row, a lane per candidate.
+__global__ void cand_exact_argmin_kernel(const int* __restrict__ rows, int n_rows, const int2* __restrict__ cand,
+                                         const int* __restrict__ cand_cnt, int cap, const float* __restrict__ x,
+                                         long long ldx, const float* __restrict__ cent, long long ldc, int d,
+                                         const float* __restrict__ xsq, const float* __restrict__ ysq, int flavour,
+                                         int q, int* __restrict__ assign, float* __restrict__ tau) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows; r += gridDim.x * (blockDim.x >> 5)) {
+    const int cnt = cand_cnt[r];
+    if (cnt > cap) continue;  // overflow: the caller re-evaluates the whole row
+    const int g = rows[r];
+    const float* xr = x + static_cast<long long>(g) * ldx;
+    float bv = __int_as_float(0x7f800000);
+    int bj = 0x7fffffff;
+    for (int e = lane; e < cnt; e += 32) {
+      const int j = cand[static_cast<long long>(r) * cap + e].x & 0x7fffffff;
+      const float* cr = cent + static_cast<long long>(j) * ldc;
+      const float ip = flavour == 0 ? exact_dot<CHAIN_FMA>(xr, cr, d, q) : exact_dot<CHAIN_MULADD>(xr, cr, d, 0);
+      float v = __fadd_rn(__fadd_rn(__fmul_rn(ip, -2.0f), xsq[g]), ysq[j]);
+      v = v > 0.0f ? v : 0.0f;
+      if (v < bv || (v == bv && j < bj)) { bv = v; bj = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+    }
+    if (lane == 0) {
+      assign[g] = bj;
+      tau[g] = bv;
+    }
+  }
+}
+
+// GATE threshold for re-evaluating ambiguous argmin rows: every column whose exact distance may
+// be <= the exact best; thr = best~ + 2 kap (xsq + ysq_max + best~ + D) with headroom, rounded up
+__global__ void argmin_cand_threshold_kernel(const int* __restrict__ rows, int n_rows, const float* __restrict__ tau,
+                                             const float* __restrict__ xsq, const float* __restrict__ ysq_max,
+                                             float kap, float* __restrict__ thr, float* __restrict__ xs_out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const int g = rows[r];
+  const double b = tau[g], base = static_cast<double>(xsq[g]) + *ysq_max;
+  const double dl = kap * (base + b);
+  thr[r] = __double2float_ru((b + 2.0 * dl + 2.0 * kap * (base + b + 2.0 * dl)) * (1.0 + 0x1p-20));
+  xs_out[r] = xsq[g];
 }
 
 __global__ void assign_stats_final_kernel(const double* __restrict__ chunk_sum, int chunks,

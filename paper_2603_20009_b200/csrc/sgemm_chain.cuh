@@ -38,12 +38,11 @@ enum ChainFlavour : int { CHAIN_FMA = 0, CHAIN_MULADD = 1 };
 enum ChainMode : int { CHAIN_STORE = 0, CHAIN_DIST = 1 };
 
 struct ChainArgs {
-  const float* a;
+  const float* a;  // row-major, at the K block's first column
   long long lda;
   const float* b;
   long long ldb;
-  int M, N, K;
-  int q;  // K block size of the blocked driver (0: one chain over all of K)
+  int M, N, K;       // K: this launch's K block
   float* out;
   long long ldo;
   const float* xsq;  // DIST: per-row norm term
@@ -118,8 +117,19 @@ __device__ float exact_dot(const float* __restrict__ x, const float* __restrict_
   return tot;
 }
 
-template <int FLAVOUR, int MODE, bool SPLIT>
-__global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(const ChainArgs g) {
+// One launch computes one K block of the blocked driver: each output's chain over the block
+// starts from +0; ACC = 1 adds it to the previous blocks' sum already in `out` (OpenBLAS's
+// C += alpha * A_blk * B_blk with alpha = 1: one fp32 add), so a K-blocked product is a sequence
+// of launches -- exactly the reference's association order -- and no block needs a second set of
+// accumulator registers (124 registers: two CTAs per SM).
+template <int FLAVOUR, int MODE, int ACC>
+#ifndef SKM_CHAIN_PREFETCH
+#define SKM_CHAIN_PREFETCH 1  // measured 36.2 -> 37.8 TFLOP/s at the c2 rotation shape
+#endif
+#ifndef SKM_CHAIN_MINB
+#define SKM_CHAIN_MINB 2
+#endif
+__global__ void __launch_bounds__(CH_THREADS, SKM_CHAIN_MINB) sgemm_chain_kernel(const ChainArgs g) {
   extern __shared__ __align__(16) uint8_t ch_smem[];
   // As2[buf][k][m] = (a, a) pairs, Bs[buf][k][n]
   unsigned long long* As2 = reinterpret_cast<unsigned long long*>(ch_smem);
@@ -165,20 +175,13 @@ __global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(
   };
 
   unsigned long long acc[8][4];
-  unsigned long long tot[SPLIT ? 8 : 1][SPLIT ? 4 : 1];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
-  if constexpr (SPLIT) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) tot[i][j] = 0ull;
-  }
-  int next_b = SPLIT ? chain_next_boundary(0, g.K, g.q) : g.K;
 
   const int ntile = (g.K + CH_BK - 1) / CH_BK;
+  const int kfull = g.K / CH_BK;  // tiles without a ragged end
   if (ntile > 0) {
     gload(0);
     sstore(0);
@@ -189,21 +192,7 @@ __global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(
     if (kt + 1 < ntile) gload((kt + 1) * CH_BK);
     const unsigned long long* A = As2 + buf * CH_BK * CH_BM;
     const float* B = Bs + buf * CH_BK * CH_BN;
-    const int kbase = kt * CH_BK;
-#pragma unroll
-    for (int kk = 0; kk < CH_BK; ++kk) {
-      if constexpr (SPLIT) {
-        if (kbase + kk == next_b) {  // K-block boundary: fold the block's chains into the output
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              tot[i][j] = add2(tot[i][j], acc[i][j]);
-              acc[i][j] = 0ull;
-            }
-          next_b = chain_next_boundary(next_b, g.K, g.q);
-        }
-      }
+    auto step = [&](int kk) {
       const ulonglong2* Ak = reinterpret_cast<const ulonglong2*>(A + kk * CH_BM);
       const ulonglong2 a01 = Ak[ty * 2], a23 = Ak[ty * 2 + 1];
       const ulonglong2 a45 = Ak[32 + ty * 2], a67 = Ak[32 + ty * 2 + 1];
@@ -211,21 +200,46 @@ __global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(
       const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
       const ulonglong2 b47 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + 64 + tx * 4);
       const unsigned long long bv[4] = {b03.x, b03.y, b47.x, b47.y};
-      if (kbase + kk < g.K) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step2<FLAVOUR>(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = chain_step2<FLAVOUR>(av[i], bv[j], acc[i][j]);
+    };
+    if (kt < kfull) {
+#if SKM_CHAIN_PREFETCH
+      // fragments of step kk + 1 are loaded while step kk's FFMA2s run
+      auto lda_ = [&](int kk, unsigned long long* av, unsigned long long* bv) {
+        const ulonglong2* Ak = reinterpret_cast<const ulonglong2*>(A + kk * CH_BM);
+        const ulonglong2 a01 = Ak[ty * 2], a23 = Ak[ty * 2 + 1];
+        const ulonglong2 a45 = Ak[32 + ty * 2], a67 = Ak[32 + ty * 2 + 1];
+        av[0] = a01.x; av[1] = a01.y; av[2] = a23.x; av[3] = a23.y;
+        av[4] = a45.x; av[5] = a45.y; av[6] = a67.x; av[7] = a67.y;
+        const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
+        const ulonglong2 b47 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + 64 + tx * 4);
+        bv[0] = b03.x; bv[1] = b03.y; bv[2] = b47.x; bv[3] = b47.y;
+      };
+      unsigned long long fa[2][8], fb[2][4];
+      lda_(0, fa[0], fb[0]);
+#pragma unroll
+      for (int kk = 0; kk < CH_BK; ++kk) {
+        if (kk + 1 < CH_BK) lda_(kk + 1, fa[(kk + 1) & 1], fb[(kk + 1) & 1]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i][j] = chain_step2<FLAVOUR>(fa[kk & 1][i], fb[kk & 1][j], acc[i][j]);
       }
+#else
+#pragma unroll
+      for (int kk = 0; kk < CH_BK; ++kk) step(kk);
+#endif
+    } else {
+      // ragged last tile: the zero-padded columns past K must not enter the chain
+      // (+0 added to a -0 running value would flip its sign)
+#pragma unroll 1
+      for (int kk = 0; kk < g.K - kt * CH_BK; ++kk) step(kk);
     }
     if (kt + 1 < ntile) sstore(buf ^ 1);
     __syncthreads();
-  }
-  if constexpr (SPLIT) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = add2(tot[i][j], acc[i][j]);
   }
   // epilogue: rows ty*4 + {0..3}, 64 + ty*4 + {0..3}; columns tx*4 + {0..3}, 64 + tx*4 + {0..3}
 #pragma unroll
@@ -238,6 +252,18 @@ __global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(
     for (int h = 0; h < 2; ++h) {
       const int c0 = n0 + h * 64 + tx * 4;
       float v[4] = {f2_lo(acc[i][2 * h]), f2_hi(acc[i][2 * h]), f2_lo(acc[i][2 * h + 1]), f2_hi(acc[i][2 * h + 1])};
+      float* o = g.out + r * g.ldo + c0;
+      const bool vec_o = c0 + 4 <= g.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0);
+      if constexpr (ACC) {  // previous K blocks' sum + this block's chain (one fp32 add)
+        if (vec_o) {
+          const float4 p = *reinterpret_cast<const float4*>(o);
+          v[0] = __fadd_rn(p.x, v[0]); v[1] = __fadd_rn(p.y, v[1]); v[2] = __fadd_rn(p.z, v[2]); v[3] = __fadd_rn(p.w, v[3]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + u < g.N) v[u] = __fadd_rn(o[u], v[u]);
+        }
+      }
       if constexpr (MODE == CHAIN_DIST) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -247,8 +273,7 @@ __global__ void __launch_bounds__(CH_THREADS, SPLIT ? 1 : 2) sgemm_chain_kernel(
           }
         }
       }
-      float* o = g.out + r * g.ldo + c0;
-      if (c0 + 4 <= g.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+      if (vec_o) {
         *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
       } else {
 #pragma unroll

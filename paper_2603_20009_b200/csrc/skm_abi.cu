@@ -147,9 +147,9 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
 
 // ---------------------------------------------------------------- exact-chain GEMM
 namespace {
-template <int FL, int MODE, bool SPLIT>
+template <int FL, int MODE, int ACC>
 int launch_chain(const skm::ChainArgs& g, cudaStream_t st) {
-  auto kern = skm::sgemm_chain_kernel<FL, MODE, SPLIT>;
+  auto kern = skm::sgemm_chain_kernel<FL, MODE, ACC>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -165,35 +165,46 @@ int launch_chain(const skm::ChainArgs& g, cudaStream_t st) {
   SKM_LAUNCH_CHECK("chain_gemm launch");
   return SKM_OK;
 }
+
+template <int FL>
+int launch_chain_block(const skm::ChainArgs& g, bool dist, bool acc, cudaStream_t st) {
+  if (dist) return acc ? launch_chain<FL, 1, 1>(g, st) : launch_chain<FL, 1, 0>(g, st);
+  return acc ? launch_chain<FL, 0, 1>(g, st) : launch_chain<FL, 0, 0>(g, st);
+}
 }  // namespace
 
+// The blocked driver's association order as a sequence of launches: K block b of every output is
+// a fresh chain added to the sum of blocks < b (stored in `out` between launches); the distance
+// expansion runs in the last block's epilogue.
 extern "C" int skm_chain_gemm(const skm_chain_params* p, void* stream) {
   if (!p || p->M < 0 || p->N < 0 || p->K < 0) return fail(SKM_E_ARG, "chain_gemm: bad shape");
   if ((long long)p->M * p->N == 0) return SKM_OK;
   if (p->mode == 1 && (!p->xsq || !p->ysq)) return fail(SKM_E_ARG, "chain_gemm: distance mode needs xsq/ysq");
-  skm::ChainArgs g{};
-  g.a = p->a; g.lda = p->lda; g.b = p->b; g.ldb = p->ldb;
-  g.M = p->M; g.N = p->N; g.K = p->K; g.q = p->q;
-  g.out = p->out; g.ldo = p->ldo; g.xsq = p->xsq; g.ysq = p->ysq;
-  const bool split = p->q > 0 && p->K > p->q;
   cudaStream_t st = as_stream(stream);
-  // rows beyond 65535 tiles: consecutive launches over row ranges
-  const int rows_per = 65535 * skm::CH_BM;
+  const int rows_per = 65535 * skm::CH_BM;  // grid.y limit: consecutive launches over row ranges
   for (int r0 = 0; r0 < p->M; r0 += rows_per) {
-    skm::ChainArgs h = g;
-    h.M = std::min(rows_per, p->M - r0);
-    h.a = p->a + (long long)r0 * p->lda;
-    h.out = p->out + (long long)r0 * p->ldo;
-    if (h.xsq) h.xsq = p->xsq + r0;
-    int rc;
-    if (p->flavour == 0) {
-      if (p->mode == 0) rc = split ? launch_chain<0, 0, true>(h, st) : launch_chain<0, 0, false>(h, st);
-      else rc = split ? launch_chain<0, 1, true>(h, st) : launch_chain<0, 1, false>(h, st);
-    } else {
-      if (p->mode == 0) rc = split ? launch_chain<1, 0, true>(h, st) : launch_chain<1, 0, false>(h, st);
-      else rc = split ? launch_chain<1, 1, true>(h, st) : launch_chain<1, 1, false>(h, st);
-    }
-    if (rc) return rc;
+    int k0 = 0;
+    do {
+      const int k1 = skm::chain_next_boundary(k0, p->K, p->flavour == 0 ? p->q : 0);
+      skm::ChainArgs h{};
+      h.M = std::min(rows_per, p->M - r0);
+      h.N = p->N;
+      h.K = k1 - k0;
+      h.a = p->a + (long long)r0 * p->lda + k0;
+      h.lda = p->lda;
+      h.b = p->b + k0;
+      h.ldb = p->ldb;
+      h.out = p->out + (long long)r0 * p->ldo;
+      h.ldo = p->ldo;
+      h.xsq = p->xsq ? p->xsq + r0 : nullptr;
+      h.ysq = p->ysq;
+      const bool last = k1 >= p->K;
+      const bool dist = last && p->mode == 1;
+      const bool acc = k0 > 0;
+      int rc = p->flavour == 0 ? launch_chain_block<0>(h, dist, acc, st) : launch_chain_block<1>(h, dist, acc, st);
+      if (rc) return rc;
+      k0 = k1;
+    } while (k0 < p->K);
   }
   return SKM_OK;
 }
@@ -499,7 +510,7 @@ int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n
   double* cs = reinterpret_cast<double*>(ws + 2 * align256(16LL * 1024));
   cudaStream_t st = as_stream(stream);
   skm::assign_stats_partial_kernel<<<parts, skm::STAT_THREADS, 0, st>>>(tau, assign, prev, n, ps, pc);
-  if (chunks > 0) skm::np_sum_chunks_kernel<<<(chunks + 127) / 128, 128, 0, st>>>(tau, n, cs);
+  if (chunks > 0) skm::np_sum_chunks_kernel<<<chunks, 64, 0, st>>>(tau, n, cs);
   skm::assign_stats_final_kernel<<<1, 32, 0, st>>>(cs, chunks, pc, parts, out_sum, out_changed);
   SKM_LAUNCH_CHECK("assign_stats");
   return SKM_OK;
@@ -535,6 +546,26 @@ int skm_dense_argmin(const float* dist, long long ld, int rows, int cols, const 
   skm::dense_argmin_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(dist, ld, rows, cols,
                                                                                              row_ids, assign, tau);
   SKM_LAUNCH_CHECK("dense_argmin");
+  return SKM_OK;
+}
+
+int skm_argmin_candidates(const int* rows, int n_rows, const float* tau, const float* xsq, const float* ysq_max,
+                          float kap, float* thr, float* xs_out, void* stream) {
+  if (n_rows <= 0) return SKM_OK;
+  skm::argmin_cand_threshold_kernel<<<(n_rows + 255) / 256, 256, 0, as_stream(stream)>>>(rows, n_rows, tau, xsq,
+                                                                                      ysq_max, kap, thr, xs_out);
+  SKM_LAUNCH_CHECK("argmin_candidates");
+  return SKM_OK;
+}
+
+int skm_cand_exact_argmin(const int* rows, int n_rows, const int* cand, const int* cand_cnt, int cap, const float* x,
+                          long long ldx, const float* centroids, long long ldc, int d, const float* xsq,
+                          const float* ysq, int flavour, int q, int* assign, float* tau, void* stream) {
+  if (n_rows <= 0) return SKM_OK;
+  skm::cand_exact_argmin_kernel<<<grid_for((long long)n_rows * 32, 256), 256, 0, as_stream(stream)>>>(
+      rows, n_rows, reinterpret_cast<const int2*>(cand), cand_cnt, cap, x, ldx, centroids, ldc, d, xsq, ysq, flavour,
+      q, assign, tau);
+  SKM_LAUNCH_CHECK("cand_exact_argmin");
   return SKM_OK;
 }
 

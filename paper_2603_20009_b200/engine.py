@@ -127,6 +127,21 @@ def _i64(t: torch.Tensor) -> int:
     return int(t.item())
 
 
+SHARD_ALIGN = 8192  # NumPy's reduction buffer: shards of whole buffers keep wcss = np.sum bitwise
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row shard of a rank.  Large inputs take equal shares rounded up to whole
+    8192-row buffers, so every rank's partial sums of tau are whole buffers of the reference's
+    np.sum (core.py:344) and the reduced wcss is bitwise the single-GPU one; the rounding is skipped
+    when it could leave a rank empty (n <= world * world * 8192)."""
+    per = -(-n // world)
+    if world > 1 and n > world * world * SHARD_ALIGN:
+        per = -(-per // SHARD_ALIGN) * SHARD_ALIGN
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
 class Comm:
     """Row-sharded data parallelism: one allreduce(sum) per iteration over a packed buffer.
 
@@ -177,9 +192,7 @@ class Comm:
 
     def shard(self, n: int) -> tuple[int, int]:
         """Contiguous row range of this rank."""
-        per = (n + self.world - 1) // self.world
-        lo = min(n, self.rank * per)
-        return lo, min(n, lo + per)
+        return shard_bounds(n, self.world, self.rank)
 
 
 @dataclass
@@ -438,7 +451,38 @@ def full_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, row0: in
                 d, ptr(xsq), ptr(cents.ysq), ws.chain_flavour, ws.chain_q, ptr(tau), st, nbytes=4.0 * n * d)
     n_amb = int(ws.amb_count.item())
     if n_amb:
-        exact_rows_argmin(data, cents, ws, ws.amb_rows[:n_amb], row0, xsq)
+        resolve_ambiguous_argmin(data, cents, ws, ws.amb_rows[:n_amb], row0, xsq)
+
+
+def resolve_ambiguous_argmin(data: DeviceData, cents: Centroids, ws: Workspace, rows_local: torch.Tensor, row0: int,
+                             xsq: torch.Tensor) -> None:
+    """Rows whose runner-up lies within the error bound of the best: a tensor-core GATE pass over
+    just these rows lists every column whose exact distance may tie or beat the best (typically
+    2-4), and the reference's chain distance of each decides (lowest column on ties).  Rows with
+    more candidates than the slab holds take the whole chain-GEMM distance row."""
+    st = stream_handle()
+    d, k = data.d, cents.k
+    kap = tc_kappa(d)
+    xsq_all = data.norms(d)
+    glob_all = (rows_local + row0).to(torch.int32)
+    for c0 in range(0, int(glob_all.numel()), ws.batch):
+        glob = glob_all[c0:c0 + ws.batch].contiguous()
+        m = int(glob.numel())
+        thr, xs = ws.bthr[:m], ws.bx[:m]
+        native.call("skm_argmin_candidates", ptr(glob), m, ptr(ws.tau), ptr(xsq_all), ptr(cents.ysq_max),
+                    float(kap), ptr(thr), ptr(xs), st)
+        xa_hi = torch.empty((m, data.ld), dtype=torch.float32, device=data.x.device)
+        xa_lo = torch.empty_like(xa_hi)
+        native.call("skm_gather_rows_i32", ptr(data.hi), data.ld, ptr(glob), m, data.ld, ptr(xa_hi), data.ld, st)
+        native.call("skm_gather_rows_i32", ptr(data.lo), data.ld, ptr(glob), m, data.ld, ptr(xa_lo), data.ld, st)
+        _gemm(xa_hi, xa_lo, cents.hi, cents.lo, m, k, d, native.GEMM_GATE, xsq=xs, ysq=cents.ysq, thr=thr,
+              cand=ws.cand, cand_cnt=ws.cand_cnt, cand_cap=ws.cap)
+        native.call("skm_cand_exact_argmin", ptr(glob), m, ptr(ws.cand), ptr(ws.cand_cnt), ws.cap, ptr(data.x),
+                    data.ld, ptr(cents.c), cents.ld, d, ptr(xsq_all), ptr(cents.ysq), ws.chain_flavour,
+                    ws.chain_q, ptr(ws.assign), ptr(ws.tau), st)
+        over = torch.nonzero(ws.cand_cnt[:m] > ws.cap).flatten()
+        if over.numel():
+            exact_rows_argmin(data, cents, ws, (glob[over] - row0).to(torch.int32), row0, xsq)
 
 
 def exact_rows_argmin(data: DeviceData, cents: Centroids, ws: Workspace, rows_local: torch.Tensor, row0: int,

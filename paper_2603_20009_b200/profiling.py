@@ -32,6 +32,36 @@ def peaks() -> dict:
                 "source": "B200_PROFILING.md fallback"}
 
 
+def _profile_json(name: str) -> dict | None:
+    try:
+        with open(os.path.join(_ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def fp32_peak() -> float:
+    """FFMA / FFMA2 peak measured on B200 (tools/micro/ffma2_bench.cu, profiles/fp32_peak.json)."""
+    m = _profile_json("fp32_peak.json")
+    return float(m["ffma2_tflops"]) if m else 74.0
+
+
+def l2_peak() -> dict:
+    """L2 read bandwidth measured on B200 (tools/micro/l2_bw.cu, profiles/l2_peak.json)."""
+    m = _profile_json("l2_peak.json")
+    if m:
+        return {"gbs": float(m["l2_read_gbs"]), "source": "profiles/l2_peak.json (measured, tools/micro/l2_bw.cu)"}
+    return {"gbs": 18000.0, "source": "estimate"}
+
+
+def traffic_per_launch(kernel: str, rows_per_launch: float) -> float | None:
+    """DRAM bytes (read + write) of one launch from a committed ncu --set full capture, scaled per row."""
+    tr = _traffic_record(kernel)
+    if not tr:
+        return None
+    return tr["dram_bytes"] / tr["rows"] * rows_per_launch
+
+
 class KernelTimer:
     def __init__(self):
         import torch
@@ -60,45 +90,6 @@ class KernelTimer:
             s["flops"] += fl
             s["bytes"] += by
         return agg
-
-    def roofline(self, steps: int, bytes_override: dict | None = None, rows_per_launch: dict | None = None) -> dict:
-        agg = self.summary()
-        for k_, v_ in (bytes_override or {}).items():
-            if k_ in agg:
-                agg[k_]["bytes"] = v_
-        if not agg:
-            return {}
-        pk = peaks()
-        name, top = max(agg.items(), key=lambda kv: kv[1]["ms"])
-        total_ms = sum(v["ms"] for v in agg.values())
-        per_launch_ms = top["ms"] / top["launches"]
-        out = {"kernel": name, "share_of_kernel_time": top["ms"] / total_ms, "launches": top["launches"],
-               "avg_launch_ms": per_launch_ms, "peak_source": pk["source"], "traffic": None}
-        if top["flops"] > 0:
-            # 3xTF32: the tensor pipe executes 3 TF32 MMAs per fp32-accurate product; dense TF32
-            # peak is half the measured dense BF16 peak.
-            alg_tflops = top["flops"] / (top["ms"] * 1e-3) / 1e12
-            exec_tflops = 3.0 * alg_tflops
-            tf32_peak = pk["bf16_tflops"] / 2.0
-            out.update({"bound": "tensor", "achieved": exec_tflops, "peak": tf32_peak, "unit": "TFLOP/s",
-                        "frac": exec_tflops / tf32_peak, "algorithmic_fp32_tflops": alg_tflops,
-                        "note": "achieved = executed TF32 MMA flops (3 per fp32-accurate product) / time; "
-                                "peak = dense TF32 = measured bf16 dense / 2"})
-        else:
-            gbs = top["bytes"] / (top["ms"] * 1e-3) / 1e9
-            out.update({"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": gbs / pk["hbm_gbs"],
-                        "note": "achieved = algorithmic bytes / time; for pruned_scan the bytes are the x tail "
-                                "rows (HBM) + 4 B per touched (vector, centroid, dim) of the L2-resident "
-                                "centroid tails (exact dims-touched counter)"})
-        out["per_kernel_ms_per_step"] = {k: round(v["ms"] / steps, 3) for k, v in agg.items()}
-        tr = _traffic_record(name)
-        if tr and rows_per_launch:
-            # DRAM bytes (read + write) of one launch of this kernel from a committed ncu --set full
-            # capture, scaled per row to this run's average launch
-            out["traffic"] = tr["dram_bytes"] / tr["rows"] * rows_per_launch.get(name, tr["rows"])
-            out["traffic_source"] = tr["source"]
-        return out
 
 
 def _traffic_record(kernel: str) -> dict | None:

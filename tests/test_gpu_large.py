@@ -19,7 +19,7 @@ D = 1024
 
 @pytest.fixture(scope="module")
 def doubled():
-    from bench import make_shard_device
+    from paper_2603_20009_b200.synth import make_shard_device
     dev = torch.device("cuda", 0)
     half = make_shard_device(N_HALF, D, 600, 0, N_HALF, 11, dev)
     return torch.cat([half, half]), dev

@@ -95,9 +95,8 @@ def _exchange_worker(rank, world, port, q):
         order = torch.as_tensor(np.argsort(a_l, kind="stable").astype(np.int32))
         counts = np.bincount(a_l, minlength=mk)
         offs = np.concatenate(([0], np.cumsum(counts)[:-1]))
-        table = np.stack([np.bincount(assign[min(n, r * ((n + world - 1) // world)):
-                                              min(n, (r + 1) * ((n + world - 1) // world))], minlength=mk)
-                          for r in range(world)])
+        from paper_2603_20009_b200.engine import shard_bounds
+        table = np.stack([np.bincount(assign[slice(*shard_bounds(n, world, r))], minlength=mk) for r in range(world)])
         owner = group_owners(table.sum(axis=0), world)
         data = types.SimpleNamespace(x=x[lo:hi], n=hi - lo, ld=ld)
         rows, gids, goff = _exchange_groups(data, order, offs, table, owner, comm, lo)

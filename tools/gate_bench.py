@@ -7,7 +7,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200.synth import make_shard_device  # noqa: E402
 from paper_2603_20009_b200 import native  # noqa: E402
 from paper_2603_20009_b200.api import _split  # noqa: E402
 from paper_2603_20009_b200.engine import _gemm  # noqa: E402

@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 os.environ.setdefault("SKM_DIAG", "1")  # scan diagnostics read back per iteration
 
-from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200.synth import make_shard_device  # noqa: E402
 from paper_2603_20009_b200 import api, engine  # noqa: E402
 from paper_2603_20009_b200.config import KMeansConfig  # noqa: E402
 from paper_2603_20009_b200.hostmath import generate_rotation  # noqa: E402

@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 os.environ.setdefault("SKM_DIAG", "1")  # scan diagnostics read back per iteration
 
-from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200.synth import make_shard_device  # noqa: E402
 from paper_2603_20009_b200 import api, profiling  # noqa: E402
 from paper_2603_20009_b200.config import EtrConfig, KMeansConfig  # noqa: E402
 from paper_2603_20009_b200.hostmath import generate_rotation  # noqa: E402

@@ -10,7 +10,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200.synth import make_shard_device  # noqa: E402
 from paper_2603_20009_b200 import profiling  # noqa: E402
 from paper_2603_20009_b200.engine import Comm  # noqa: E402
 from paper_2603_20009_b200.hierarchical import HierarchicalConfig, hierarchical_fit, hierarchical_fit_device  # noqa: E402

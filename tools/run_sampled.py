@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200.synth import make_shard_device  # noqa: E402
 import paper_2603_20009_b200 as skb  # noqa: E402
 
 ap = argparse.ArgumentParser()

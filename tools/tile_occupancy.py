@@ -8,7 +8,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from bench import make_shard_device  # noqa: E402
+from paper_2603_20009_b200.synth import make_shard_device  # noqa: E402
 from paper_2603_20009_b200 import api, engine  # noqa: E402
 from paper_2603_20009_b200.config import KMeansConfig  # noqa: E402
 from paper_2603_20009_b200.hostmath import generate_rotation  # noqa: E402
