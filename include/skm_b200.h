@@ -175,6 +175,9 @@ int skm_apply_splits(float* centroids, long long ldc, int d, const int* empties,
                      float eps, void* stream);
 /* stats[0] (f64) = sum(tau), stats[1] (u64) = count(assign != prev) (prev may be NULL) */
 long long skm_stats_workspace_bytes(int n);
+/* out[c] = NumPy's pairwise sum (f64) of tau[8192 c, 8192 (c + 1)) -- the per-buffer partials of
+ * np.sum(tau, dtype=np.float64) (core.py:344); summed in buffer order they give wcss bitwise. */
+int skm_tau_chunk_sums(const float* tau, long long n, double* out, void* stream);
 int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n, double* out_sum,
                      unsigned long long* out_changed, void* workspace, long long workspace_bytes, void* stream);
 

@@ -83,4 +83,10 @@ def __getattr__(name):
                 "update_centroids", "split_empty_clusters"):
         from . import extras
         return getattr(extras, name)
+    if name in ("PruneOutcome", "initial_threshold", "prune_and_assign", "measure_prune_rate"):
+        from . import pruning
+        return getattr(pruning, name)
+    if name in ("fit_lloyd", "LloydResult"):
+        from . import lloyd
+        return getattr(lloyd, name)
     raise AttributeError(name)

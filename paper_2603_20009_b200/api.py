@@ -26,7 +26,7 @@ from .config import (
     pruning_supported,
     validate_vector_set,
 )
-from .device import padded_ld, ptr, require_cuda, stream_handle
+from .device import on_device, padded_ld, ptr, require_cuda, stream_handle
 from .engine import (
     Centroids,
     Comm,
@@ -381,11 +381,12 @@ class DeviceFit:
 def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: RotationMatrix, inspect=None,
                comm: Comm | None = None, n_global: int | None = None, row_lo: int = 0, keep_data: bool = False,
                init_rows: torch.Tensor | None = None, consume_input: bool = False) -> DeviceFit:
-    """The hot path with inputs already in HBM: rotate (tcgen05 GEMM), Lloyd loop, un-rotate.
+    """The hot path with inputs already in HBM: exact-chain rotation, Lloyd loop, un-rotation.
 
     ``x_dev`` is this rank's (n_local, ld) shard (pad columns zero); with ``comm.world > 1``
-    the Forgy rows are assembled across ranks by one allreduce."""
-    comm = comm or Comm()
+    (pass ``comm=Comm()`` under torch.distributed, plus ``n_global`` / ``row_lo``) the Forgy rows
+    are assembled across ranks by one allreduce.  Without ``comm`` the rows are one process's."""
+    comm = comm or Comm.local()
     dev = x_dev.device
     timer = _Timer()
     ws = None
@@ -422,9 +423,18 @@ def fit_device(x_dev: torch.Tensor, d: int, cfg: KMeansConfig, rotation: Rotatio
     return DeviceFit(loop=out, rotation=rotation, centroids_dev=cent, data=data, phase=phase)
 
 
-def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
+@on_device
+def fit(x, cfg: KMeansConfig, inspect=None, device=None, comm: Comm | None = None) -> KMeansResult:
     """Sample, rotate, cluster and un-rotate on the B200 (core.py:417-460).  ``x``: any 2-D
-    array-like (a pinned float32 CPU tensor is copied with a single DMA)."""
+    array-like (a pinned float32 CPU tensor is copied with a single DMA).
+
+    Under torch.distributed (or with ``comm``) every rank passes the same matrix and copies only
+    its contiguous row shard (like ``hierarchical_fit``); the loop runs row-sharded with one
+    allreduce per iteration, and every rank returns the same result (assignments of all rows).
+    ``inspect`` then receives this rank's rows only."""
+    comm = comm or Comm()
+    if comm.world > 1:
+        return _fit_sharded(x, cfg, inspect, device, comm)
     src = _pinned_source(x)
     x = validate_vector_set(x, check_finite=False)  # finiteness: on the device, below
     dev = require_cuda(device)
@@ -478,6 +488,39 @@ def fit(x, cfg: KMeansConfig, inspect=None, device=None) -> KMeansResult:
     )
 
 
+def _fit_sharded(x, cfg: KMeansConfig, inspect, device, comm: Comm) -> KMeansResult:
+    """fit() across ranks: shard-wise finiteness (same error on every rank), the sample drawn on
+    every host with the same stream, each rank's contiguous shard of the sampled rows uploaded,
+    the sharded loop, and the assignments assembled by one allreduce."""
+    x = validate_vector_set(x, check_finite=False)
+    dev = require_cuda(device)
+    n_total, d = x.shape
+    job = _RotationJob(d, cfg.seed)
+    lo0, hi0 = comm.shard(n_total)
+    _check_finite_sharded(x[lo0:hi0], dev, lo0, comm)
+    sidx = sample_indices(n_total, cfg.sampling_fraction, [cfg.seed, 1], k=cfg.k)
+    xs = x if sidx is None else x[sidx]
+    n = xs.shape[0]
+    lo, hi = comm.shard(n)
+    x_dev = _h2d(xs[lo:hi], dev)
+    res = fit_device(x_dev, d, cfg, job, inspect=inspect, comm=comm, n_global=n, row_lo=lo, consume_input=True)
+    out = res.loop
+    full = torch.zeros(n, dtype=torch.int32, device=dev)
+    full[lo:hi] = out.assign_dev[:hi - lo]
+    comm.allreduce_(full)
+    assignments = full.cpu().numpy()
+    ld = padded_ld(d)
+    phase = dict(res.phase)
+    phase["rotation_host"] = job.seconds
+    return KMeansResult(
+        centroids=res.centroids_dev[:, :d].cpu().numpy().copy(), assignments=assignments, stats=out.stats,
+        terminated_by=out.terminated_by, rotation=res.rotation, centroids_rotated=out.centroids_rotated,
+        d_prime_final=out.d_prime_final, sample_indices=sidx, init_indices=out.init_indices, work=out.work,
+        phase_seconds=phase, peak_aux_values=3 * (hi - lo) * ld + 6 * (hi - lo) + 4 * cfg.k * ld, n_train=n,
+        recall_history=out.recall_history)
+
+
+@on_device
 def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, batch_rows: int = 1 << 20
                  ) -> np.ndarray:
     """Assign every vector to the fitted centroids with the pruned pass (core.py:463-541).

@@ -35,6 +35,17 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Per-device "first use" flag for function attributes (cudaFuncSetAttribute is per device): one
+// bit per device ordinal in the caller's static mask.
+inline bool first_use_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
 inline int grid_for(long long work, int threads, int cap = 148 * 32) {
   long long g = (work + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -98,11 +109,10 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
     if ((rc = make_tmap(&te_b_lo, p->b_lo + p->K, p->N, ext_k, p->ldb, BN))) return rc;
   }
   auto kern = skm::gemm_tf32x3_kernel<STAGES, MODE, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set_mask = 0;
+  if (first_use_on_device(attr_set_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (e != cudaSuccess) return cuda_fail(e, "gemm smem attribute");
-    attr_set = true;
   }
   skm::GemmArgs a{};
   a.M = p->M;
@@ -150,14 +160,11 @@ namespace {
 template <int FL, int MODE, int ACC>
 int launch_chain(const skm::ChainArgs& g, cudaStream_t st) {
   auto kern = skm::sgemm_chain_kernel<FL, MODE, ACC>;
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
+  static unsigned long long attr_dev_mask = 0;
+  if (first_use_on_device(attr_dev_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(skm::chain_smem_bytes()));
     if (e != cudaSuccess) return cuda_fail(e, "chain_gemm smem attribute");
-    attr_dev = dev;
   }
   dim3 grid((g.N + skm::CH_BN - 1) / skm::CH_BN, (g.M + skm::CH_BM - 1) / skm::CH_BM);
   if (grid.y > 65535) return fail(SKM_E_ARG, "chain_gemm: too many row tiles for one launch");
@@ -329,12 +336,11 @@ int skm_seed_thresholds(const float* x, long long ldx, const float* centroids, l
   const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(centroids)) & 15) == 0 &&
                        ldx % 4 == 0 && ldc % 4 == 0;
   if (aligned) {
-    static bool set = false;
-    if (!set) {
+    static unsigned long long set_mask = 0;
+    if (first_use_on_device(set_mask)) {
       cudaError_t e = cudaFuncSetAttribute(skm::seed_thresholds_async_kernel<0>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "seed_thresholds smem attribute");
-      set = true;
     }
     skm::seed_thresholds_async_kernel<0><<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, skm::SEEDA_SMEM,
                                         as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out);
@@ -434,12 +440,11 @@ int skm_cluster_sums(const float* x, long long ldx, const int* order, const int*
   if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && ldx % 4 == 0) {
     const int groups = (d + 3) / 4;
     const int threads = std::min(768, (groups + 31) / 32 * 32);  // ring <= 768 x 16 x 16 B = 192 KB
-    static bool set = false;
-    if (!set) {
+    static unsigned long long set_mask = 0;
+    if (first_use_on_device(set_mask)) {
       cudaError_t e = cudaFuncSetAttribute(skm::ordered_cluster_sums_vec_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SUMV_RING * 768 * 16);
       if (e != cudaSuccess) return cuda_fail(e, "cluster_sums smem attribute");
-      set = true;
     }
     skm::ordered_cluster_sums_vec_kernel<<<k, threads, skm::SUMV_RING * threads * 16, as_stream(stream)>>>(
         x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
@@ -497,6 +502,14 @@ int skm_apply_splits(float* centroids, long long ldc, int d, const int* empties,
 long long skm_stats_workspace_bytes(int n) {
   const long long chunks = (std::max(n, 1) + skm::NP_SUM_BUF - 1) / skm::NP_SUM_BUF;
   return 2 * align256(16LL * 1024) + align256(8 * chunks);
+}
+
+int skm_tau_chunk_sums(const float* tau, long long n, double* out, void* stream) {
+  if (n <= 0) return SKM_OK;
+  const long long chunks = (n + skm::NP_SUM_BUF - 1) / skm::NP_SUM_BUF;
+  skm::np_sum_chunks_kernel<<<static_cast<unsigned>(chunks), 64, 0, as_stream(stream)>>>(tau, n, out);
+  SKM_LAUNCH_CHECK("tau_chunk_sums");
+  return SKM_OK;
 }
 
 int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n, double* out_sum,
@@ -584,14 +597,11 @@ int skm_exact_pair_dist(const float* x, long long ldx, const float* centroids, l
   if (!aligned) return fail(SKM_E_ARG, "exact_pair_dist: needs 16-byte aligned rows");
   auto k1 = skm::seed_thresholds_async_kernel<1>;
   auto k2 = skm::seed_thresholds_async_kernel<2>;
-  static int set_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (set_dev != dev) {
+  static unsigned long long set_dev_mask = 0;
+  if (first_use_on_device(set_dev_mask)) {
     cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "exact_pair_dist smem attribute");
-    set_dev = dev;
   }
   const int grid = (n + skm::SEED_ROWS - 1) / skm::SEED_ROWS;
   if (flavour == 0)
@@ -682,21 +692,19 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms * std::max(per_sm, 1)));
   cudaStream_t st = as_stream(stream);
   if (p->dense_mode) {
-    static bool set = false;
-    if (!set) {
+    static unsigned long long set_mask = 0;
+    if (first_use_on_device(set_mask)) {
       cudaFuncSetAttribute(skm::pruned_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(skm::scan_dyn_smem(skm::SCAN_NB_MAX)));
-      set = true;
     }
     skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   } else {
-    static bool set = false;
-    if (!set) {
+    static unsigned long long set_mask = 0;
+    if (first_use_on_device(set_mask)) {
       cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(skm::scan_dyn_smem(skm::SCAN_NB_MAX)));
       const char* cv = getenv("SKM_SCAN_CARVEOUT");
       if (cv) cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
-      set = true;
     }
     skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   }
@@ -731,10 +739,9 @@ int skm_etr_hits(const int* gt, int gt_ld, int top_k, const int* probe, int prob
   if (nq <= 0) return SKM_OK;
   const size_t smem = sizeof(unsigned) * ((k + 31) / 32);
   if (smem > 200 * 1024) return fail(SKM_E_ARG, "etr_hits: k too large for the shared bitmap");
-  static bool set = false;
-  if (!set) {
+  static unsigned long long set_mask = 0;
+  if (first_use_on_device(set_mask)) {
     cudaFuncSetAttribute(skm::etr_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    set = true;
   }
   skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, row_lo,
                                                              row_hi, k, hits);
@@ -749,10 +756,9 @@ int skm_probe_tally(const int* gt, int gt_ld, int top_k, const int* probe, int p
   if (nq <= 0) return SKM_OK;
   const size_t smem = sizeof(unsigned) * ((k + 31) / 32);
   if (smem > 200 * 1024) return fail(SKM_E_ARG, "probe_tally: k too large for the shared bitmap");
-  static bool set = false;
-  if (!set) {
+  static unsigned long long set_mask = 0;
+  if (first_use_on_device(set_mask)) {
     cudaFuncSetAttribute(skm::etr_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    set = true;
   }
   skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, 0, n,
                                                              k, hits, sizes, explored);

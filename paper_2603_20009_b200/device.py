@@ -17,6 +17,24 @@ import torch
 from . import native
 
 
+def on_device(fn):
+    """Public entry points with a ``device=`` argument run with that device current: native
+    kernels launch on the current device's stream (stream_handle), so torch work and native work
+    stay on one device and one stream."""
+    import functools
+    import inspect as _inspect
+    pos = list(_inspect.signature(fn).parameters).index("device")
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        dev = kw.get("device", args[pos] if len(args) > pos else None)
+        if dev is None or not torch.cuda.is_available():
+            return fn(*args, **kw)
+        with torch.cuda.device(torch.device(dev)):
+            return fn(*args, **kw)
+    return wrapper
+
+
 def require_cuda(device=None) -> torch.device:
     if not torch.cuda.is_available():
         raise native.NativeUnavailable("a CUDA device is required (no CPU fallback by design)")

@@ -653,28 +653,20 @@ def _scan_exact_args(sp, data: DeviceData, cents: Centroids, ws: Workspace, xsq:
 def update_centroids_device(data: DeviceData, cents: Centroids, ws: Workspace, comm: Comm,
                             sums_buf: torch.Tensor | None = None, sorted_counts: np.ndarray | None = None
                             ) -> np.ndarray:
-    """Mean of member rows (f64 ordered sums), empties keep their previous centroid.
-    Returns host int64 counts (global).  ``sorted_counts``: the cluster sort already ran
-    (ws.order / counts / offsets current) and these are its counts."""
+    """One-GPU update: mean of member rows (f64 ordered sums, bitwise the reference's serial loop),
+    empties keep their previous centroid.  Returns host int64 counts.  ``sorted_counts``: the
+    cluster sort already ran (ws.order / counts / offsets current) and these are its counts.
+    (Multi-GPU updates go through Reducer, inside the iteration's one allreduce.)"""
     st = stream_handle()
     k, d = cents.k, cents.d
+    if comm.world > 1:
+        raise RuntimeError("update_centroids_device is the 1-GPU update; sharded loops use Reducer")
     if sorted_counts is None:
         native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
                     ptr(ws.sort_ws), ws.sort_ws.numel(), st, nbytes=32.0 * data.n)
-    if comm.world == 1:
-        native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k, d,
-                    None, 0, ptr(cents.c), cents.ld, 0, st, nbytes=4.0 * data.n * d + 4.0 * k * d)
-        return sorted_counts if sorted_counts is not None else ws.counts.cpu().numpy().astype(np.int64)
-    # multi-GPU: local ordered sums -> one packed allreduce [sums | counts] -> finalize
-    packed = sums_buf if sums_buf is not None else torch.empty(k * d + k, dtype=torch.float64, device=data.x.device)
-    sums = packed[: k * d]
     native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k, d,
-                ptr(sums), 0, None, 0, 1, st)
-    packed[k * d:].copy_(ws.counts.to(torch.float64))
-    comm.allreduce_(packed)
-    counts64 = packed[k * d:].round().to(torch.int64)
-    native.call("skm_finalize_centroids", ptr(sums), ptr(counts64), k, d, ptr(cents.c), cents.ld, st)
-    return counts64.cpu().numpy()
+                None, 0, ptr(cents.c), cents.ld, 0, st, nbytes=4.0 * data.n * d + 4.0 * k * d)
+    return sorted_counts if sorted_counts is not None else ws.counts.cpu().numpy().astype(np.int64)
 
 
 def apply_splits_device(cents: Centroids, counts: np.ndarray, rng) -> int:
@@ -692,6 +684,108 @@ def apply_splits_device(cents: Centroids, counts: np.ndarray, rng) -> int:
 def assign_stats(ws: Workspace, n: int, with_prev: bool) -> None:
     native.call("skm_assign_stats", ptr(ws.tau), ptr(ws.assign), ptr(ws.prev) if with_prev else None, n,
                 ptr(ws.wcss), ptr(ws.changed), ptr(ws.stats_ws), ws.stats_ws.numel(), stream_handle())
+
+
+# ------------------------------------------------------------------------------ multi-GPU reduction
+class Reducer:
+    """The iteration's only collective at N > 1: ONE allreduce(sum) of a packed f64 buffer
+    [centroid sums k*d | counts k | n_changed, survivors, dims touched | tau buffer partials]
+    (SURVEY.md 8e).  The update's sums are computed before the convergence test and dropped when
+    the loop stops there (core.py:354-363).
+
+    * tau buffer partials: NumPy sums tau in 8192-element buffers (core.py:344); shards start on
+      buffer boundaries (shard_bounds), so each rank writes its buffers' pairwise sums into their
+      global slots and the host adds the slots in order -- wcss is the 1-GPU (= reference) value.
+    * exact=True: the f64 member sums are chained in rank order -- rank r continues rank r-1's
+      running sums over its own members (rows are sharded in ascending order, so this is the
+      reference's serial row order, _kernels.pyx:115-119) -- pipelined over cluster chunks with
+      point-to-point sends; only the last rank's sums enter the allreduce (the others add 0.0,
+      exact).  Centroids are then bitwise the 1-GPU result.  exact=False: each rank's sums start
+      from 0 and the allreduce adds them (centroids equal up to f64 association)."""
+
+    def __init__(self, comm: "Comm", k: int, d: int, n_global: int, row_lo: int, n_local: int, dev, exact: bool):
+        self.comm, self.k, self.d, self.exact = comm, k, d, exact
+        self.aligned = row_lo % SHARD_ALIGN == 0 and (n_local % SHARD_ALIGN == 0 or row_lo + n_local == n_global)
+        self.n_chunks = -(-n_global // SHARD_ALIGN) if self.aligned else 1
+        self.chunk0 = row_lo // SHARD_ALIGN if self.aligned else 0
+        self.o_cnt = k * d
+        self.o_scal = self.o_cnt + k
+        self.o_tau = self.o_scal + 3
+        self.buf = torch.zeros(self.o_tau + self.n_chunks, dtype=torch.float64, device=dev)
+        self.pin = torch.empty(self.buf.numel() - self.o_cnt, dtype=torch.float64, pin_memory=True)
+        self.counts64 = torch.empty(k, dtype=torch.int64, device=dev)
+
+    def reduce(self, data: "DeviceData", ws: "Workspace", n_local: int) -> tuple[np.ndarray, float, float, float, float]:
+        """Local stats + sorted sums -> one allreduce -> (counts, wcss, n_changed, survivors, touched)."""
+        st = stream_handle()
+        k, d = self.k, self.d
+        buf = self.buf
+        buf[self.o_tau:].zero_()
+        if self.aligned:
+            nloc = max(n_local, 0)
+            if nloc:
+                native.call("skm_tau_chunk_sums", ptr(ws.tau), nloc, ptr(buf[self.o_tau + self.chunk0:]), st)
+        else:
+            buf[self.o_tau] = ws.wcss[0]
+        buf[self.o_scal] = ws.changed[0].to(torch.float64)
+        buf[self.o_scal + 1] = ws.counters[0].to(torch.float64)
+        buf[self.o_scal + 2] = ws.counters[1].to(torch.float64)
+        buf[self.o_cnt:self.o_scal].copy_(ws.counts.to(torch.float64))
+        sums = buf[:self.o_cnt]
+        if self.exact and self.comm.world > 1:
+            self._chained_sums(data, ws, sums)
+        else:
+            native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k,
+                        d, ptr(sums), 0, None, 0, 1, st, nbytes=4.0 * data.n * d)
+        self.comm.allreduce_(buf)
+        self.pin.copy_(buf[self.o_cnt:], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = self.pin.numpy()
+        counts = np.rint(h[:k]).astype(np.int64)
+        ch, sv, td = (float(v) for v in h[k:k + 3])
+        wcss = 0.0
+        for v in h[k + 3:]:  # NumPy's buffer order: bitwise the reference's np.sum
+            wcss += float(v)
+        return counts, wcss, ch, sv, td
+
+    def finalize(self, cents: "Centroids", counts: np.ndarray) -> None:
+        """centroid = f32(sum / count); empty clusters keep their previous row (core.py:93-99)."""
+        self.counts64.copy_(torch.from_numpy(counts))
+        native.call("skm_finalize_centroids", ptr(self.buf), ptr(self.counts64), self.k, self.d, ptr(cents.c),
+                    cents.ld, stream_handle())
+
+    def _chained_sums(self, data, ws, sums: torch.Tensor, chunks: int = 16) -> None:
+        """Rank-order f64 sums, pipelined over cluster chunks: receive rank r-1's running sums of
+        a chunk, continue them over this rank's members, send them on; ranks before the last
+        then contribute zeros to the allreduce."""
+        comm, k, d = self.comm, self.k, self.d
+        r, w = comm.rank, comm.world
+        st = stream_handle()
+        step = -(-k // chunks)
+        nccl = comm.dist.get_backend(comm.group) == "nccl"
+        pending = []
+        for c0 in range(0, k, step):
+            c1 = min(k, c0 + step)
+            seg = sums[c0 * d:c1 * d]
+            if r > 0:
+                if nccl:
+                    comm.dist.recv(seg, src=r - 1, group=comm.group)
+                else:
+                    tmp = torch.empty(seg.shape, dtype=seg.dtype)
+                    comm.dist.recv(tmp, src=r - 1, group=comm.group)
+                    seg.copy_(tmp)
+            native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets[c0:]),
+                        ptr(ws.counts[c0:]), c1 - c0, d, ptr(seg), int(r > 0), None, 0, 1, st,
+                        nbytes=4.0 * data.n * d * (c1 - c0) / k)
+            if r < w - 1:
+                if nccl:
+                    pending.append(comm.dist.isend(seg, dst=r + 1, group=comm.group))
+                else:
+                    comm.dist.send(seg.cpu(), dst=r + 1, group=comm.group)
+        for p_ in pending:
+            p_.wait()
+        if r < w - 1:
+            sums.zero_()
 
 
 # ------------------------------------------------------------------------------ the loop
@@ -715,8 +809,9 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
                        init_idx: np.ndarray | None = None, etr=None, timer: _Timer | None = None,
                        ws: Workspace | None = None, first_pass_done: bool = False) -> LoopOutput:
     """Device twin of core._fit_rotated.  ``data`` holds this rank's rows; ``n_global`` the
-    total across ranks.  ``init_rows`` (k, ld) are the Forgy rows gathered from all ranks."""
-    comm = comm or Comm()
+    total across ranks.  ``init_rows`` (k, ld) are the Forgy rows gathered from all ranks.
+    Without ``comm`` the rows are one process's (sharding is explicit: pass ``Comm()``)."""
+    comm = comm or Comm.local()
     dev = data.x.device
     n_local, d = data.n, data.d
     n = n_local if n_global is None else n_global
@@ -743,9 +838,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         timer.start("ground_truth")
         etr.setup(data, comm, n_global=n, row_lo=row_lo)
         timer.stop("ground_truth")
-    sums_buf = None
-    if comm.world > 1:
-        sums_buf = torch.empty(k * d + k, dtype=torch.float64, device=dev)
+    reducer = Reducer(comm, k, d, n, row_lo, n_local, dev, cfg.exact_reduce) if comm.world > 1 else None
     scal = torch.zeros(4, dtype=torch.float64, device=dev)
     pin_scal = torch.empty(4, dtype=torch.float64, pin_memory=True)
     pin_counts = torch.empty(k, dtype=torch.int32, pin_memory=True)
@@ -781,26 +874,26 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             if not cfg.pruning_sentinel:
                 work.seed_dims += n * d
         assign_stats(ws, n_local, it > 1)
-        # ---- one reduction of the iteration's scalars (packed) ----
-        scal[0] = ws.wcss[0]
-        scal[1] = ws.changed[0].to(torch.float64)
-        scal[2] = ws.counters[0].to(torch.float64)
-        scal[3] = ws.counters[1].to(torch.float64)
-        comm.allreduce_(scal)
+        # the update's stable cluster sort runs before the convergence test (it does not touch
+        # the centroids, so a converged stop is unaffected); its counts come back with the scalars
+        native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
+                    ptr(ws.sort_ws), ws.sort_ws.numel(), stream_handle(), nbytes=32.0 * data.n)
         sorted_counts = None
-        if comm.world == 1:
-            # one host synchronisation per iteration: the stable cluster sort of the update (it
-            # does not touch the centroids, so a converged stop below is unaffected) runs first and
-            # its counts come back together with the scalars
-            native.call("skm_cluster_sort", ptr(ws.assign), data.n, k, ptr(ws.order), ptr(ws.counts), ptr(ws.offsets),
-                        ptr(ws.sort_ws), ws.sort_ws.numel(), stream_handle(), nbytes=32.0 * data.n)
+        if reducer is None:
+            # one host synchronisation per iteration
+            scal[0] = ws.wcss[0]
+            scal[1] = ws.changed[0].to(torch.float64)
+            scal[2] = ws.counters[0].to(torch.float64)
+            scal[3] = ws.counters[1].to(torch.float64)
             pin_scal.copy_(scal, non_blocking=True)
             pin_counts.copy_(ws.counts, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
             wcss, ch, sv, td = pin_scal.tolist()
             sorted_counts = pin_counts.numpy().astype(np.int64)
         else:
-            wcss, ch, sv, td = scal.tolist()
+            # sums (computed before the convergence test, dropped if it stops the loop) + counts +
+            # scalars + tau buffer partials: the iteration's one collective and one host sync
+            sorted_counts, wcss, ch, sv, td = reducer.reduce(data, ws, n_local)
         if it > 1:
             n_changed = int(round(ch))
         if pruned_iter:
@@ -827,7 +920,11 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             terminated = "converged"
             break
         timer.start("update")
-        counts = update_centroids_device(data, cents, ws, comm, sums_buf, sorted_counts=sorted_counts)
+        if reducer is None:
+            counts = update_centroids_device(data, cents, ws, comm, sorted_counts=sorted_counts)
+        else:
+            reducer.finalize(cents, sorted_counts)
+            counts = sorted_counts
         have_order = True  # ws.order now lists rows grouped by their current assignment
         n_splits = apply_splits_device(cents, counts, rng_split) if cfg.split_empty else 0
         timer.stop("update")

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import native
-from .device import padded_ld, ptr, require_cuda, stream_handle
+from .device import on_device, padded_ld, ptr, require_cuda, stream_handle
 from .hostmath import etr_should_stop
 
 
@@ -157,6 +157,7 @@ class EtrState:
 
 
 # ------------------------------------------------------------------ host-array entry points
+@on_device
 def brute_force_topk(x, queries, k_gt: int, query_batch: int = 128, device=None) -> GroundTruth:
     """Exact top-k by squared L2 over the collection, ties to the lower index
     (evaluation.py:53-75), computed on the B200."""
@@ -178,6 +179,7 @@ def brute_force_topk(x, queries, k_gt: int, query_batch: int = 128, device=None)
     return GroundTruth(indices=gi.cpu().numpy().astype(np.int64), distances=gv.cpu().numpy(), k_gt=k_gt)
 
 
+@on_device
 def build_cluster_lists(assignments, k: int, device=None) -> list:
     """Per-cluster row lists in ascending row order (evaluation.py:78-83) from the device
     stable cluster sort."""
@@ -196,6 +198,7 @@ def build_cluster_lists(assignments, k: int, device=None) -> list:
     return np.split(o, bounds)
 
 
+@on_device
 def etr_probe(centroids, train_x, assignments, queries, gt: GroundTruth, nprobe: int, top_k: int,
               device=None) -> float:
     """Mean probe recall of the current state (evaluation.py:142-170), device tally."""
@@ -245,6 +248,7 @@ def _probe_ranking(centroids: np.ndarray, queries: np.ndarray, nprobe: int, dev)
     return pi
 
 
+@on_device
 def probe_eval(centroids, cluster_lists, x, queries, gt: GroundTruth, nprobe: int, top_ks=(10, 100),
                device=None) -> dict:
     """IVF probe-search quality (evaluation.py:173-203): recall@t for each t <= gt.k_gt and the
@@ -293,6 +297,7 @@ def probe_eval(centroids, cluster_lists, x, queries, gt: GroundTruth, nprobe: in
     return out
 
 
+@on_device
 def ivf_probe_search(centroids, cluster_lists, x, q, nprobe: int, top_k: int, device=None):
     """Scan the nprobe clusters nearest to one query (evaluation.py:86-105).  Returns
     (indices int64, squared distances float32, vectors_explored); ties resolve to the lower
@@ -339,6 +344,7 @@ def recall_at_k(result_ids, gt_row, k: int) -> float:
     return np.intersect1d(result_ids[:k], gt_row[:k]).size / k
 
 
+@on_device
 def wcss(x, centroids, assignments, batch: int = 4096, device=None) -> float:
     """Sum of squared distances to the assigned centroids in double (evaluation.py:205-215),
     on the B200 (deterministic fixed-order reduction)."""

@@ -9,10 +9,11 @@ import torch
 
 from . import native
 from .config import DimensionMismatch, NormCache, RotationMatrix
-from .device import ptr, require_cuda, stream_handle
+from .device import on_device, ptr, require_cuda, stream_handle
 from .hostmath import SPLIT_EPS, init_indices, plan_splits, sample_indices
 
 
+@on_device
 def apply_rotation(x: np.ndarray, rotation: RotationMatrix, device=None) -> np.ndarray:
     """x @ R on the tensor cores (3xTF32)."""
     from .api import DeviceRotation, _h2d
@@ -23,6 +24,7 @@ def apply_rotation(x: np.ndarray, rotation: RotationMatrix, device=None) -> np.n
     return rot.apply(_h2d(np.ascontiguousarray(x, dtype=np.float32), dev))[:, :rotation.dim].cpu().numpy()
 
 
+@on_device
 def unapply_rotation(x: np.ndarray, rotation: RotationMatrix, device=None) -> np.ndarray:
     from .api import DeviceRotation, _h2d
     if x.shape[1] != rotation.dim:
@@ -51,6 +53,7 @@ def _row_norms_dev(x: np.ndarray, dims: int, dev) -> np.ndarray:
     return out[: x.shape[0]].cpu().numpy()
 
 
+@on_device
 def compute_norms(m: np.ndarray, d_prime: int, device=None) -> NormCache:
     if not 0 < d_prime <= m.shape[1]:
         raise DimensionMismatch(f"d_prime {d_prime} out of range for dim {m.shape[1]}")
@@ -59,6 +62,7 @@ def compute_norms(m: np.ndarray, d_prime: int, device=None) -> NormCache:
                      d_prime=d_prime)
 
 
+@on_device
 def update_centroids(x: np.ndarray, assignments: np.ndarray, k: int, prev_centroids: np.ndarray | None = None,
                      kernel_impl=None, device=None):
     """Per-cluster means with ordered f64 sums on the device; empties keep their previous
@@ -83,6 +87,7 @@ def update_centroids(x: np.ndarray, assignments: np.ndarray, k: int, prev_centro
     return Cd[:, :d].cpu().numpy().copy(), counts.cpu().numpy().astype(np.int64)
 
 
+@on_device
 def split_empty_clusters(centroids: np.ndarray, counts: np.ndarray, rng, device=None):
     """In-place split of donors into empty clusters (host RNG, device row arithmetic)."""
     from .api import _h2d

@@ -95,6 +95,7 @@ _SIGS = {
     "skm_dense_argmin": ([_vp, _ll, _i, _i, _vp, _vp, _vp, _vp], _i),
     "skm_exact_pair_dist": ([_vp, _ll, _vp, _ll, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _vp], _i),
     "skm_max_f32": ([_vp, _i, _vp, _vp], _i),
+    "skm_tau_chunk_sums": ([_vp, _ll, _vp, _vp], _i),
     "skm_argmin_candidates": ([_vp, _i, _vp, _vp, _vp, _f, _vp, _vp, _vp], _i),
     "skm_cand_exact_argmin": ([_vp, _i, _vp, _vp, _i, _vp, _ll, _vp, _ll, _i, _vp, _vp, _i, _i, _vp, _vp, _vp], _i),
     "skm_chain_gemm": ([C.POINTER(ChainParams), _vp], _i),

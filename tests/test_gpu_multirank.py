@@ -1,11 +1,13 @@
 """Row-sharded data-parallel fit on the real device path with world size 2.
 
 Only one GPU is available to this build, so both ranks share cuda:0 and talk over gloo
-(which accepts CUDA tensors); the device kernels, the sharded update (ordered partial sums ->
-packed allreduce -> finalize), the Forgy-row / ETR-query assembly, the sharded ETR ground
-truth (per-rank top-k -> allgather -> stable merge) and the integer hit tally all run exactly
-as under NCCL.  Result must match the single-process fit: integer outputs equal, centroids
-equal up to the f64 summation order of the cross-rank reduction."""
+(which accepts CUDA tensors for collectives; point-to-point sends are staged through the host);
+the device kernels, the sharded update (rank-ordered chained f64 sums or per-rank partials, then
+the iteration's one packed allreduce -> finalize), the Forgy-row / ETR-query assembly, the sharded
+ETR ground truth (per-rank top-k -> allgather -> stable merge) and the integer hit tally all run
+exactly as under NCCL.  With the default exact_reduce the result is bitwise the single-process fit
+(assignments, every per-iteration stat incl. wcss, centroids); with exact_reduce=False the integer
+outputs must still match and the centroids equal up to the f64 association of the reduction."""
 
 import os
 
@@ -17,65 +19,87 @@ from conftest import make_blobs
 pytestmark = pytest.mark.gpu
 
 
-def _run(rank, world, port, q, etr):
+def _run(rank, world, port, q, etr, exact, public):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        import paper_2603_20009_b200 as skb
         from paper_2603_20009_b200 import api
         from paper_2603_20009_b200.config import EtrConfig, KMeansConfig
         from paper_2603_20009_b200.engine import Comm
         from paper_2603_20009_b200.hostmath import generate_rotation
         torch.cuda.set_device(0)
-        x = make_blobs(12000, 128, 200, seed=3, spread=4.0)
+        x = make_blobs(40000, 128, 200, seed=3, spread=4.0)
         n, d = x.shape
+        cfg = KMeansConfig(k=100, max_iters=8, seed=1, exact_reduce=exact,
+                           etr=EtrConfig(n_queries=300, top_k=10) if etr else None)
+        if public:  # the drop-in entry under an initialised process group shards by itself
+            res = skb.fit(x, cfg)
+            st = res.stats
+            q.put((rank, {"assign": res.assignments, "lo": 0, "cent": res.centroids,
+                          "dp": [s.d_prime for s in st], "changed": [s.n_changed for s in st],
+                          "surv": [s.survivors for s in st], "wcss": [s.wcss for s in st],
+                          "recall": res.recall_history, "term": res.terminated_by}))
+            return
         comm = Comm()
         lo, hi = comm.shard(n)
-        cfg = KMeansConfig(k=100, max_iters=8, seed=1,
-                           etr=EtrConfig(n_queries=300, top_k=10) if etr else None)
         xd = api._h2d(x[lo:hi], torch.device("cuda", 0))
         res = api.fit_device(xd, d, cfg, generate_rotation(d, 1), comm=comm, n_global=n, row_lo=lo)
         st = res.loop.stats
         q.put((rank, {"assign": res.loop.assignments, "lo": lo,
                       "cent": res.centroids_dev[:, :d].cpu().numpy(),
                       "dp": [s.d_prime for s in st], "changed": [s.n_changed for s in st],
-                      "surv": [s.survivors for s in st], "recall": res.loop.recall_history,
-                      "term": res.loop.terminated_by}))
-    except Exception as e:  # pragma: no cover
+                      "surv": [s.survivors for s in st], "wcss": [s.wcss for s in st],
+                      "recall": res.loop.recall_history, "term": res.loop.terminated_by}))
+    except Exception:  # pragma: no cover
         import traceback
         q.put((rank, traceback.format_exc()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("etr", [False, True])
-def test_two_ranks_match_single_rank(etr):
+def _spawn(world, port, fn, args):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=fn, args=(r, world, port, q) + args) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in ps:
+        p.join(timeout=120)
+    for r, v in res.items():
+        assert isinstance(v, dict), v
+    return res
+
+
+@pytest.mark.parametrize("etr,exact,public", [(False, True, False), (True, True, False), (False, False, False),
+                                              (False, True, True)])
+def test_two_ranks_match_single_rank(etr, exact, public):
     outs = {}
     for world in (1, 2):
-        q = ctx.Queue()
-        port = 29600 + world + (os.getpid() % 500) + (100 if etr else 0)
-        ps = [ctx.Process(target=_run, args=(r, world, port, q, etr)) for r in range(world)]
-        for p in ps:
-            p.start()
-        res = dict(q.get(timeout=600) for _ in range(world))
-        for p in ps:
-            p.join(timeout=120)
-        for r, v in res.items():
-            assert isinstance(v, dict), v
-        outs[world] = res
+        port = 29600 + world + (os.getpid() % 400) + (100 if etr else 0) + (30 if exact else 0) + (60 if public else 0)
+        outs[world] = _spawn(world, port, _run, (etr, exact, public))
     one = outs[1][0]
     two = outs[2]
-    a2 = np.concatenate([two[r]["assign"] for r in sorted(two, key=lambda r: two[r]["lo"])])
-    assert np.array_equal(a2, one["assign"])
+    if public:
+        for r in two:
+            assert np.array_equal(two[r]["assign"], one["assign"])
+    else:
+        a2 = np.concatenate([two[r]["assign"] for r in sorted(two, key=lambda r: two[r]["lo"])])
+        assert np.array_equal(a2, one["assign"])
     for r in two:
         for key in ("dp", "changed", "surv", "recall", "term"):
             assert two[r][key] == one[key], key
-        rel = np.linalg.norm(two[r]["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
-        assert rel <= 1e-6, rel
+        if exact:  # rank-ordered sums + buffer-aligned shards: the 1-GPU result bit for bit
+            assert two[r]["wcss"] == one["wcss"]
+            assert np.array_equal(two[r]["cent"], one["cent"])
+        else:
+            rel = np.linalg.norm(two[r]["cent"] - one["cent"]) / np.linalg.norm(one["cent"])
+            assert rel <= 1e-6, rel
     assert np.array_equal(two[0]["cent"], two[1]["cent"])  # replicas stay identical
 
 
