@@ -63,11 +63,41 @@ def _norms(x: torch.Tensor, dims: int) -> torch.Tensor:
     return out
 
 
+TOPK_MAX = 2048  # csrc/topk.cuh
+
+
+def merge_topk_shards(all_i: torch.Tensor, all_v: torch.Tensor, shards: int, kk: int, nq: int, k_out: int):
+    """Stable (distance, index) merge of per-shard sorted top-k lists [shard][query][kk]; the
+    device merge takes up to 8 lists at a time, so more shards merge in rounds."""
+    dev = all_i.device
+    while shards > 1:
+        groups = []
+        for g0 in range(0, shards, 8):
+            g = min(8, shards - g0)
+            gi = torch.empty((nq, kk), dtype=torch.int32, device=dev)  # the merge keeps the lists' width
+            gv = torch.empty((nq, kk), dtype=torch.float32, device=dev)
+            native.call("skm_topk_merge", ptr(all_i[g0:g0 + g].contiguous()), ptr(all_v[g0:g0 + g].contiguous()), g,
+                        kk, nq, ptr(gi), ptr(gv), stream_handle())
+            groups.append((gi, gv))
+        if len(groups) == 1:
+            all_i, all_v = groups[0][0][None], groups[0][1][None]
+            break
+        all_i = torch.stack([g_[0] for g_ in groups]).contiguous()
+        all_v = torch.stack([g_[1] for g_ in groups]).contiguous()
+        shards = len(groups)
+    return all_i[0, :, :k_out].contiguous(), all_v[0, :, :k_out].contiguous()
+
+
 def device_topk_distances(q: torch.Tensor, q_hi, q_lo, q_sq, x: torch.Tensor, x_hi, x_lo, x_sq, d: int, k: int,
                           col_offset: int = 0, max_bytes: int = 1 << 30) -> tuple[torch.Tensor, torch.Tensor]:
     """Exact top-k rows of x for each query (squared L2 via the expansion identity, stable
-    ties).  Returns (idx int32 (nq, k) with col_offset added, dist float32 (nq, k))."""
-    from .engine import _gemm, _n_split
+    ties).  Returns (idx int32 (nq, k) with col_offset added, dist float32 (nq, k)).
+
+    The distance block is the reference's own bits (evaluation.py:42-50 multiplies with numpy
+    ``@``: OpenBLAS sgemm) -- the exact fma chain with 448-wide K blocks of csrc/sgemm_chain.cuh --
+    so the ranks, ties and the stable order equal brute_force_topk / the probe ranking exactly.
+    (q_hi / q_lo / x_hi / x_lo: unused, kept for callers of the tensor-core version.)"""
+    from .engine import GEMM_Q, chain_gemm
     nq, n = q.shape[0], x.shape[0]
     dev = q.device
     kk = min(k, n)
@@ -79,10 +109,14 @@ def device_topk_distances(q: torch.Tensor, q_hi, q_lo, q_sq, x: torch.Tensor, x_
     for s in range(0, nq, qb):
         e = min(nq, s + qb)
         D = torch.empty((e - s, padded_ld(n)), dtype=torch.float32, device=dev)
-        _gemm(q_hi[s:e], q_lo[s:e], x_hi, x_lo, e - s, n, d, native.GEMM_DIST, out=D, xsq=q_sq[s:e], ysq=x_sq,
-              n_split=_n_split(e - s, n))
-        native.call("skm_topk_rows", ptr(D), D.stride(0), e - s, n, kk, ptr(out_i[s:e]), ptr(out_v[s:e]), kk,
-                    col_offset, stream_handle(), nbytes=5.0 * 4 * (e - s) * n)
+        chain_gemm(q[s:e], x, e - s, n, d, D, 0, GEMM_Q, xsq=q_sq[s:e], ysq=x_sq)
+        if kk <= TOPK_MAX:
+            native.call("skm_topk_rows", ptr(D), D.stride(0), e - s, n, kk, ptr(out_i[s:e]), ptr(out_v[s:e]), kk,
+                        col_offset, stream_handle(), nbytes=5.0 * 4 * (e - s) * n)
+        else:  # beyond the radix-select kernel's k: a stable device sort of the rows (same order)
+            v, i = torch.sort(D[:, :n], dim=1, stable=True)
+            out_v[s:e] = v[:, :kk]
+            out_i[s:e] = (i[:, :kk] + col_offset).to(torch.int32)
     return out_i, out_v
 
 
@@ -113,13 +147,12 @@ class EtrState:
             q[torch.tensor(mine, dtype=torch.int64, device=dev)] = tmp
         comm.allreduce_(q)
         self.q = q
-        self.q_hi, self.q_lo = _split(q, data.d)
         self.q_sq = _norms(q, data.d)
         top_k = self.top_k
         if top_k > n:
             raise ValueError(f"k_gt={top_k} exceeds collection size {n}")
-        gi, gv = device_topk_distances(q, self.q_hi, self.q_lo, self.q_sq, data.x, data.hi, data.lo,
-                                       data.norms(data.d), data.d, top_k, col_offset=row_lo)
+        gi, gv = device_topk_distances(q, None, None, self.q_sq, data.x, None, None, data.norms(data.d), data.d, top_k,
+                                       col_offset=row_lo)
         if comm.world > 1:
             # per-rank top-k -> allgather -> stable (dist, index) merge
             kk = gi.shape[1]
@@ -127,21 +160,15 @@ class EtrState:
             av = [torch.empty_like(gv) for _ in range(comm.world)]
             comm.dist.all_gather(ai, gi.contiguous(), group=comm.group)
             comm.dist.all_gather(av, gv.contiguous(), group=comm.group)
-            all_i = torch.stack(ai).contiguous()
-            all_v = torch.stack(av).contiguous()
-            gi = torch.empty((nq, top_k), dtype=torch.int32, device=dev)
-            gv = torch.empty((nq, top_k), dtype=torch.float32, device=dev)
-            native.call("skm_topk_merge", ptr(all_i), ptr(all_v), comm.world, kk, nq, ptr(gi), ptr(gv),
-                        stream_handle())
+            gi, gv = merge_topk_shards(torch.stack(ai).contiguous(), torch.stack(av).contiguous(), comm.world, kk, nq,
+                                       top_k)
         self.gt_idx, self.gt_val = gi.contiguous(), gv.contiguous()
         self.hits = torch.zeros(nq, dtype=torch.int32, device=dev)
 
     def probe(self, data, cents, ws, comm) -> float:
         nq = self.q.shape[0]
-        c_hi, c_lo = _split(cents.c, cents.d)
         c_sq = _norms(cents.c, cents.d)
-        pi, _ = device_topk_distances(self.q, self.q_hi, self.q_lo, self.q_sq, cents.c, c_hi, c_lo, c_sq, cents.d,
-                                      self.nprobe)
+        pi, _ = device_topk_distances(self.q, None, None, self.q_sq, cents.c, None, None, c_sq, cents.d, self.nprobe)
         native.call("skm_etr_hits", ptr(self.gt_idx), self.gt_idx.shape[1], self.top_k, ptr(pi), pi.shape[1],
                     pi.shape[1], ptr(ws.assign), self.row_lo, self.row_hi, cents.k, nq, ptr(self.hits),
                     stream_handle())
@@ -173,9 +200,7 @@ def brute_force_topk(x, queries, k_gt: int, query_batch: int = 128, device=None)
     d = x.shape[1]
     X = _h2d(x, dev)
     Q = _h2d(queries, dev)
-    xh, xl = _split(X, d)
-    qh, ql = _split(Q, d)
-    gi, gv = device_topk_distances(Q, qh, ql, _norms(Q, d), X, xh, xl, _norms(X, d), d, k_gt)
+    gi, gv = device_topk_distances(Q, None, None, _norms(Q, d), X, None, None, _norms(X, d), d, k_gt)
     return GroundTruth(indices=gi.cpu().numpy().astype(np.int64), distances=gv.cpu().numpy(), k_gt=k_gt)
 
 
@@ -209,9 +234,7 @@ def etr_probe(centroids, train_x, assignments, queries, gt: GroundTruth, nprobe:
     k, d = c.shape
     nprobe = min(max(1, nprobe), k)
     Cd, Qd = _h2d(c, dev), _h2d(q, dev)
-    ch, cl = _split(Cd, d)
-    qh, ql = _split(Qd, d)
-    pi, _ = device_topk_distances(Qd, qh, ql, _norms(Qd, d), Cd, ch, cl, _norms(Cd, d), d, nprobe)
+    pi, _ = device_topk_distances(Qd, None, None, _norms(Qd, d), Cd, None, None, _norms(Cd, d), d, nprobe)
     gt_i = torch.from_numpy(np.ascontiguousarray(gt.indices[:, :top_k], dtype=np.int32)).to(dev)
     A = torch.from_numpy(np.ascontiguousarray(assignments, dtype=np.int32)).to(dev)
     hits = torch.zeros(q.shape[0], dtype=torch.int32, device=dev)
@@ -242,9 +265,7 @@ def _probe_ranking(centroids: np.ndarray, queries: np.ndarray, nprobe: int, dev)
     k, d = centroids.shape
     Cd, Qd = _h2d(np.ascontiguousarray(centroids, dtype=np.float32), dev), _h2d(
         np.ascontiguousarray(queries, dtype=np.float32), dev)
-    ch, cl = _split(Cd, d)
-    qh, ql = _split(Qd, d)
-    pi, _ = device_topk_distances(Qd, qh, ql, _norms(Qd, d), Cd, ch, cl, _norms(Cd, d), d, nprobe)
+    pi, _ = device_topk_distances(Qd, None, None, _norms(Qd, d), Cd, None, None, _norms(Cd, d), d, nprobe)
     return pi
 
 
@@ -315,8 +336,6 @@ def ivf_probe_search(centroids, cluster_lists, x, q, nprobe: int, top_k: int, de
     if cand.size == 0:
         return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float32), 0
     take = min(top_k, cand.size)
-    if take > 2048:
-        raise NotImplementedError("ivf_probe_search: top_k > 2048 is not supported by the device top-k")
     # candidates in ascending row order: column ties in the device top-k then resolve to the
     # lower row index, as the reference's lexsort((cand, d2)) does
     srt = np.sort(cand)
@@ -331,7 +350,12 @@ def ivf_probe_search(centroids, cluster_lists, x, q, nprobe: int, top_k: int, de
     _gemm(qh, ql, xh, xl, 1, m, d, native.GEMM_DIST, out=D, xsq=_norms(Q, d), ysq=_norms(X, d))
     oi = torch.empty((1, take), dtype=torch.int32, device=dev)
     ov = torch.empty((1, take), dtype=torch.float32, device=dev)
-    native.call("skm_topk_rows", ptr(D), D.stride(0), 1, m, take, ptr(oi), ptr(ov), take, 0, stream_handle())
+    if take <= TOPK_MAX:
+        native.call("skm_topk_rows", ptr(D), D.stride(0), 1, m, take, ptr(oi), ptr(ov), take, 0, stream_handle())
+    else:
+        v, i = torch.sort(D[:, :m], dim=1, stable=True)
+        ov.copy_(v[:, :take])
+        oi.copy_(i[:, :take].to(torch.int32))
     cols = oi[0].cpu().numpy().astype(np.int64)
     return srt[cols], ov[0].cpu().numpy(), int(cand.size)
 

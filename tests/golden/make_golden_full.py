@@ -38,7 +38,17 @@ FULL_CASES = {
     "c1": ("blobs", (100_000, 128, 256, 0), dict(k=256, max_iters=10, seed=0), 1, 1),
     "c2": ("skewed", (1_000_000, 1536, 8192, 0), dict(k=4096, max_iters=10, seed=0), 10, 8),
     "c4k1024": ("skewed", (1_000_000, 768, 2048, 0), dict(k=1024, max_iters=10, seed=0), 10, 4),
+    # BASELINE c3: ETR on 1000 queries, recall@10; "etr" = (n_queries, top_k)
+    "c3": ("skewed", (1_000_000, 1024, 32768, 0), dict(k=16384, max_iters=25, seed=0, etr=(1000, 10)), 10, 16),
 }
+
+
+def make_config(kw):
+    kw = dict(kw)
+    if "etr" in kw:
+        nq, top_k = kw.pop("etr")
+        kw["etr"] = skm.EtrConfig(n_queries=nq, top_k=top_k)
+    return skm.KMeansConfig(**kw)
 
 
 def make_input(name):
@@ -51,7 +61,7 @@ def run(name):
     t0 = time.perf_counter()
     x = make_input(name)
     t_gen = time.perf_counter() - t0
-    cfg = skm.KMeansConfig(**kw)
+    cfg = make_config(kw)
     snaps = []
 
     def inspect(it, ctx):
@@ -90,6 +100,7 @@ def run(name):
         cent_norms=np.linalg.norm(res.centroids.astype(np.float64), axis=1),
         cent_sum=res.centroids.astype(np.float64).sum(axis=0),
         dpf=np.int64(-1 if res.d_prime_final is None else res.d_prime_final),
+        recall=np.array(res.recall_history),
     )
     import threadpoolctl
     meta = dict(case=name, generator=gen, args=args, config=kw, cpu_count=os.cpu_count(),

@@ -36,11 +36,9 @@ def test_brute_force_topk_matches_oracle():
     q = x[np.random.default_rng(1).choice(20000, 200, replace=False)]
     gt = skb.brute_force_topk(x, q, 10)
     oi, od = skm_ref.brute_force_topk(x, q, 10)
-    agree = np.mean(gt.indices == oi)
-    assert agree >= 0.999, agree  # distance near-ties between GEMMs may swap neighbours
-    # expansion identity: absolute error floor ~ ulp(|q|^2 + |x|^2) (cancellation at d2 ~ 0)
-    floor = 4e-6 * (np.sum(q.astype(np.float64) ** 2, axis=1)[:, None] + np.sum(x[gt.indices].astype(np.float64) ** 2, axis=2))
-    assert np.all(np.abs(gt.distances - od) <= 1e-5 * od + floor)
+    # the distance block is the exact sgemm chain + expansion: neighbours and distances bitwise
+    assert np.array_equal(gt.indices, oi)
+    assert np.array_equal(gt.distances, od)
 
 
 def test_etr_probe_equals_reference_formula():
@@ -64,10 +62,9 @@ def test_hierarchical_matches_reference():
     x = make_blobs(6000, 128, 50, seed=31, spread=5.0, noise=0.8)
     h = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=120, seed=2))
     assert h.k == int(g["hier_k"])
-    agree = float(np.mean(h.assignments == g["hier_assign"]))
-    assert agree >= 0.999, agree
-    rel = np.linalg.norm(h.centroids - g["hier_centroids"]) / np.linalg.norm(g["hier_centroids"])
-    assert rel <= 1e-3, rel
+    # meso loop and every group loop reproduce the reference bit for bit
+    assert np.array_equal(h.assignments, g["hier_assign"])
+    assert np.array_equal(h.centroids, g["hier_centroids"])
 
 
 def test_hierarchical_wide_matches_reference():
@@ -78,10 +75,9 @@ def test_hierarchical_wide_matches_reference():
     x = make_skewed_blobs(20000, 1024, 300, 29)
     h = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=400, seed=6))
     assert h.k == int(g["hierw_k"])
-    agree = float(np.mean(h.assignments == g["hierw_assign"]))
-    assert agree >= 0.999, agree
-    rel = np.linalg.norm(h.centroids - g["hierw_centroids"]) / np.linalg.norm(g["hierw_centroids"])
-    assert rel <= 1e-3, rel
+    # meso loop and every group loop reproduce the reference bit for bit
+    assert np.array_equal(h.assignments, g["hierw_assign"])
+    assert np.array_equal(h.centroids, g["hierw_centroids"])
 
 
 def test_hierarchical_concurrent_groups_bitwise_equal_serial(monkeypatch):
@@ -132,8 +128,10 @@ def test_probe_eval_and_ivf_search_vs_reference(case, n, d, centers, k, seed):
         r = skb.probe_eval(cents, lists, x, queries, gt, nprobe, top_ks=(10, 100))
         for t in (10, 100):
             want = float(P[f"{key}_np{nprobe}_r{t}"])
-            assert abs(r[f"recall_at_{t}"] - want) <= 0.005, (nprobe, t, r, want)
-            assert abs(r[f"recall_at_{t}"] - want) <= 2.0 / (t * queries.shape[0])  # at most ~1 near-tie
+            # exact probe ranking + integer tally; the reference ranks each query's candidates with
+            # a GEMV (numpy (1, d) @ (d, m): OpenBLAS sgemv, another summation order), so a distance
+            # near-tie at position t can move one hit
+            assert abs(r[f"recall_at_{t}"] - want) <= 1.0 / (t * queries.shape[0]) + 1e-12, (nprobe, t, r, want)
         assert r["vectors_explored_mean"] == float(P[f"{key}_np{nprobe}_explored"])
     for qi in range(5):
         ids, dist, ex = skb.ivf_probe_search(cents, lists, x, queries[qi], 3, 20)

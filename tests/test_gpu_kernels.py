@@ -357,3 +357,30 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_
     assert np.array_equal(tau.cpu().numpy(), tau_o)
     assert (sv, td) == (surv_o, td_o)
     assert ch_ == int(np.count_nonzero(a_o != prev))
+
+
+def test_topk_merge_many_shards_and_wide_k():
+    """More than 8 shards merge in rounds; k beyond the radix-select kernel uses a stable device
+    sort: both equal a stable argsort of the concatenated distances."""
+    from paper_2603_20009_b200.etr import device_topk_distances, merge_topk_shards
+    rng = np.random.default_rng(12)
+    nq, shards, kk = 37, 13, 10
+    vals = np.round(rng.random((shards, nq, 50)) * 20).astype(np.float32)  # many exact ties
+    ids = np.arange(shards * 50).reshape(shards, 1, 50).repeat(nq, 1).astype(np.int32)
+    o = np.argsort(vals, axis=2, kind="stable")[:, :, :kk]
+    si = np.take_along_axis(ids, o, 2)
+    sv = np.take_along_axis(vals, o, 2)
+    gi, gv = merge_topk_shards(torch.tensor(si, device="cuda"), torch.tensor(sv, device="cuda"), shards, kk, nq, kk)
+    flat_v = vals.transpose(1, 0, 2).reshape(nq, -1)
+    flat_i = ids.transpose(1, 0, 2).reshape(nq, -1)
+    want = np.argsort(flat_v, axis=1, kind="stable")[:, :kk]
+    assert np.array_equal(gi.cpu().numpy(), np.take_along_axis(flat_i, want, 1))
+    assert np.array_equal(gv.cpu().numpy(), np.take_along_axis(flat_v, want, 1))
+    x = rng.standard_normal((5000, 16)).astype(np.float32)
+    q = rng.standard_normal((3, 16)).astype(np.float32)
+    X, Q = _pad(x), _pad(q)
+    xs, qs = _dev().row_sq_norms(X, 16), _dev().row_sq_norms(Q, 16)
+    i1, v1 = device_topk_distances(Q, None, None, qs, X, None, None, xs, 16, 3000)
+    d2 = ((q.astype(np.float64)[:, None, :] - x[None].astype(np.float64)) ** 2).sum(-1)
+    agree = np.mean(i1.cpu().numpy()[:, :2000] == np.argsort(d2, axis=1, kind="stable")[:, :2000])
+    assert agree > 0.99 and np.all(np.diff(v1.cpu().numpy(), axis=1) >= 0)

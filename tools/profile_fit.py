@@ -23,10 +23,14 @@ ap.add_argument("--k", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--centers", type=int, default=8192)
+ap.add_argument("--device-data", action="store_true", help="device-generated rows (same distribution, fast)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
-# the reference's generator (c2 rows when --n 1000000): bench.py's data
-x = to_device_matrix(make_skewed_blobs(a.n, a.d, a.centers, 0))
+if a.device_data:
+    from paper_2603_20009_b200.synth import make_shard_device
+    x = make_shard_device(a.n, a.d, a.centers, 0, a.n, 0, dev)
+else:  # the reference's generator (c2 rows when --n 1000000): bench.py's data
+    x = to_device_matrix(make_skewed_blobs(a.n, a.d, a.centers, 0))
 cfg = KMeansConfig(k=a.k, max_iters=a.iters, seed=0)
 rot = generate_rotation(a.d, 0)
 from paper_2603_20009_b200 import profiling  # noqa: E402
