@@ -158,6 +158,7 @@ typedef struct skm_chain_params {
   int mode;                    /* 0 store, 1 distance */
   float* out; long long ldo;
   const float* xsq; const float* ysq;
+  int b_kmajor;                /* 0: b is [N][K] (b[j][t]); 1: b is [K][N] (b[t][j], e.g. R for x @ R) */
 } skm_chain_params;
 int skm_chain_gemm(const skm_chain_params* p, void* stream);
 

@@ -113,7 +113,9 @@ class DeviceRotation:
                       n_split=_store_split(m, self.d))
                 del x_lo
             else:
-                chain_gemm(x_dev[r0:r0 + m], self.r if inverse else self.rt, m, self.d, self.d, dst, 0, GEMM_Q)
+                # k-major operand: x @ R reads R's rows, x @ R^T the rows of R^T
+                chain_gemm(x_dev[r0:r0 + m], self.rt if inverse else self.r, m, self.d, self.d, dst, 0, GEMM_Q,
+                           b_kmajor=True)
             if inplace:
                 out[r0:r0 + m].copy_(dst)
         return out

@@ -88,6 +88,9 @@ struct ScanArgs {
   long long ldc;
   int chain_flavour;       // 0 fma chain with K blocks of chain_q (OpenBLAS), 1 mul+add (portable)
   int chain_q;
+  // 1: the row's d' front and the centroid fronts of the re-evaluated candidates are staged in the
+  // warp's shared memory (scan_dyn_smem(nb, d', true)) and re-evaluated there; 0: from global
+  int ex_stage;
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -204,6 +207,50 @@ __device__ __noinline__ float exact_front_dist(const float* __restrict__ xr, con
   return e > 0.0f ? e : 0.0f;
 }
 
+// exact_dot on shared-memory operands: the same chains (K blocks of q, ascending t), with the
+// operands of 16 steps loaded ahead of their fma chain so the chain runs at fma latency.
+template <int FLAVOUR>
+__device__ __forceinline__ float exact_dot_staged(const float* __restrict__ x, const float* __restrict__ y, int K,
+                                                  int q) {
+  float tot = 0.0f;
+  int k0 = 0;
+  while (k0 < K) {
+    const int k1 = chain_next_boundary(k0, K, q);
+    float acc = 0.0f;
+    int t = k0;
+    if ((k0 & 3) == 0) {
+      for (; t + 16 <= k1; t += 16) {
+        float4 u[4], v[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          u[h] = *reinterpret_cast<const float4*>(x + t + 4 * h);
+          v[h] = *reinterpret_cast<const float4*>(y + t + 4 * h);
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          acc = chain_scalar_step<FLAVOUR>(u[h].x, v[h].x, acc);
+          acc = chain_scalar_step<FLAVOUR>(u[h].y, v[h].y, acc);
+          acc = chain_scalar_step<FLAVOUR>(u[h].z, v[h].z, acc);
+          acc = chain_scalar_step<FLAVOUR>(u[h].w, v[h].w, acc);
+        }
+      }
+    }
+    for (; t < k1; ++t) acc = chain_scalar_step<FLAVOUR>(x[t], y[t], acc);
+    tot = __fadd_rn(tot, acc);
+    k0 = k1;
+  }
+  return tot;
+}
+
+__device__ __noinline__ float exact_front_dist_staged(const float* __restrict__ xr, const float* __restrict__ cr,
+                                                      int dp, int flavour, int q, float xs, float ys) {
+  const float ip = flavour == 0 ? exact_dot_staged<CHAIN_FMA>(xr, cr, dp, q) : exact_dot_staged<CHAIN_MULADD>(xr, cr, dp, 0);
+  const float e = __fadd_rn(__fadd_rn(__fmul_rn(ip, -2.0f), xs), ys);
+  return e > 0.0f ? e : 0.0f;
+}
+
+constexpr int SCAN_EXS = 2;  // centroid fronts staged per cooperative re-evaluation round
+
 #ifndef SKM_SCAN_MINB
 #define SKM_SCAN_MINB 3  // 12 warps per SM: caps registers at 168 (the exact-chain call site raised it to 231)
 #endif
@@ -228,8 +275,12 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
   }
   __syncthreads();
 
-  float* xsm = scan_smem + static_cast<long long>(warp) * (64 * nb + SCAN_WINDOW * nb);
+  const int dpp = (a.d_prime + 3) & ~3;
+  const bool ex_stage = a.ex_stage != 0;
+  float* xsm = scan_smem + static_cast<long long>(warp) * (64 * nb + SCAN_WINDOW * nb + (ex_stage ? (1 + SCAN_EXS) * dpp : 0));
   float* rec = xsm + 64 * nb;
+  float* xfs = rec + SCAN_WINDOW * nb;  // ex_stage: the row's d' front columns
+  float* cfs = xfs + dpp;               // ex_stage: SCAN_EXS staged centroid fronts
   ScanWarpSmem& W = wsm[warp];
   const float4* xsm4 = reinterpret_cast<const float4*>(xsm);
   const int tail_dims = s_bdcum[nb];
@@ -272,6 +323,17 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
       for (int u = lane; u < 64 * nb; u += 32) {
         const int b = u >> 6, t = u & 63;
         xsm[((t >> 2) * nb + b) * 4 + (t & 3)] = (u < tail_dims) ? xrow[u] : 0.0f;
+      }
+    }
+    if (ex_stage) {  // the d' front (read only by exact re-evaluations)
+      const float* xf = a.x + row * a.ldx;
+      if (x_aligned) {
+        for (int c = lane; c < dpp / 4; c += 32) {
+          const int valid = min(4, a.d_prime - 4 * c);
+          cp_async_16_zfill(xfs + 4 * c, xf + 4 * c, 4 * valid);
+        }
+      } else {
+        for (int u = lane; u < dpp; u += 32) xfs[u] = u < a.d_prime ? xf[u] : 0.0f;
       }
     }
     float tcur = a.tau[row];
@@ -416,6 +478,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         int st = ST_NOTSURV;  // lanes beyond D: neutral
         float run = 0.0f, run_hi = 0.0f;
         int pb = 0, j = 0;
+        bool need_exact = false;
         if (p < D) {
           const int qs = p % SCAN_WINDOW;
           st = W.qstat[qs];
@@ -439,22 +502,64 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             // an unsettled outcome, or an inexact candidate that may replace the best (its
             // running sum would become tau): recompute p with the reference's chain, walk exactly
             const bool may_improve = st == ST_COMPLETE && (run < tcur || (run == tcur && j < best));
-            if (st == ST_AMBIG || (may_improve && W.qdl[qs] > 0.0f)) {
-              const float pe = SKM_EXF(a.x + row * a.ldx, a.cent + static_cast<long long>(j) * a.ldc,
-                                                a.d_prime, a.chain_flavour, a.chain_q, xs_row, __ldg(a.ysq + j));
-              W.qp[qs] = pe;
-              W.qdl[qs] = 0.0f;
-              st = walk_interval(pe, 0.0f, rec + qs * nb, W.qdone[qs], nb, tcur, f0, s_theta, pb, run, run_hi);
-              if (st != ST_PENDING) {
-                W.qstat[qs] = st;
-                W.qpb[qs] = pb;
-                W.qrun[qs] = run;
-                W.qrunhi[qs] = run;
-                W.qver[qs] = ver;
-              }
-              ++exact_acc;
-            }
+            need_exact = st == ST_AMBIG || (may_improve && W.qdl[qs] > 0.0f);
           }
+        }
+        float pe = 0.0f;
+        if (ex_stage) {
+          // warp-cooperative: the fronts of up to SCAN_EXS candidates are copied into the warp's
+          // shared memory by all lanes (coalesced), then their lanes run the chains side by side
+          unsigned needm = __ballot_sync(FULL, need_exact);
+          while (needm) {
+            unsigned batch = 0, mm = needm;
+#pragma unroll
+            for (int s2 = 0; s2 < SCAN_EXS; ++s2) {
+              if (mm) {
+                batch |= mm & (0u - mm);
+                mm &= mm - 1u;
+              }
+            }
+            int slotc = 0;
+            for (unsigned bm = batch; bm; bm &= bm - 1u, ++slotc) {
+              const int jj = __shfl_sync(FULL, j, __ffs(bm) - 1);
+              const float* crow = a.cent + static_cast<long long>(jj) * a.ldc;
+              float* dst = cfs + slotc * dpp;
+              if (x_aligned && ((a.ldc & 3) == 0)) {
+                for (int c = lane; c < dpp / 4; c += 32) {
+                  const int valid = min(4, a.d_prime - 4 * c);
+                  cp_async_16_zfill(dst + 4 * c, crow + 4 * c, 4 * valid);
+                }
+              } else {
+                for (int u = lane; u < dpp; u += 32) dst[u] = u < a.d_prime ? crow[u] : 0.0f;
+              }
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            if ((batch >> lane) & 1u) {
+              const int my = __popc(batch & ((1u << lane) - 1u));
+              pe = exact_front_dist_staged(xfs, cfs + my * dpp, a.d_prime, a.chain_flavour, a.chain_q, xs_row,
+                                           __ldg(a.ysq + j));
+            }
+            __syncwarp();
+            needm &= ~batch;
+          }
+        } else if (need_exact) {
+          pe = SKM_EXF(a.x + row * a.ldx, a.cent + static_cast<long long>(j) * a.ldc, a.d_prime, a.chain_flavour,
+                       a.chain_q, xs_row, __ldg(a.ysq + j));
+        }
+        if (need_exact) {
+          const int qs = p % SCAN_WINDOW;
+          W.qp[qs] = pe;
+          W.qdl[qs] = 0.0f;
+          st = walk_interval(pe, 0.0f, rec + qs * nb, W.qdone[qs], nb, tcur, f0, s_theta, pb, run, run_hi);
+          if (st != ST_PENDING) {
+            W.qstat[qs] = st;
+            W.qpb[qs] = pb;
+            W.qrun[qs] = run;
+            W.qrunhi[qs] = run;
+            W.qver[qs] = ver;
+          }
+          ++exact_acc;
         }
         const bool improve = st == ST_COMPLETE && (run < tcur || (run == tcur && j < best));
         const unsigned ev = __ballot_sync(FULL, p < D && (improve || st == ST_PENDING));
@@ -589,6 +694,9 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
   }
 }
 
-inline size_t scan_dyn_smem(int nb) { return static_cast<size_t>(SCAN_WARPS) * (64 * nb + SCAN_WINDOW * nb) * 4; }
+inline size_t scan_dyn_smem(int nb, int d_prime = 0, bool ex_stage = false) {
+  const int dpp = (d_prime + 3) & ~3;
+  return static_cast<size_t>(SCAN_WARPS) * (64 * nb + SCAN_WINDOW * nb + (ex_stage ? (1 + SCAN_EXS) * dpp : 0)) * 4;
+}
 
 }  // namespace skm

@@ -26,6 +26,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "ptx.cuh"
+
 namespace skm {
 
 constexpr int CH_BM = 128;
@@ -255,6 +257,182 @@ __global__ void __launch_bounds__(CH_THREADS, SKM_CHAIN_MINB) sgemm_chain_kernel
       float* o = g.out + r * g.ldo + c0;
       const bool vec_o = c0 + 4 <= g.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0);
       if constexpr (ACC) {  // previous K blocks' sum + this block's chain (one fp32 add)
+        if (vec_o) {
+          const float4 p = *reinterpret_cast<const float4*>(o);
+          v[0] = __fadd_rn(p.x, v[0]); v[1] = __fadd_rn(p.y, v[1]); v[2] = __fadd_rn(p.z, v[2]); v[3] = __fadd_rn(p.w, v[3]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + u < g.N) v[u] = __fadd_rn(o[u], v[u]);
+        }
+      }
+      if constexpr (MODE == CHAIN_DIST) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c0 + u < g.N) {
+            const float e = __fadd_rn(__fadd_rn(__fmul_rn(v[u], -2.0f), xs), g.ysq[c0 + u]);
+            v[u] = e > 0.0f ? e : 0.0f;
+          }
+        }
+      }
+      if (vec_o) {
+        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u < g.N) o[u] = v[u];
+      }
+    }
+  }
+}
+
+// ---- k-major B operand (B[t][j], e.g. the rotation R for x @ R): cp.async pipeline -------------
+// Same per-output chains and K-block launches as sgemm_chain_kernel; the B tile is a plain copy of
+// B rows (no transpose), so both operands stream through a KN_STAGES-deep cp.async ring without
+// register staging, and A stays in its row-major [m][k] layout (read as float2 = 2 chain steps of
+// one row).  A's scalar is the broadcast operand of FFMA2 (`R.F32` in the SASS), so it is not
+// duplicated in shared memory.
+constexpr int KN_STAGES = 4;
+constexpr int KN_ALD = CH_BK + 4;  // A row stride in floats (80 B: 16-B aligned chunks, rows 4 apart hit other banks)
+
+__device__ __forceinline__ unsigned long long ffma2_bcast(float a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("{\n\t.reg .b64 ap;\n\tmov.b64 ap, {%1, %1};\n\tfma.rn.f32x2 %0, ap, %2, %3;\n\t}"
+      : "=l"(d) : "f"(a), "l"(b), "l"(c));
+  return d;
+}
+
+template <int FLAVOUR>
+__device__ __forceinline__ unsigned long long chain_step_bcast(float a, unsigned long long b, unsigned long long c) {
+  if constexpr (FLAVOUR == CHAIN_FMA) {
+    return ffma2_bcast(a, b, c);
+  } else {
+    return f2_pack(__fadd_rn(f2_lo(c), __fmul_rn(a, f2_lo(b))), __fadd_rn(f2_hi(c), __fmul_rn(a, f2_hi(b))));
+  }
+}
+
+inline size_t chain_kn_smem_bytes() { return (size_t)KN_STAGES * (CH_BM * KN_ALD + CH_BK * CH_BN) * 4; }
+
+// requires lda, ldb % 4 == 0 and 16-B aligned a, b (the launcher checks and falls back otherwise)
+template <int FLAVOUR, int MODE, int ACC>
+__global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const ChainArgs g) {
+  extern __shared__ __align__(16) uint8_t kn_smem[];
+  float* As = reinterpret_cast<float*>(kn_smem);                 // [S][BM][KN_ALD]
+  float* Bs = As + KN_STAGES * CH_BM * KN_ALD;                    // [S][BK][BN]
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * CH_BM, n0 = blockIdx.x * CH_BN;
+  const int ntile = (g.K + CH_BK - 1) / CH_BK;
+  const int kfull = g.K / CH_BK;
+  const bool a_vec = ((reinterpret_cast<uintptr_t>(g.a) & 15) == 0) && (g.lda & 3) == 0;
+
+  auto issue = [&](int kt) {
+    const int st = kt % KN_STAGES;
+    const int k0 = kt * CH_BK;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = tid + h * CH_THREADS;
+      // A: row c >> 2, 4-float chunk c & 3
+      const int ar = c >> 2, ak = (c & 3) * 4;
+      const long long grow = m0 + ar;
+      const int kk = k0 + ak;
+      int bytes = 0;
+      if (grow < g.M && kk < g.K) bytes = 4 * min(4, g.K - kk);
+      const float* src = bytes ? g.a + grow * g.lda + kk : g.a;
+      if (a_vec) {
+        cp_async_16_zfill(As + (st * CH_BM + ar) * KN_ALD + ak, src, bytes);
+      } else {  // K block starting off a 16-byte boundary (odd halves of the blocked driver)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          cp_async_4_zfill(As + (st * CH_BM + ar) * KN_ALD + ak + u, 4 * u < bytes ? src + u : g.a,
+                           4 * u < bytes ? 4 : 0);
+      }
+      // B: k row c >> 5, 4-column chunk c & 31
+      const int bk = c >> 5, bn = (c & 31) * 4;
+      const int kb = k0 + bk;
+      const int col = n0 + bn;
+      int bbytes = 0;
+      if (kb < g.K && col < g.N) bbytes = 4 * min(4, g.N - col);
+      const float* bsrc = bbytes ? g.b + (long long)kb * g.ldb + col : g.b;
+      cp_async_16_zfill(Bs + (st * CH_BK + bk) * CH_BN + bn, bsrc, bbytes);
+    }
+  };
+
+  unsigned long long acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+
+#pragma unroll
+  for (int s = 0; s < KN_STAGES - 1; ++s) {
+    if (s < ntile) issue(s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < ntile; ++kt) {
+    cp_async_wait_group<KN_STAGES - 2>();
+    __syncthreads();
+    if (kt + KN_STAGES - 1 < ntile) issue(kt + KN_STAGES - 1);
+    cp_async_commit();
+    const int st = kt % KN_STAGES;
+    const float* A = As + st * CH_BM * KN_ALD;
+    const float* B = Bs + st * CH_BK * CH_BN;
+    auto bload = [&](int kk, unsigned long long* bv) {
+      const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
+      const ulonglong2 b47 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + 64 + tx * 4);
+      bv[0] = b03.x; bv[1] = b03.y; bv[2] = b47.x; bv[3] = b47.y;
+    };
+    if (kt < kfull) {
+#pragma unroll
+      for (int k2 = 0; k2 < CH_BK; k2 += 2) {
+        float2 av[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+          av[i] = *reinterpret_cast<const float2*>(A + r * KN_ALD + k2);
+        }
+        unsigned long long b0[4], b1[4];
+        bload(k2, b0);
+        bload(k2 + 1, b1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(av[i].x, b0[j], acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(av[i].y, b1[j], acc[i][j]);
+      }
+    } else {
+      // ragged last tile: the zero-filled columns past K must not enter the chain
+#pragma unroll 1
+      for (int kk = 0; kk < g.K - kt * CH_BK; ++kk) {
+        unsigned long long bv[4];
+        bload(kk, bv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+          const float a = A[r * KN_ALD + kk];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(a, bv[j], acc[i][j]);
+        }
+      }
+    }
+  }
+  cp_async_wait_all();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const long long r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (r >= g.M) continue;
+    float xs = 0.0f;
+    if constexpr (MODE == CHAIN_DIST) xs = g.xsq[r];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c0 = n0 + h * 64 + tx * 4;
+      float v[4] = {f2_lo(acc[i][2 * h]), f2_hi(acc[i][2 * h]), f2_lo(acc[i][2 * h + 1]), f2_hi(acc[i][2 * h + 1])};
+      float* o = g.out + r * g.ldo + c0;
+      const bool vec_o = c0 + 4 <= g.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0);
+      if constexpr (ACC) {
         if (vec_o) {
           const float4 p = *reinterpret_cast<const float4*>(o);
           v[0] = __fadd_rn(p.x, v[0]); v[1] = __fadd_rn(p.y, v[1]); v[2] = __fadd_rn(p.z, v[2]); v[3] = __fadd_rn(p.w, v[3]);

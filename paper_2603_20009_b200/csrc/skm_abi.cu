@@ -173,8 +173,28 @@ int launch_chain(const skm::ChainArgs& g, cudaStream_t st) {
   return SKM_OK;
 }
 
+template <int FL, int MODE, int ACC>
+int launch_chain_kn(const skm::ChainArgs& g, cudaStream_t st) {
+  auto kern = skm::sgemm_chain_kn_kernel<FL, MODE, ACC>;
+  static unsigned long long attr_dev_mask = 0;
+  if (first_use_on_device(attr_dev_mask)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(skm::chain_kn_smem_bytes()));
+    if (e != cudaSuccess) return cuda_fail(e, "chain_gemm smem attribute");
+  }
+  dim3 grid((g.N + skm::CH_BN - 1) / skm::CH_BN, (g.M + skm::CH_BM - 1) / skm::CH_BM);
+  if (grid.y > 65535) return fail(SKM_E_ARG, "chain_gemm: too many row tiles for one launch");
+  kern<<<grid, skm::CH_THREADS, skm::chain_kn_smem_bytes(), st>>>(g);
+  SKM_LAUNCH_CHECK("chain_gemm_kn launch");
+  return SKM_OK;
+}
+
 template <int FL>
-int launch_chain_block(const skm::ChainArgs& g, bool dist, bool acc, cudaStream_t st) {
+int launch_chain_block(const skm::ChainArgs& g, bool dist, bool acc, bool kmajor, cudaStream_t st) {
+  if (kmajor) {
+    if (dist) return acc ? launch_chain_kn<FL, 1, 1>(g, st) : launch_chain_kn<FL, 1, 0>(g, st);
+    return acc ? launch_chain_kn<FL, 0, 1>(g, st) : launch_chain_kn<FL, 0, 0>(g, st);
+  }
   if (dist) return acc ? launch_chain<FL, 1, 1>(g, st) : launch_chain<FL, 1, 0>(g, st);
   return acc ? launch_chain<FL, 0, 1>(g, st) : launch_chain<FL, 0, 0>(g, st);
 }
@@ -187,6 +207,8 @@ extern "C" int skm_chain_gemm(const skm_chain_params* p, void* stream) {
   if (!p || p->M < 0 || p->N < 0 || p->K < 0) return fail(SKM_E_ARG, "chain_gemm: bad shape");
   if ((long long)p->M * p->N == 0) return SKM_OK;
   if (p->mode == 1 && (!p->xsq || !p->ysq)) return fail(SKM_E_ARG, "chain_gemm: distance mode needs xsq/ysq");
+  if (p->b_kmajor && ((p->ldb & 3) != 0 || (reinterpret_cast<uintptr_t>(p->b) & 15) != 0))
+    return fail(SKM_E_ARG, "chain_gemm: k-major b needs a 16-byte aligned b and ldb % 4 == 0");
   cudaStream_t st = as_stream(stream);
   const int rows_per = 65535 * skm::CH_BM;  // grid.y limit: consecutive launches over row ranges
   for (int r0 = 0; r0 < p->M; r0 += rows_per) {
@@ -199,7 +221,7 @@ extern "C" int skm_chain_gemm(const skm_chain_params* p, void* stream) {
       h.K = k1 - k0;
       h.a = p->a + (long long)r0 * p->lda + k0;
       h.lda = p->lda;
-      h.b = p->b + k0;
+      h.b = p->b_kmajor ? p->b + (long long)k0 * p->ldb : p->b + k0;
       h.ldb = p->ldb;
       h.out = p->out + (long long)r0 * p->ldo;
       h.ldo = p->ldo;
@@ -208,7 +230,8 @@ extern "C" int skm_chain_gemm(const skm_chain_params* p, void* stream) {
       const bool last = k1 >= p->K;
       const bool dist = last && p->mode == 1;
       const bool acc = k0 > 0;
-      int rc = p->flavour == 0 ? launch_chain_block<0>(h, dist, acc, st) : launch_chain_block<1>(h, dist, acc, st);
+      int rc = p->flavour == 0 ? launch_chain_block<0>(h, dist, acc, p->b_kmajor != 0, st)
+                               : launch_chain_block<1>(h, dist, acc, p->b_kmajor != 0, st);
       if (rc) return rc;
       k0 = k1;
     } while (k0 < p->K);
@@ -681,7 +704,35 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.chain_q = p->chain_q;
   if (a.kap > 0.0f && (!a.xsq || !a.ysq || !a.ysq_max || !a.cent))
     return fail(SKM_E_ARG, "pruned_scan: kap > 0 needs xsq, ysq, ysq_max and cent");
-  const size_t smem = skm::scan_dyn_smem(p->nb);
+  // dynamic shared memory available to the scan kernel: the opt-in limit minus its static part
+  static int dyn_limit = -1;
+  if (dyn_limit < 0) {
+    int dv = 0, optin = 0;
+    cudaGetDevice(&dv);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dv);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, skm::pruned_scan_kernel<false>);
+    cudaFuncAttributes fb{};
+    cudaFuncGetAttributes(&fb, skm::pruned_scan_kernel<true>);
+    dyn_limit = optin - static_cast<int>(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes));
+  }
+  if (skm::scan_dyn_smem(p->nb) > static_cast<size_t>(dyn_limit))
+    return fail(SKM_E_ARG, "pruned_scan: tail too long for the shared-memory staging");
+  // exact re-evaluations from shared memory when the row's front + SCAN_EXS centroid fronts fit
+  a.ex_stage = (a.kap > 0.0f && skm::scan_dyn_smem(p->nb, p->d_prime, true) <= static_cast<size_t>(dyn_limit)) ? 1 : 0;
+  if (getenv("SKM_SCAN_EXSTAGE") && atoi(getenv("SKM_SCAN_EXSTAGE")) == 0) a.ex_stage = 0;
+  const size_t smem = skm::scan_dyn_smem(p->nb, p->d_prime, a.ex_stage != 0);
+  cudaStream_t st = as_stream(stream);
+  {
+    static unsigned long long set_mask_d = 0, set_mask_l = 0;
+    if (first_use_on_device(set_mask_d))
+      cudaFuncSetAttribute(skm::pruned_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit);
+    if (first_use_on_device(set_mask_l)) {
+      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit);
+      const char* cv = getenv("SKM_SCAN_CARVEOUT");
+      if (cv) cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+    }
+  }
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -690,24 +741,10 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skm::pruned_scan_kernel<false>, skm::SCAN_WARPS * 32, smem);
   const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms * std::max(per_sm, 1)));
-  cudaStream_t st = as_stream(stream);
-  if (p->dense_mode) {
-    static unsigned long long set_mask = 0;
-    if (first_use_on_device(set_mask)) {
-      cudaFuncSetAttribute(skm::pruned_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(skm::scan_dyn_smem(skm::SCAN_NB_MAX)));
-    }
+  if (p->dense_mode)
     skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
-  } else {
-    static unsigned long long set_mask = 0;
-    if (first_use_on_device(set_mask)) {
-      cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(skm::scan_dyn_smem(skm::SCAN_NB_MAX)));
-      const char* cv = getenv("SKM_SCAN_CARVEOUT");
-      if (cv) cudaFuncSetAttribute(skm::pruned_scan_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
-    }
+  else
     skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
-  }
   SKM_LAUNCH_CHECK("pruned_scan");
   return SKM_OK;
 }

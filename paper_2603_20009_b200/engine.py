@@ -109,12 +109,15 @@ def tc_kappa(k_dim: int) -> float:
 
 
 def chain_gemm(a: torch.Tensor, b: torch.Tensor, M: int, N: int, K: int, out: torch.Tensor, flavour: int = 0,
-               q: int = GEMM_Q, xsq: torch.Tensor | None = None, ysq: torch.Tensor | None = None) -> None:
-    """out = the reference's sgemm (flavour 0) / portable_matmul (1) bits of a[:, :K] . b[:, :K]^T,
-    or (with xsq / ysq) the clamped squared distances of distance.expand_to_sq_l2."""
+               q: int = GEMM_Q, xsq: torch.Tensor | None = None, ysq: torch.Tensor | None = None,
+               b_kmajor: bool = False) -> None:
+    """out = the reference's sgemm (flavour 0) / portable_matmul (1) bits of a[:, :K] . b[:, :K]^T
+    (b_kmajor: a[:, :K] . b[:K, :N], b stored [K][N] -- the cp.async kernel), or (with xsq / ysq)
+    the clamped squared distances of distance.expand_to_sq_l2."""
     p = native.ChainParams()
     p.a, p.lda, p.b, p.ldb = a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0)
     p.M, p.N, p.K, p.flavour, p.q = M, N, K, flavour, q
+    p.b_kmajor = 1 if b_kmajor else 0
     p.mode = 1 if xsq is not None else 0
     p.out, p.ldo = out.data_ptr(), out.stride(0)
     if xsq is not None:

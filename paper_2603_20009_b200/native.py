@@ -52,6 +52,7 @@ class ChainParams(C.Structure):
         ("flavour", _i), ("q", _i), ("mode", _i),
         ("out", _vp), ("ldo", _ll),
         ("xsq", _vp), ("ysq", _vp),
+        ("b_kmajor", _i),
     ]
 
 

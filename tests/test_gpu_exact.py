@@ -39,15 +39,20 @@ def _pad(x):
     return device.to_device_matrix(x)
 
 
+@pytest.mark.parametrize("kmajor", [False, True])
 @pytest.mark.parametrize("case", MB.GEMM_CASES)
-def test_chain_gemm_bitwise_openblas(case):
-    """skm_chain_gemm (fma chain, K blocks of 448) == the survey container's sgemm, bit for bit."""
+def test_chain_gemm_bitwise_openblas(case, kmajor):
+    """skm_chain_gemm (fma chain, K blocks of 448) == the survey container's sgemm, bit for bit,
+    with b as [N][K] rows and as a k-major [K][N] matrix (the cp.async kernel the rotation uses)."""
     from paper_2603_20009_b200.engine import chain_gemm
     M, N, K, lay = case
     a, b = MB.gemm_inputs(M, N, K, lay, 0)
     bt = b if lay == "nt" else np.ascontiguousarray(b.T)
     out = torch.empty((M, (N + 3) // 4 * 4), dtype=torch.float32, device="cuda")
-    chain_gemm(_pad(a), _pad(bt), M, N, K, out, 0, 448)
+    if kmajor:
+        chain_gemm(_pad(a), _pad(np.ascontiguousarray(bt.T)), M, N, K, out, 0, 448, b_kmajor=True)
+    else:
+        chain_gemm(_pad(a), _pad(bt), M, N, K, out, 0, 448)
     got = out[:, :N].cpu().numpy()
     g = np.load(GOLD)
     here = a @ b.T if lay == "nt" else a @ b
@@ -67,6 +72,36 @@ def test_chain_gemm_portable_bitwise():
     out = torch.empty((130, 72), dtype=torch.float32, device="cuda")
     chain_gemm(_pad(a), _pad(b), 130, 70, 700, out, 1, 0)
     assert np.array_equal(out[:, :70].cpu().numpy(), want)
+    out.zero_()
+    chain_gemm(_pad(a), _pad(np.ascontiguousarray(b.T)), 130, 70, 700, out, 1, 0, b_kmajor=True)
+    assert np.array_equal(out[:, :70].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape", [(1000, 1536, 1536), (517, 1002, 1002), (300, 77, 1001), (129, 130, 449),
+                                   (64, 40, 7), (257, 1024, 897)])
+def test_chain_gemm_kmajor_equals_rowmajor(shape):
+    """The k-major cp.async kernel and the [N][K] kernel produce the same bits, including ragged
+    M / N / K tiles, K blocks that start off a 16-byte boundary (K = 1002: 448 + 277 + 277) and
+    signed zeros from the distance clamp."""
+    from paper_2603_20009_b200.engine import chain_gemm
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K)
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K)).astype(np.float32)
+    a[:, ::5] = 0.0
+    A, B, BT = _pad(a), _pad(b), _pad(np.ascontiguousarray(b.T))
+    ld = (N + 3) // 4 * 4
+    for mode in (0, 1):
+        kw = {}
+        if mode:
+            kw = dict(xsq=torch.from_numpy((a.astype(np.float64) ** 2).sum(1).astype(np.float32)).cuda(),
+                      ysq=torch.from_numpy((b.astype(np.float64) ** 2).sum(1).astype(np.float32)).cuda())
+        for fl, q in ((0, 448), (1, 0)):
+            o1 = torch.full((M, ld), 7.0, device="cuda")
+            o2 = torch.full((M, ld), 7.0, device="cuda")
+            chain_gemm(A, B, M, N, K, o1, fl, q, **kw)
+            chain_gemm(A, BT, M, N, K, o2, fl, q, b_kmajor=True, **kw)
+            assert torch.equal(o1[:, :N].view(torch.int32), o2[:, :N].view(torch.int32)), (shape, mode, fl)
 
 
 @pytest.mark.parametrize("case", MB.NORM_CASES)
