@@ -113,6 +113,10 @@ typedef struct skm_gemm_params {
    * candidates carry bit 31 in the record's index.  xsq_ext/ysq_ext: norms over K + ext_k columns,
    * thr1: per-row fl(tau * F[1]), cert_eps: margin relative to xsq_ext + ysq_ext. */
   int ext_k; const float* xsq_ext; const float* ysq_ext; const float* thr1; float cert_eps;
+  /* grouped columns (hierarchical fine phase, ARGMIN / GATE, n_split 1): row i only sees columns
+   * [row_crange[i].x, row_crange[i].y) (its group's centroids); M tile t walks only the N tiles
+   * covering [tile_nrange[t].x, tile_nrange[t].y) (the union of its rows' ranges).  Both int2. */
+  const int* row_crange; const int* tile_nrange;
 } skm_gemm_params;
 int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream);
 /* Merge the ARGMIN top-2 records: assign = lowest index among the smallest distances, tau = its
@@ -211,6 +215,9 @@ typedef struct skm_scan_params {
    * with the exact chain over the d' front columns of x and cent (flavour / q as skm_chain_gemm) */
   float kap; const float* xsq; const float* ysq; const float* ysq_max;
   const float* cent; long long ldc; int chain_flavour; int chain_q;
+  /* grouped rows (hierarchical fine phase): with group_counters, the counters of row r go to
+   * group_counters[3 * row_group[r] + {0, 1, 2}] (global row r) instead of counters */
+  const int* row_group; unsigned long long* group_counters;
 } skm_scan_params;
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
 

@@ -58,6 +58,11 @@ struct GemmArgs {
   const float* thr1;          // per-row fl(tau * F[1])
   float cert_eps;             // margin: eps * (xsq_ext + ysq_ext)
   int dbg;                    // experiments: 1 = GATE drains partials only (no gate phase)
+  // grouped columns (ARGMIN / GATE): row i sees columns [row_crange[i].x, row_crange[i].y);
+  // M tile t walks the N tiles covering tile_nrange[t] (hierarchical fine phase, one launch
+  // for every group: each group's rows against its own centroid block)
+  const int2* row_crange;
+  const int2* tile_nrange;
 };
 constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 
@@ -133,8 +138,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const int m0 = (blockIdx.x / args.n_split) * GEMM_BM;
   const int n_tiles = (args.N + BN - 1) / BN;
-  const int t_begin = (blockIdx.x % args.n_split) * args.tiles_per_cta;
-  const int t_end = min(n_tiles, t_begin + args.tiles_per_cta);
+  int t_begin = (blockIdx.x % args.n_split) * args.tiles_per_cta;
+  int t_end = min(n_tiles, t_begin + args.tiles_per_cta);
+  if (args.tile_nrange) {
+    const int2 nr = args.tile_nrange[blockIdx.x];
+    t_begin = nr.x / BN;
+    t_end = min(n_tiles, (nr.y + BN - 1) / BN);
+  }
   const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
   // extension k-blocks (GATE certification): accumulated into ONE extra TMEM partial per tile
   const int num_e = (MODE == GEMM_GATE) ? (args.ext_k + GEMM_BK - 1) / GEMM_BK : 0;
@@ -241,6 +251,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (MODE == GEMM_DIST || MODE == GEMM_ARGMIN || MODE == GEMM_GATE) {
       if (row_ok) xs = args.xsq[row];
     }
+    int c_lo = 0, c_hi = args.N;  // columns this row may see
+    if constexpr (MODE == GEMM_ARGMIN || MODE == GEMM_GATE) {
+      if (args.row_crange && row_ok) {
+        const int2 cr = args.row_crange[row];
+        c_lo = cr.x;
+        c_hi = min(cr.y, args.N);
+      }
+    }
     float xs_e = 0.0f, thr1 = 0.0f;
     if constexpr (MODE == GEMM_GATE) {
       if (row_ok) thr = args.thr[row];
@@ -343,13 +361,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       } else if constexpr (MODE == GEMM_ARGMIN) {
         if (row_ok) {
-          const int lim = args.N - col0;  // valid columns in this slice
+          const int lim = c_hi - col0;  // valid columns in this slice: [lo, lim)
+          const int lo = c_lo - col0;
           float bv = best, sv = second;
           int bl = -1;
 #pragma unroll
           for (int j = 0; j < HALF; ++j) {
             const float dv = expand_dist(acc[j], xs, ys_tile[j]);
-            if (j < lim) {
+            if (j < lim && j >= lo) {
               // ascending columns: a strictly smaller value takes over (lowest index on ties);
               // every other value, ties included, competes for the second place
               sv = fminf(sv, dv < bv ? bv : dv);
@@ -403,7 +422,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           ++kcount;
         }
         if (args.dbg == 1) continue;
-        const int lim = row_ok ? args.N - col0 : 0;
+        const int lim = row_ok ? c_hi - col0 : 0;
+        const int lo = c_lo - col0;
         uint32_t mask[W];
         int my = 0;
 #pragma unroll
@@ -426,6 +446,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           const int l = lim - w * 32;
           m &= l >= 32 ? 0xffffffffu : (l <= 0 ? 0u : ((1u << l) - 1u));
+          const int l0 = lo - w * 32;  // columns below the row's range (grouped mode)
+          m &= l0 <= 0 ? 0xffffffffu : (l0 >= 32 ? 0u : ~((1u << l0) - 1u));
           mask[w] = m;
           my += __popc(m);
         }

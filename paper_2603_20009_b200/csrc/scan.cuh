@@ -91,6 +91,10 @@ struct ScanArgs {
   // 1: the row's d' front and the centroid fronts of the re-evaluated candidates are staged in the
   // warp's shared memory (scan_dyn_smem(nb, d', true)) and re-evaluated there; 0: from global
   int ex_stage;
+  // grouped rows (hierarchical fine phase): counters go to group_counters[3 * row_group[row] + c]
+  // instead of counters (each group has its own d' controller and convergence test)
+  const int* row_group;
+  unsigned long long* group_counters;
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -294,6 +298,16 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
 
   unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0, exact_acc = 0;
   const int n_rows = a.n_rows;
+  int cur_g = -1;  // grouped mode: group of the accumulated counters
+  auto flush_group = [&]() {
+    if (cur_g >= 0) {
+      unsigned long long* gc = a.group_counters + 3LL * cur_g;
+      warp_add_u64(surv_acc, &gc[0]);
+      warp_add_u64(touched_acc, &gc[1]);
+      warp_add_u64(changed_acc, &gc[2]);
+    }
+    surv_acc = touched_acc = changed_acc = 0;
+  };
   while (true) {
     // rows are handed out in order from a global counter: warps running concurrently work on
     // neighbouring (cluster-sorted) rows, so their candidate centroids' tails stay L2-hot
@@ -310,6 +324,13 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
       if (n_src > a.cap) continue;  // overflow row: handled by the dense pass
     }
     const long long row = a.row_map ? static_cast<long long>(a.row_map[rl]) : a.row0 + rl;
+    if (a.group_counters) {
+      const int g = __ldg(a.row_group + row);
+      if (g != cur_g) {
+        flush_group();
+        cur_g = g;
+      }
+    }
     // ---- stage the x tail, quad layout (q, b, r): 16-byte async copies (zero-filled past the
     //      tail) whose latency overlaps the row's scalar loads and first queue fill
     const float* xrow = a.x + row * a.ldx + a.d_prime;
@@ -684,9 +705,13 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     }
     __syncwarp();
   }
-  warp_add_u64(surv_acc, &a.counters[0]);
-  warp_add_u64(touched_acc, &a.counters[1]);
-  warp_add_u64(changed_acc, &a.counters[2]);
+  if (a.group_counters) {
+    flush_group();
+  } else {
+    warp_add_u64(surv_acc, &a.counters[0]);
+    warp_add_u64(touched_acc, &a.counters[1]);
+    warp_add_u64(changed_acc, &a.counters[2]);
+  }
   if (a.counters_ext) {
     warp_add_u64(blocks_acc, &a.counters_ext[0]);  // speculative block sums computed
     if (lane == 0 && waves_acc) atomicAdd(&a.counters_ext[1], waves_acc);  // warp waves executed

@@ -138,6 +138,17 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   a.ysq_ext = p->ysq_ext;
   a.thr1 = p->thr1;
   a.cert_eps = p->cert_eps;
+  a.row_crange = reinterpret_cast<const int2*>(p->row_crange);
+  a.tile_nrange = reinterpret_cast<const int2*>(p->tile_nrange);
+  if ((a.row_crange != nullptr) != (a.tile_nrange != nullptr))
+    return fail(SKM_E_ARG, "gemm: row_crange and tile_nrange go together");
+  if (a.tile_nrange && (MODE == skm::GEMM_STORE || MODE == skm::GEMM_DIST))
+    return fail(SKM_E_ARG, "gemm: grouped columns need ARGMIN or GATE");
+  if (a.tile_nrange) {  // one CTA per M tile, N range from the table
+    split = 1;
+    a.n_split = 1;
+    a.tiles_per_cta = n_tiles;
+  }
   {
     static int dbg = -1;
     if (dbg < 0) { const char* e = getenv("SKM_GEMM_DBG"); dbg = e ? atoi(e) : 0; }
@@ -702,6 +713,10 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.ldc = p->ldc;
   a.chain_flavour = p->chain_flavour;
   a.chain_q = p->chain_q;
+  a.row_group = p->row_group;
+  a.group_counters = p->group_counters;
+  if ((a.row_group != nullptr) != (a.group_counters != nullptr))
+    return fail(SKM_E_ARG, "pruned_scan: row_group and group_counters go together");
   if (a.kap > 0.0f && (!a.xsq || !a.ysq || !a.ysq_max || !a.cent))
     return fail(SKM_E_ARG, "pruned_scan: kap > 0 needs xsq, ysq, ysq_max and cent");
   // dynamic shared memory available to the scan kernel: the opt-in limit minus its static part

@@ -41,6 +41,7 @@ class GemmParams(C.Structure):
         ("cand", _vp), ("cand_cnt", _vp), ("cand_cap", _i),
         ("row_offset", _ll),
         ("ext_k", _i), ("xsq_ext", _vp), ("ysq_ext", _vp), ("thr1", _vp), ("cert_eps", _f),
+        ("row_crange", _vp), ("tile_nrange", _vp),
     ]
 
 
@@ -72,6 +73,7 @@ class ScanParams(C.Structure):
         ("prune_hist", _vp),
         ("kap", _f), ("xsq", _vp), ("ysq", _vp), ("ysq_max", _vp),
         ("cent", _vp), ("ldc", _ll), ("chain_flavour", _i), ("chain_q", _i),
+        ("row_group", _vp), ("group_counters", _vp),
     ]
 
 

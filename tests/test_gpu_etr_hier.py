@@ -97,6 +97,34 @@ def test_hierarchical_concurrent_groups_bitwise_equal_serial(monkeypatch):
     assert a.work == b.work
 
 
+@pytest.mark.parametrize("case", ["blobs96", "blobs48_full", "skewed1024", "sentinel"])
+def test_hierarchical_batched_fine_phase_bitwise_equal_per_group(monkeypatch, case):
+    """The group-batched fine phase (grouped.py: one loop, grouped GEMM column ranges, per-group
+    d' classes / counters / convergence / splits) equals one independent loop per group bit for
+    bit: assignments, centroids and work counters."""
+    import paper_2603_20009_b200 as skb
+    from paper_2603_20009_b200 import hierarchical as hmod
+    from conftest import make_skewed_blobs
+    if case == "blobs96":
+        x, cfg = make_blobs(40000, 96, 300, seed=7, spread=4.0, noise=1.0), dict(k_total=900, seed=3)
+    elif case == "blobs48_full":  # d < 80: every iteration is a full (grouped ARGMIN) pass
+        x, cfg = make_blobs(30000, 48, 200, seed=5, spread=3.0, noise=1.0), dict(k_total=700, seed=4)
+    elif case == "skewed1024":
+        x, cfg = make_skewed_blobs(30000, 1024, 400, 11), dict(k_total=1600, seed=8)
+    else:
+        x, cfg = make_blobs(20000, 128, 150, seed=9, spread=4.0, noise=1.0), dict(k_total=500, seed=1,
+                                                                                 pruning_sentinel=True)
+    monkeypatch.setattr(hmod, "FINE_BATCHED", False)
+    monkeypatch.setattr(hmod, "FINE_STREAMS", 1)
+    a = skb.hierarchical_fit(x, skb.HierarchicalConfig(**cfg))
+    monkeypatch.setattr(hmod, "FINE_BATCHED", True)
+    b = skb.hierarchical_fit(x, skb.HierarchicalConfig(**cfg))
+    assert a.k == b.k
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids_rotated, b.centroids_rotated)
+    assert a.work == b.work
+
+
 def test_update_centroids_bitwise_vs_oracle():
     import paper_2603_20009_b200 as skb
     from oracle import skm_ref

@@ -55,3 +55,4 @@ print("d'", [s.d_prime for s in st], "surv/vec", [round(s.survivors / a.n, 1) fo
       "n_changed", [s.n_changed for s in st], "chain re-evaluations/vec", [round(dg[3] / a.n, 2) for dg in r.loop.scan_diag],
       "lane util", [round(dg[0] / max(1, 32 * dg[1]), 3) for dg in r.loop.scan_diag],
       "phase", {k: round(v * 1e3, 1) for k, v in r.phase.items()})
+print("per-iteration pruning ms", [round(1e3 * s.timings.get("pruning", 0.0), 1) for s in st])

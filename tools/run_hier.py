@@ -48,11 +48,18 @@ if world > 1:
     dist.barrier()
 t0 = time.perf_counter()
 prof = profiling.KernelTimer()
+prof_host = None
+if os.environ.get("SKM_CPROFILE"):
+    import cProfile
+    prof_host = cProfile.Profile()
+    prof_host.enable()
 with profiling.active(prof):
     if device_entry:
         r = hierarchical_fit_device(x, a.d, cfg, comm=comm, n_global=a.n, row_lo=lo)
     else:
         r = hierarchical_fit(x, cfg)
+if prof_host is not None:
+    prof_host.disable()
 torch.cuda.synchronize()
 wall = time.perf_counter() - t0
 if world > 1:
@@ -63,5 +70,8 @@ if rank == 0:
     print("kernels ms:", {kk: round(v["ms"], 1) for kk, v in sorted(prof.summary().items(), key=lambda kv: -kv[1]["ms"])})
     print(f"hierarchical n={a.n} d={a.d} k_total={a.k} ranks={world} entry={'device' if device_entry else 'host'}: "
           f"achieved k={r.k} wall={wall:.3f}s phase={ {k: round(v, 3) for k, v in r.phase_seconds.items()} }")
+if prof_host is not None and rank == 0:
+    import pstats
+    pstats.Stats(prof_host).sort_stats("tottime").print_stats(30)
 if world > 1:
     dist.destroy_process_group()
