@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs (c1, c3, c4 sweep)")
-    ap.add_argument("--extra", default=",".join(EXTRA), help="secondary configs to measure at N=1")
+    ap.add_argument("--extra", default=",".join(EXTRA) + ",c5", help="secondary configs to measure at N=1")
     return ap.parse_args()
 
 
@@ -202,6 +202,37 @@ def cpu_baseline_sample(args, x: np.ndarray) -> dict | None:
             "sample": f"reference fit (baseline/_ref, compiled kernels: {compiled}) with max_iters=1 on the full "
                       f"{args.n}x{args.d} rows: rotation + the iteration-1 full-distance pass, {dt:.1f} s; the "
                       f"--impl reference arm times all iterations"}
+
+
+def run_c5(dev) -> dict:
+    """BASELINE c5: hierarchical k-means of 10M x 1024 into k_total = 65536 with meso_k = 430
+    (the reference's rule caps near 50.7K at meso_k = 256), rows generated on the GPU
+    with the skewed-blob distribution (the host generator would take minutes at 41 GB).  Device-
+    resident entry; one warm-up on 200K rows, then one timed fit (CUDA events)."""
+    import torch
+    from paper_2603_20009_b200.hierarchical import HierarchicalConfig, hierarchical_fit_device
+    from paper_2603_20009_b200.hostmath import generate_rotation
+    from paper_2603_20009_b200.synth import make_shard_device
+    n, d, k_total, meso_k = 10_000_000, 1024, 65536, 430
+    rot = generate_rotation(d, 0)
+    w = make_shard_device(200_000, d, 4096, 0, 200_000, 1, dev)
+    hierarchical_fit_device(w, d, HierarchicalConfig(k_total=2048, seed=0), rotation=rot)
+    del w
+    t0 = time.perf_counter()
+    x = make_shard_device(n, d, 2 * k_total, 0, n, 0, dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = hierarchical_fit_device(x, d, HierarchicalConfig(k_total=k_total, meso_k=meso_k, seed=0), rotation=rot)
+    e1.record()
+    torch.cuda.synchronize()
+    del x
+    return {"workload": f"hierarchical_fit_device: {n} x {d} skewed blobs generated on the GPU (same distribution as "
+                        f"make_skewed_blobs, not its values), HierarchicalConfig(k_total={k_total}, meso_k={meso_k}, "
+                        f"seed=0), meso 3 + fine 5 iterations, groups batched in one loop",
+            "s_per_fit": round(e0.elapsed_time(e1) / 1e3, 3), "achieved_k": int(r.k),
+            "phase_s": {k_: round(v_, 3) for k_, v_ in r.phase_seconds.items()}, "data_gen_s": round(gen_s, 1)}
 
 
 # ----------------------------------------------------------------------------- roofline
@@ -430,6 +461,9 @@ def main():
                 "recall_history": [round(v, 4) for v in r.loop.recall_history], "data_gen_s": round(gs, 1),
             }
             del xd
+
+    if world == 1 and not args.no_extra and "c5" in args.extra.split(","):
+        extra["c5"] = run_c5(dev)
 
     if rank == 0:
         line = {
