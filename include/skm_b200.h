@@ -165,6 +165,17 @@ typedef struct skm_chain_params {
   int b_kmajor;                /* 0: b is [N][K] (b[j][t]); 1: b is [K][N] (b[t][j], e.g. R for x @ R) */
 } skm_chain_params;
 int skm_chain_gemm(const skm_chain_params* p, void* stream);
+/* Fused exact-chain distances + per-tile top-k (the ETR ground truth without the distance matrix).
+ * rows: the collection [n][K] (row-major, ldr); queries_t: the queries k-major [K][nq] (ldq % 4 == 0).
+ * For query j and 128-row tile t, out_{v,i}[(j * n_tiles + t) * k_top + r] = the k_top smallest
+ * max(0, fl(fl(-2 chain(q_j . x_i) + q_sq_j) + row_sq_i)) of the tile's rows with the row index
+ * i + col_offset, ascending by (value, row); (+inf, INT_MAX) past the tile's rows.
+ * n_tiles = ceil(n / 128), k_top <= 32, chain flavour / q as skm_chain_gemm (all K blocks in one
+ * launch, each added to the running sum with one fp32 add).
+ * Replaces: evaluation.py:42-75 (distances + argsort of each query's row). */
+int skm_chain_topk_tiles(const float* rows, long long ldr, const float* queries_t, long long ldq, int n, int nq, int K,
+                         int flavour, int q, const float* row_sq, const float* q_sq, int k_top, float* out_v,
+                         int* out_i, int col_offset, void* stream);
 
 /* ---- centroid update ------------------------------------------------------------------ */
 /* stable sort of row ids by assignment; counts/offsets int32[k] */

@@ -462,6 +462,200 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
   }
 }
 
+// ---- fused exact-chain distances + per-tile top-k (ETR ground truth, evaluation.py:53-75) -----
+// Rows of the collection are the A operand (M = n rows, row-major) and the queries the k-major
+// B operand (B[t][q] = query q's column t): the cp.async pipeline of sgemm_chain_kn_kernel with
+// 2 stages, EVERY K block of the blocked driver in one launch (each block's chain from +0, added
+// to the running sum kept in shared memory with one fp32 add -- the association of the
+// launch-per-block kernel), the expansion, and for each query column the k_top smallest
+// (distance, row) of the tile, ascending, ties to the lower row:
+// out[(query * n_tiles + tile) * k_top + r].  The distance matrix never reaches HBM; a radix top-k
+// over the n_tiles * k_top survivors of each query finishes the selection in the same stable
+// order (candidates are laid out tile by tile, each tile's in (value, row) order).
+constexpr int TOPK_TILE_MAX = 32;
+constexpr int KNT_STAGES = 2;
+
+struct ChainTopkArgs {
+  const float* a;  // collection rows [M][K]
+  long long lda;
+  const float* b;  // queries, k-major [K][N]
+  long long ldb;
+  int M, N, K, q;
+  const float* xsq;  // per row of a
+  const float* ysq;  // per query
+  int k_top;
+  int n_tiles;       // ceil(M / 128)
+  float* out_v;
+  int* out_i;
+  int col_offset;    // added to the row index
+};
+
+inline size_t chain_topk_smem_bytes() {
+  return (size_t)KNT_STAGES * (CH_BM * KN_ALD + CH_BK * CH_BN) * 4 + (size_t)CH_BM * CH_BN * 4;
+}
+
+template <int FLAVOUR>
+__global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_topk_kernel(const ChainTopkArgs g) {
+  extern __shared__ __align__(16) uint8_t kt_smem[];
+  float* As = reinterpret_cast<float*>(kt_smem);                 // [S][BM][KN_ALD]
+  float* Bs = As + KNT_STAGES * CH_BM * KN_ALD;                   // [S][BK][BN]
+  float* tot = Bs + KNT_STAGES * CH_BK * CH_BN;                   // [BM][BN] running sums
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.x * CH_BM, n0 = blockIdx.y * CH_BN;
+  const bool a_al = ((reinterpret_cast<uintptr_t>(g.a) & 15) == 0) && (g.lda & 3) == 0;
+  int k0 = 0;
+  bool first = true;
+  while (k0 < g.K) {
+    const int k1 = chain_next_boundary(k0, g.K, FLAVOUR == CHAIN_FMA ? g.q : 0);
+    const int KB = k1 - k0;
+    const bool a_vec = a_al && (k0 & 3) == 0;
+    const int ntile = (KB + CH_BK - 1) / CH_BK;
+    const int kfull = KB / CH_BK;
+    auto issue = [&](int kt) {
+      const int st = kt % KNT_STAGES;
+      const int kb0 = kt * CH_BK;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tid + h * CH_THREADS;
+        const int ar = c >> 2, ak = (c & 3) * 4;
+        const long long grow = m0 + ar;
+        const int kk = kb0 + ak;
+        int bytes = 0;
+        if (grow < g.M && kk < KB) bytes = 4 * min(4, KB - kk);
+        const float* src = bytes ? g.a + grow * g.lda + k0 + kk : g.a;
+        if (a_vec) {
+          cp_async_16_zfill(As + (st * CH_BM + ar) * KN_ALD + ak, src, bytes);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            cp_async_4_zfill(As + (st * CH_BM + ar) * KN_ALD + ak + u, 4 * u < bytes ? src + u : g.a,
+                             4 * u < bytes ? 4 : 0);
+        }
+        const int bk = c >> 5, bn = (c & 31) * 4;
+        const int kb = kb0 + bk;
+        const int col = n0 + bn;
+        int bbytes = 0;
+        if (kb < KB && col < g.N) bbytes = 4 * min(4, g.N - col);
+        const float* bsrc = bbytes ? g.b + (long long)(k0 + kb) * g.ldb + col : g.b;
+        cp_async_16_zfill(Bs + (st * CH_BK + bk) * CH_BN + bn, bsrc, bbytes);
+      }
+    };
+    unsigned long long acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+    __syncthreads();  // the previous block's last stage reads are complete
+#pragma unroll
+    for (int s2 = 0; s2 < KNT_STAGES - 1; ++s2) {
+      if (s2 < ntile) issue(s2);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < ntile; ++kt) {
+      cp_async_wait_group<KNT_STAGES - 2>();
+      __syncthreads();
+      if (kt + KNT_STAGES - 1 < ntile) issue(kt + KNT_STAGES - 1);
+      cp_async_commit();
+      const int st = kt % KNT_STAGES;
+      const float* A = As + st * CH_BM * KN_ALD;
+      const float* B = Bs + st * CH_BK * CH_BN;
+      auto bload = [&](int kk, unsigned long long* bv) {
+        const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
+        const ulonglong2 b47 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + 64 + tx * 4);
+        bv[0] = b03.x; bv[1] = b03.y; bv[2] = b47.x; bv[3] = b47.y;
+      };
+      if (kt < kfull) {
+#pragma unroll
+        for (int k2 = 0; k2 < CH_BK; k2 += 2) {
+          float2 av[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+            av[i] = *reinterpret_cast<const float2*>(A + r * KN_ALD + k2);
+          }
+          unsigned long long b0[4], b1[4];
+          bload(k2, b0);
+          bload(k2 + 1, b1);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(av[i].x, b0[j], acc[i][j]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(av[i].y, b1[j], acc[i][j]);
+        }
+      } else {
+#pragma unroll 1
+        for (int kk = 0; kk < KB - kt * CH_BK; ++kk) {
+          unsigned long long bv[4];
+          bload(kk, bv);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+            const float a = A[r * KN_ALD + kk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(a, bv[j], acc[i][j]);
+          }
+        }
+      }
+    }
+    cp_async_wait_all();
+    // block chain -> running sum (C += A_blk * B_blk: one fp32 add; the first block is stored)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4* t = reinterpret_cast<float4*>(tot + r * CH_BN + h * 64 + tx * 4);
+        float4 v = make_float4(f2_lo(acc[i][2 * h]), f2_hi(acc[i][2 * h]), f2_lo(acc[i][2 * h + 1]),
+                               f2_hi(acc[i][2 * h + 1]));
+        if (!first) {
+          const float4 p = *t;
+          v = make_float4(__fadd_rn(p.x, v.x), __fadd_rn(p.y, v.y), __fadd_rn(p.z, v.z), __fadd_rn(p.w, v.w));
+        }
+        *t = v;
+      }
+    }
+    first = false;
+    k0 = k1;
+  }
+  __syncthreads();
+  if (tid < CH_BN && n0 + tid < g.N) {
+    const int c = tid;  // query column
+    const long long qcol = n0 + c;
+    const float ys = g.ysq[qcol];
+    const int valid = min(CH_BM, g.M - m0);
+    float v[TOPK_TILE_MAX];
+    int ix[TOPK_TILE_MAX];
+    const int K = g.k_top;
+    int cnt = 0;
+    for (int r = 0; r < valid; ++r) {
+      // expand_to_sq_l2 with the query as the "x" side (evaluation.py:42-50: vals = q . x^T * -2,
+      // += q_sq, += x_sq): fl(fl(-2 ip + q_sq) + x_sq)
+      const float e = __fadd_rn(__fadd_rn(__fmul_rn(tot[r * CH_BN + c], -2.0f), ys), __ldg(g.xsq + m0 + r));
+      const float dv = e > 0.0f ? e : 0.0f;
+      if (cnt < K || dv < v[K - 1]) {
+        int p = cnt < K ? cnt : K - 1;
+        while (p > 0 && v[p - 1] > dv) {
+          v[p] = v[p - 1];
+          ix[p] = ix[p - 1];
+          --p;
+        }
+        v[p] = dv;
+        ix[p] = r;
+        if (cnt < K) ++cnt;
+      }
+    }
+    const long long o = (qcol * g.n_tiles + blockIdx.x) * K;
+    for (int i = 0; i < K; ++i) {
+      g.out_v[o + i] = i < cnt ? v[i] : __int_as_float(0x7f800000);
+      g.out_i[o + i] = i < cnt ? m0 + ix[i] + g.col_offset : 0x7fffffff;
+    }
+  }
+}
+
 inline size_t chain_smem_bytes() { return 2 * CH_BK * CH_BM * 8 + 2 * CH_BK * CH_BN * 4; }
 
 // Squared row norms over the leading `dims` columns, bitwise equal to the reference's

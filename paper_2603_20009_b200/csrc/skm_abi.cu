@@ -250,6 +250,40 @@ extern "C" int skm_chain_gemm(const skm_chain_params* p, void* stream) {
   return SKM_OK;
 }
 
+template <int FL>
+static int launch_chain_topk(const skm::ChainTopkArgs& g, cudaStream_t st) {
+  auto kern = skm::sgemm_chain_topk_kernel<FL>;
+  static unsigned long long attr_dev_mask = 0;
+  if (first_use_on_device(attr_dev_mask)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(skm::chain_topk_smem_bytes()));
+    if (e != cudaSuccess) return cuda_fail(e, "chain_topk smem attribute");
+  }
+  dim3 grid(static_cast<unsigned>(g.n_tiles), static_cast<unsigned>((g.N + skm::CH_BN - 1) / skm::CH_BN));
+  kern<<<grid, skm::CH_THREADS, skm::chain_topk_smem_bytes(), st>>>(g);
+  SKM_LAUNCH_CHECK("chain_topk launch");
+  return SKM_OK;
+}
+
+extern "C" int skm_chain_topk_tiles(const float* rows, long long ldr, const float* queries_t, long long ldq, int n,
+                                    int nq, int K, int flavour, int q, const float* row_sq, const float* q_sq,
+                                    int k_top, float* out_v, int* out_i, int col_offset, void* stream) {
+  if (n <= 0 || nq <= 0) return SKM_OK;
+  if (K <= 0 || k_top < 1 || k_top > skm::TOPK_TILE_MAX) return fail(SKM_E_ARG, "chain_topk: bad K or k_top (1..32)");
+  if ((nq + skm::CH_BN - 1) / skm::CH_BN > 65535) return fail(SKM_E_ARG, "chain_topk: too many query tiles");
+  if ((ldq & 3) != 0 || (reinterpret_cast<uintptr_t>(queries_t) & 15) != 0)
+    return fail(SKM_E_ARG, "chain_topk: k-major queries need 16-byte alignment and ld % 4 == 0");
+  skm::ChainTopkArgs g{};
+  g.a = rows; g.lda = ldr; g.b = queries_t; g.ldb = ldq;
+  g.M = n; g.N = nq; g.K = K; g.q = q;
+  g.xsq = row_sq; g.ysq = q_sq;
+  g.k_top = k_top;
+  g.n_tiles = (n + skm::CH_BM - 1) / skm::CH_BM;
+  g.out_v = out_v; g.out_i = out_i; g.col_offset = col_offset;
+  cudaStream_t st = as_stream(stream);
+  return flavour == 0 ? launch_chain_topk<0>(g, st) : launch_chain_topk<1>(g, st);
+}
+
 extern "C" {
 
 const char* skm_last_error(void) { return g_err.c_str(); }

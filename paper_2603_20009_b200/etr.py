@@ -88,6 +88,10 @@ def merge_topk_shards(all_i: torch.Tensor, all_v: torch.Tensor, shards: int, kk:
     return all_i[0, :, :k_out].contiguous(), all_v[0, :, :k_out].contiguous()
 
 
+TOPK_FUSED_MAX = 32  # csrc/sgemm_chain.cuh TOPK_TILE_MAX
+FUSED_GT = True      # tests flip it to compare with the materialised distance blocks
+
+
 def device_topk_distances(q: torch.Tensor, q_hi, q_lo, q_sq, x: torch.Tensor, x_hi, x_lo, x_sq, d: int, k: int,
                           col_offset: int = 0, max_bytes: int = 1 << 30) -> tuple[torch.Tensor, torch.Tensor]:
     """Exact top-k rows of x for each query (squared L2 via the expansion identity, stable
@@ -104,6 +108,25 @@ def device_topk_distances(q: torch.Tensor, q_hi, q_lo, q_sq, x: torch.Tensor, x_
     out_i = torch.empty((nq, kk), dtype=torch.int32, device=dev)
     out_v = torch.empty((nq, kk), dtype=torch.float32, device=dev)
     if nq == 0 or n == 0:
+        return out_i, out_v
+    if kk <= TOPK_FUSED_MAX and FUSED_GT:
+        # fused: each 128-row tile keeps its kk best per query in the chain kernel's epilogue,
+        # a radix top-k over the n_tiles * kk survivors finishes (no distance matrix in HBM)
+        n_tiles = (n + 127) // 128
+        qb = max(1, min(nq, max_bytes // (8 * n_tiles * kk)))
+        for s in range(0, nq, qb):
+            e = min(nq, s + qb)
+            qt = torch.zeros((d, padded_ld(e - s)), dtype=torch.float32, device=dev)
+            qt[:, :e - s] = q[s:e, :d].t()
+            cv = torch.empty((e - s, n_tiles * kk), dtype=torch.float32, device=dev)
+            ci = torch.empty((e - s, n_tiles * kk), dtype=torch.int32, device=dev)
+            native.call("skm_chain_topk_tiles", ptr(x), x.stride(0), ptr(qt), qt.stride(0), n, e - s, d, 0, GEMM_Q,
+                        ptr(x_sq), ptr(q_sq[s:e]), kk, ptr(cv), ptr(ci), col_offset, stream_handle(),
+                        flops=2.0 * (e - s) * n * d, tag="chain_topk")
+            pos = torch.empty((e - s, kk), dtype=torch.int32, device=dev)
+            native.call("skm_topk_rows", ptr(cv), cv.stride(0), e - s, n_tiles * kk, kk, ptr(pos), ptr(out_v[s:e]),
+                        kk, 0, stream_handle(), nbytes=5.0 * 4 * (e - s) * n_tiles * kk)
+            out_i[s:e] = torch.gather(ci, 1, pos.long())
         return out_i, out_v
     qb = max(1, min(nq, max_bytes // (4 * padded_ld(n))))
     for s in range(0, nq, qb):

@@ -102,6 +102,7 @@ _SIGS = {
     "skm_argmin_candidates": ([_vp, _i, _vp, _vp, _vp, _f, _vp, _vp, _vp], _i),
     "skm_cand_exact_argmin": ([_vp, _i, _vp, _vp, _i, _vp, _ll, _vp, _ll, _i, _vp, _vp, _i, _i, _vp, _vp, _vp], _i),
     "skm_chain_gemm": ([C.POINTER(ChainParams), _vp], _i),
+    "skm_chain_topk_tiles": ([_vp, _ll, _vp, _ll, _i, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _i, _vp], _i),
     "skm_cluster_sort": ([_vp, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp], _i),
     "skm_cluster_sums": ([_vp, _ll, _vp, _vp, _vp, _i, _i, _vp, _i, _vp, _ll, _i, _vp], _i),
     "skm_finalize_centroids": ([_vp, _vp, _i, _i, _vp, _ll, _vp], _i),

@@ -125,6 +125,30 @@ def test_hierarchical_batched_fine_phase_bitwise_equal_per_group(monkeypatch, ca
     assert a.work == b.work
 
 
+@pytest.mark.parametrize("shape", [(70, 1000, 64, 10), (130, 300, 1000, 32), (33, 5000, 1536, 1), (5, 129, 96, 7)])
+def test_fused_gt_topk_equals_materialised(monkeypatch, shape):
+    """The fused chain-distance + per-tile top-k kernel (no distance matrix) returns exactly the
+    materialised chain distances' stable top-k: ragged tiles, K blocks off a 16-byte boundary
+    (d = 1000: 448 + 276 + 276), duplicated rows (ties to the lower index), a column offset."""
+    import torch
+    from paper_2603_20009_b200 import etr
+    from paper_2603_20009_b200.device import to_device_matrix
+    nq, n, d, k = shape
+    rng = np.random.default_rng(nq + n + d)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    x[1::7] = x[0::7][:len(x[1::7])]  # exact duplicates -> tied distances
+    q = np.concatenate([x[:nq // 2], rng.standard_normal((nq - nq // 2, d)).astype(np.float32)])
+    X, Q = to_device_matrix(x), to_device_matrix(q)
+    xs = torch.from_numpy((x.astype(np.float64) ** 2).sum(1).astype(np.float32)).cuda()
+    qs = torch.from_numpy((q.astype(np.float64) ** 2).sum(1).astype(np.float32)).cuda()
+    monkeypatch.setattr(etr, "FUSED_GT", True)
+    fi, fv = etr.device_topk_distances(Q, None, None, qs, X, None, None, xs, d, k, col_offset=17)
+    monkeypatch.setattr(etr, "FUSED_GT", False)
+    mi, mv = etr.device_topk_distances(Q, None, None, qs, X, None, None, xs, d, k, col_offset=17)
+    assert torch.equal(fi, mi)
+    assert torch.equal(fv.view(torch.int32), mv.view(torch.int32))
+
+
 def test_update_centroids_bitwise_vs_oracle():
     import paper_2603_20009_b200 as skb
     from oracle import skm_ref
