@@ -229,6 +229,11 @@ typedef struct skm_scan_params {
   /* grouped rows (hierarchical fine phase): with group_counters, the counters of row r go to
    * group_counters[3 * row_group[r] + {0, 1, 2}] (global row r) instead of counters */
   const int* row_group; unsigned long long* group_counters;
+  /* flat = 1 (list mode, kap > 0): a first pass resolves every row whose threshold changes only at
+   * its own previous centroid (flatscan.cuh); the rest (their batch-local indices appended to
+   * fb_rows, count in *fb_count -- both device workspace, fb_rows >= n_rows entries) are then
+   * scanned by the exact kernel.  Same outputs as flat = 0. */
+  int flat; int* fb_rows; unsigned int* fb_count;
 } skm_scan_params;
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
 

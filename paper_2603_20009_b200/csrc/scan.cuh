@@ -95,6 +95,8 @@ struct ScanArgs {
   // instead of counters (each group has its own d' controller and convergence test)
   const int* row_group;
   unsigned long long* group_counters;
+  // optional: the row count is read from the device (the flat pass's fallback list length)
+  const unsigned int* n_rows_dev;
 };
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
                               : (SCAN_DEPTH == 2) ? 0x55555555u : 0xffffffffu;  // slot leader lanes
 
   unsigned long long surv_acc = 0, touched_acc = 0, changed_acc = 0, blocks_acc = 0, waves_acc = 0, exact_acc = 0;
-  const int n_rows = a.n_rows;
+  const int n_rows = a.n_rows_dev ? static_cast<int>(*a.n_rows_dev) : a.n_rows;
   int cur_g = -1;  // grouped mode: group of the accumulated counters
   auto flush_group = [&]() {
     if (cur_g >= 0) {

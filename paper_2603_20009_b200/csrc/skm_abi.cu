@@ -13,6 +13,7 @@
 #include "gemm_tf32x3.cuh"
 #include "update.cuh"
 #include "scan.cuh"
+#include "flatscan.cuh"
 #include "sgemm_chain.cuh"
 #include "topk.cuh"
 
@@ -790,6 +791,28 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skm::pruned_scan_kernel<false>, skm::SCAN_WARPS * 32, smem);
   const int blocks = std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms * std::max(per_sm, 1)));
+  const bool flat = p->flat && !p->dense_mode && a.ex_stage && a.kap > 0.0f && !a.rows &&
+                    skm::flat_dyn_smem(p->nb, p->d_prime) <= static_cast<size_t>(dyn_limit);
+  if (p->flat && flat && (!p->fb_rows || !p->fb_count)) return fail(SKM_E_ARG, "pruned_scan: flat needs fb_rows/fb_count");
+  if (flat) {
+    static unsigned long long set_mask_f = 0;
+    if (first_use_on_device(set_mask_f))
+      cudaFuncSetAttribute(skm::flat_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit);
+    const size_t fsm = skm::flat_dyn_smem(p->nb, p->d_prime);
+    int per_sm_f = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, skm::flat_scan_kernel, skm::SCAN_WARPS * 32, fsm);
+    const int fblocks =
+        std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms * std::max(per_sm_f, 1)));
+    cudaError_t e = cudaMemsetAsync(p->fb_count, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "pruned_scan fallback reset");
+    skm::flat_scan_kernel<<<fblocks, skm::SCAN_WARPS * 32, fsm, st>>>(a, p->fb_rows, p->fb_count);
+    SKM_LAUNCH_CHECK("flat_scan");
+    // the fallback rows through the exact kernel (row count read on the device)
+    e = cudaMemsetAsync(p->work, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "pruned_scan work reset");
+    a.rows = p->fb_rows;
+    a.n_rows_dev = p->fb_count;
+  }
   if (p->dense_mode)
     skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
   else

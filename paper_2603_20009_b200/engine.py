@@ -57,6 +57,13 @@ COLLECT_DIAG = os.environ.get("SKM_DIAG", "0") == "1"  # read scan diagnostics b
 # so the scan counts them (survivor, 64 dims) without walking them.
 # (a prefix of tail block 0 lower-bounds its running sum, so any ext <= 64 is a valid certificate)
 CERT_EXT = int(os.environ.get("SKM_CERT_EXT", "64")) if os.environ.get("SKM_CERT", "1") != "0" else 0
+# flat first pass of the scan (csrc/flatscan.cuh): rows whose threshold changes only at their own
+# previous centroid are resolved without in-order resolution; the rest take the exact kernel
+SCAN_FLAT = os.environ.get("SKM_SCAN_FLAT", "1") != "0"
+# ... used once the loop has nearly converged: rows that change assignment fall back to the exact
+# kernel after a partial flat walk, so early iterations (10-40 % changing) are faster without it
+# (c2: -3 % scan time at <= 1.4 % changed, +13 % at 40 %; profiles/r2_summary.md)
+FLAT_MAX_CHANGED = float(os.environ.get("SKM_SCAN_FLAT_MAX", "0.02"))
 
 
 def cert_eps(k_dim: int) -> float:
@@ -395,6 +402,9 @@ class Workspace:
         self.work = torch.zeros(256, dtype=torch.int32, device=dev)  # per-SM scan row queues
         # scan diagnostics: spec blocks, spec waves, exact blocks, exact waves, rows routed to the exact phase
         self.diag = torch.zeros(8, dtype=torch.int64, device=dev)
+        self.flat = False  # this pass uses the flat scan (the loop decides per iteration)
+        self.fb_rows = torch.empty(b, dtype=i32, device=dev)  # flat scan: fallback rows of a batch
+        self.fb_count = torch.zeros(1, dtype=i32, device=dev)
         self.bx = torch.empty(b, dtype=f32, device=dev)
         self.bthr = torch.empty(b, dtype=f32, device=dev)
         self.thr1 = torch.empty(nn, dtype=f32, device=dev)
@@ -599,7 +609,7 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         sp.counters_ext = ws.diag.data_ptr()
         if PRUNE_HIST is not None:
             sp.prune_hist = PRUNE_HIST.data_ptr()
-        _scan_exact_args(sp, data, cents, ws, xsq, kap)
+        _scan_exact_args(sp, data, cents, ws, xsq, kap, plan.sentinel)
         native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
         if ws.cap < k:
             # rows whose candidate list overflowed the slab: dense distance rows, same kernel
@@ -645,8 +655,11 @@ def _dense_overflow(data, cents, ws, plan, glob_rows, n_over, xsq):
         native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan_dense", nbytes=4.0 * cn * k)
 
 
-def _scan_exact_args(sp, data: DeviceData, cents: Centroids, ws: Workspace, xsq: torch.Tensor, kap: float) -> None:
+def _scan_exact_args(sp, data: DeviceData, cents: Centroids, ws: Workspace, xsq: torch.Tensor, kap: float,
+                     sentinel: bool = False) -> None:
     """Interval decisions on tensor-core distances + the exact chain for the unsettled ones."""
+    if SCAN_FLAT and ws.flat and not sentinel:
+        sp.flat, sp.fb_rows, sp.fb_count = 1, ws.fb_rows.data_ptr(), ws.fb_count.data_ptr()
     sp.kap = kap
     sp.xsq, sp.ysq, sp.ysq_max = xsq.data_ptr(), cents.ysq.data_ptr(), cents.ysq_max.data_ptr()
     sp.cent, sp.ldc = cents.c.data_ptr(), cents.ld
@@ -846,6 +859,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
     pin_scal = torch.empty(4, dtype=torch.float64, pin_memory=True)
     pin_counts = torch.empty(k, dtype=torch.int32, pin_memory=True)
     have_order = False
+    last_changed = None  # n_changed of the previous iteration (flat-scan policy)
     scan_blocks: list[int] = []
     scan_waves: list[int] = []
     scan_diag: list[list[int]] = []
@@ -871,6 +885,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             cents.refresh(d_prime, d_prime)
             ws.counters.zero_()
             ws.diag.zero_()
+            ws.flat = last_changed is not None and last_changed <= FLAT_MAX_CHANGED * n
             pruned_assign_pass(data, cents, ws, plan, order=ws.order[:n_local] if have_order else None)
             timer.stop("pruning")
             work.front_pair_dims += n * k * d_prime
@@ -899,6 +914,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             sorted_counts, wcss, ch, sv, td = reducer.reduce(data, ws, n_local)
         if it > 1:
             n_changed = int(round(ch))
+            last_changed = n_changed
         if pruned_iter:
             if COLLECT_DIAG:
                 dg = ws.diag.tolist()

@@ -32,6 +32,8 @@ from .config import KMeansConfig, WorkCounters, initial_d_prime, pruning_support
 from .device import padded_ld, ptr, stream_handle
 from .engine import (
     CERT_EXT,
+    FLAT_MAX_CHANGED,
+    SCAN_FLAT,
     Centroids,
     DeviceData,
     PrunePlan,
@@ -171,6 +173,8 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
         sp.cent, sp.ldc = cents.c.data_ptr(), cents.ld
         sp.chain_flavour, sp.chain_q = ws.chain_flavour, ws.chain_q
         sp.row_group, sp.group_counters = lay.row_group.data_ptr(), gcount.data_ptr()
+        if SCAN_FLAT and ws.flat and not plan.sentinel:
+            sp.flat, sp.fb_rows, sp.fb_count = 1, ws.fb_rows.data_ptr(), ws.fb_count.data_ptr()
         native.call("skm_pruned_scan", ctypes_ref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
 
 
@@ -213,6 +217,7 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
     pin_g = torch.empty((G, 3), dtype=torch.int64, pin_memory=True)
     pin_counts = torch.empty(lay.k_total, dtype=torch.int32, pin_memory=True)
     nk = lay.sizes * lay.ks
+    last_changed = None
 
     for it in range(1, max_iters + 1):
         act = np.flatnonzero(active)
@@ -237,6 +242,7 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
         else:
             native.call("skm_seed_thresholds", ptr(data.x), data.ld, ptr(cents.c), cents.ld, ptr(ws.assign), n, d,
                         ptr(ws.tau), st, nbytes=4.0 * n * d + 8.0 * n)
+            ws.flat = last_changed is not None and last_changed <= FLAT_MAX_CHANGED * int(lay.sizes[act].sum())
             for dp in np.unique(dprime[act]):
                 cls = act[dprime[act] == dp]
                 plan = PrunePlan(d, int(dp), cfg.epsilon0, cfg.pruning_sentinel, dev)
@@ -261,6 +267,7 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
         pin_counts.copy_(ws.counts, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
         gc = pin_g.numpy().copy()
+        last_changed = int(gc[act, 2].sum()) if it > 1 else None
         counts = pin_counts.numpy().astype(np.int64)
         stop_now = np.zeros(G, dtype=bool)
         if it > 1:

@@ -74,6 +74,7 @@ class ScanParams(C.Structure):
         ("kap", _f), ("xsq", _vp), ("ysq", _vp), ("ysq_max", _vp),
         ("cent", _vp), ("ldc", _ll), ("chain_flavour", _i), ("chain_q", _i),
         ("row_group", _vp), ("group_counters", _vp),
+        ("flat", _i), ("fb_rows", _vp), ("fb_count", _vp),
     ]
 
 

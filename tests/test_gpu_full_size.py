@@ -1,6 +1,7 @@
 """Full-size parity with the REAL reference on BASELINE configs (tests/golden/make_golden_full.py):
-c1 (100K x 128, k=256, 10 iterations) and c2 (1M x 1536, k=4096, 10 iterations -- the headline
-bench workload), inputs regenerated from the reference's own seeded generators.
+c1 (100K x 128, k=256, 10 iterations), c2 (1M x 1536, k=4096, 10 iterations -- the headline
+bench workload) and c4 at k=1024 (1M x 768, 10 iterations), inputs regenerated from the
+reference's own seeded generators.
 
 The device loop reproduces the reference's arithmetic exactly (exact-chain rotation, einsum-order
 norms, tensor-core distances settled on rigorous intervals with the reference's chain where they
@@ -38,13 +39,18 @@ def _input(name):
     return make_blobs(*args) if gen == "blobs" else make_skewed_blobs(*args)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("name", [c for c in ["c1", "c2", "c4k1024", "c3"]
+                                  if os.path.exists(os.path.join(HERE, "golden", f"full_{c}.npz"))])
 def test_full_size_trajectory_bitwise(name):
     import paper_2603_20009_b200 as skb
     path = os.path.join(HERE, "golden", f"full_{name}.npz")
     g = np.load(path)
     _, _, kw, rs, cs = CASES[name]
     x = _input(name)
+    kw = dict(kw)
+    if "etr" in kw:
+        nq, top_k = kw.pop("etr")
+        kw["etr"] = skb.EtrConfig(n_queries=nq, top_k=top_k)
     cfg = skb.KMeansConfig(**kw)
     snaps = []
 
@@ -83,6 +89,8 @@ def test_full_size_trajectory_bitwise(name):
     assert [s.n_empty_splits for s in st] == g["splits"].tolist()
     assert [s.wcss for s in st] == g["wcss"].tolist()
     assert res.terminated_by == str(g["term"])
+    if "recall" in g.files:
+        assert res.recall_history == g["recall"].tolist()
     assert np.array_equal(res.assignments, g["assign"].astype(np.int32))
     cent = res.centroids[::int(g["cent_stride"])]
     rel = float(np.linalg.norm(cent.astype(np.float64) - g["cent_sub"]) / np.linalg.norm(g["cent_sub"]))

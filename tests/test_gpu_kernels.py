@@ -215,12 +215,15 @@ SCAN_CASES = [
 
 
 @pytest.mark.parametrize("seed,n,k,d,dp,sentinel", SCAN_CASES)
-@pytest.mark.parametrize("exact,prev_mode,cert", [(False, "random", False), (True, "random", False),
-                                                  (True, "nearest", False), (True, "mixed", False),
-                                                  (True, "nearest", True), (False, "mixed", True),
-                                                  (True, "mixed", True), (True, "dup", False),
-                                                  (True, "dup", True)])
-def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_mode, cert):
+@pytest.mark.parametrize("exact,prev_mode,cert,flat", [(False, "random", False, False), (True, "random", False, False),
+                                                       (True, "nearest", False, False), (True, "mixed", False, False),
+                                                       (True, "nearest", True, False), (False, "mixed", True, False),
+                                                       (True, "mixed", True, False), (True, "dup", False, False),
+                                                       (True, "dup", True, False),
+                                                       (True, "random", False, True), (True, "nearest", False, True),
+                                                       (True, "mixed", True, True), (True, "nearest", True, True),
+                                                       (True, "dup", True, True), (True, "dup", False, True)])
+def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_mode, cert, flat):
     """Production scan equals the sequential reference scan over all centroids, including the
     survivor/dims counters.  ``exact``: the oracle scans the reference's own partial distances
     (the exact fma chain of OpenBLAS sgemm, computed here by the device chain GEMM) while the
@@ -337,8 +340,15 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_
     p.kap = kap
     p.xsq, p.ysq, p.ysq_max = xs.data_ptr(), cs.data_ptr(), ymax.data_ptr()
     p.cent, p.ldc, p.chain_flavour, p.chain_q = Cm.data_ptr(), Cm.stride(0), 0, 448
+    if flat:  # flat first pass + exact kernel on its fallback rows (csrc/flatscan.cuh)
+        fb_rows = torch.empty(n, dtype=torch.int32, device="cuda")
+        fb_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+        p.flat, p.fb_rows, p.fb_count = 1, fb_rows.data_ptr(), fb_count.data_ptr()
     import ctypes
     native.check(native.load().skm_pruned_scan(ctypes.byref(p), dev.stream_handle()), "scan")
+    if flat:
+        print("flat pass fallback rows:", int(fb_count.item()), "of", n)
+        p.flat = 0
     # overflow rows -> dense pass over their full distance rows
     over = torch.nonzero(cc > cap).flatten().to(torch.int32)
     if over.numel():
