@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     // ---- every other candidate under its known threshold, 8 slots x 4 blocks per wave
     int src = 0;
     int spos = -1, sj = 0, snxt = 0;                 // all lanes of the slot
-    float sp = 0.0f, sdl = 0.0f, stc = 0.0f;         // leader: front distance, bound, threshold
+    float stc = 0.0f;                                // leader: the candidate's threshold
     float slo = 0.0f, shi = 0.0f;                    // leader: running-sum interval
     bool samb = false, sneed = false, scert = false; // leader
     bool failed = false;
@@ -266,8 +266,6 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             spos = src + sl;
             sj = nj;
             snxt = 0;
-            sp = np_;
-            sdl = ndl;
             stc = ntc;
             scert = ncert;
             slo = fmaxf(__fsub_rn(np_, ndl), 0.0f);
@@ -298,8 +296,6 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
             const int my = __popc(batch & ((1u << lane) - 1u));
             const float pe = exact_front_dist_staged(xfs, cfs + my * dpp, a.d_prime, a.chain_flavour, a.chain_q,
                                                      xs_row, __ldg(a.ysq + sj));
-            sp = pe;
-            sdl = 0.0f;
             sneed = false;
             samb = false;
             int fin = 0;  // 1 not survivor, 2 pruned (counted), 3 complete -> violation check below

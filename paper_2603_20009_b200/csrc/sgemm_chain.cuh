@@ -292,8 +292,15 @@ __global__ void __launch_bounds__(CH_THREADS, SKM_CHAIN_MINB) sgemm_chain_kernel
 // register staging, and A stays in its row-major [m][k] layout (read as float2 = 2 chain steps of
 // one row).  A's scalar is the broadcast operand of FFMA2 (`R.F32` in the SASS), so it is not
 // duplicated in shared memory.
-constexpr int KN_STAGES = 4;
-constexpr int KN_ALD = CH_BK + 4;  // A row stride in floats (80 B: 16-B aligned chunks, rows 4 apart hit other banks)
+#ifndef SKM_KN_STAGES
+#define SKM_KN_STAGES 2
+#endif
+#ifndef SKM_KN_BK
+#define SKM_KN_BK 32
+#endif
+constexpr int KN_STAGES = SKM_KN_STAGES;
+constexpr int KN_BK = SKM_KN_BK;   // k depth of one pipeline stage
+constexpr int KN_ALD = KN_BK + 4;  // A row stride in floats (80 B: 16-B aligned chunks, rows 4 apart hit other banks)
 
 __device__ __forceinline__ unsigned long long ffma2_bcast(float a, unsigned long long b, unsigned long long c) {
   unsigned long long d;
@@ -311,7 +318,7 @@ __device__ __forceinline__ unsigned long long chain_step_bcast(float a, unsigned
   }
 }
 
-inline size_t chain_kn_smem_bytes() { return (size_t)KN_STAGES * (CH_BM * KN_ALD + CH_BK * CH_BN) * 4; }
+inline size_t chain_kn_smem_bytes() { return (size_t)KN_STAGES * (CH_BM * KN_ALD + KN_BK * CH_BN) * 4; }
 
 // requires lda, ldb % 4 == 0 and 16-B aligned a, b (the launcher checks and falls back otherwise)
 template <int FLAVOUR, int MODE, int ACC>
@@ -322,18 +329,18 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.y * CH_BM, n0 = blockIdx.x * CH_BN;
-  const int ntile = (g.K + CH_BK - 1) / CH_BK;
-  const int kfull = g.K / CH_BK;
+  const int ntile = (g.K + KN_BK - 1) / KN_BK;
+  const int kfull = g.K / KN_BK;
   const bool a_vec = ((reinterpret_cast<uintptr_t>(g.a) & 15) == 0) && (g.lda & 3) == 0;
 
   auto issue = [&](int kt) {
     const int st = kt % KN_STAGES;
-    const int k0 = kt * CH_BK;
+    const int k0 = kt * KN_BK;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < KN_BK / 8; ++h) {
       const int c = tid + h * CH_THREADS;
-      // A: row c >> 2, 4-float chunk c & 3
-      const int ar = c >> 2, ak = (c & 3) * 4;
+      // A: row c / (KN_BK / 4), 4-float chunk c % (KN_BK / 4)
+      const int ar = c / (KN_BK / 4), ak = (c % (KN_BK / 4)) * 4;
       const long long grow = m0 + ar;
       const int kk = k0 + ak;
       int bytes = 0;
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
       int bbytes = 0;
       if (kb < g.K && col < g.N) bbytes = 4 * min(4, g.N - col);
       const float* bsrc = bbytes ? g.b + (long long)kb * g.ldb + col : g.b;
-      cp_async_16_zfill(Bs + (st * CH_BK + bk) * CH_BN + bn, bsrc, bbytes);
+      cp_async_16_zfill(Bs + (st * KN_BK + bk) * CH_BN + bn, bsrc, bbytes);
     }
   };
 
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
     cp_async_commit();
     const int st = kt % KN_STAGES;
     const float* A = As + st * CH_BM * KN_ALD;
-    const float* B = Bs + st * CH_BK * CH_BN;
+    const float* B = Bs + st * KN_BK * CH_BN;
     auto bload = [&](int kk, unsigned long long* bv) {
       const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
       const ulonglong2 b47 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + 64 + tx * 4);
@@ -384,7 +391,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
     };
     if (kt < kfull) {
 #pragma unroll
-      for (int k2 = 0; k2 < CH_BK; k2 += 2) {
+      for (int k2 = 0; k2 < KN_BK; k2 += 2) {
         float2 av[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
     } else {
       // ragged last tile: the zero-filled columns past K must not enter the chain
 #pragma unroll 1
-      for (int kk = 0; kk < g.K - kt * CH_BK; ++kk) {
+      for (int kk = 0; kk < g.K - kt * KN_BK; ++kk) {
         unsigned long long bv[4];
         bload(kk, bv);
 #pragma unroll
@@ -474,6 +481,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
 // order (candidates are laid out tile by tile, each tile's in (value, row) order).
 constexpr int TOPK_TILE_MAX = 32;
 constexpr int KNT_STAGES = 2;
+constexpr int KNT_ALD = CH_BK + 4;
 
 struct ChainTopkArgs {
   const float* a;  // collection rows [M][K]
@@ -491,14 +499,14 @@ struct ChainTopkArgs {
 };
 
 inline size_t chain_topk_smem_bytes() {
-  return (size_t)KNT_STAGES * (CH_BM * KN_ALD + CH_BK * CH_BN) * 4 + (size_t)CH_BM * CH_BN * 4;
+  return (size_t)KNT_STAGES * (CH_BM * KNT_ALD + CH_BK * CH_BN) * 4 + (size_t)CH_BM * CH_BN * 4;
 }
 
 template <int FLAVOUR>
 __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_topk_kernel(const ChainTopkArgs g) {
   extern __shared__ __align__(16) uint8_t kt_smem[];
-  float* As = reinterpret_cast<float*>(kt_smem);                 // [S][BM][KN_ALD]
-  float* Bs = As + KNT_STAGES * CH_BM * KN_ALD;                   // [S][BK][BN]
+  float* As = reinterpret_cast<float*>(kt_smem);                 // [S][BM][KNT_ALD]
+  float* Bs = As + KNT_STAGES * CH_BM * KNT_ALD;                   // [S][BK][BN]
   float* tot = Bs + KNT_STAGES * CH_BK * CH_BN;                   // [BM][BN] running sums
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -525,11 +533,11 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_topk_kernel(const C
         if (grow < g.M && kk < KB) bytes = 4 * min(4, KB - kk);
         const float* src = bytes ? g.a + grow * g.lda + k0 + kk : g.a;
         if (a_vec) {
-          cp_async_16_zfill(As + (st * CH_BM + ar) * KN_ALD + ak, src, bytes);
+          cp_async_16_zfill(As + (st * CH_BM + ar) * KNT_ALD + ak, src, bytes);
         } else {
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            cp_async_4_zfill(As + (st * CH_BM + ar) * KN_ALD + ak + u, 4 * u < bytes ? src + u : g.a,
+            cp_async_4_zfill(As + (st * CH_BM + ar) * KNT_ALD + ak + u, 4 * u < bytes ? src + u : g.a,
                              4 * u < bytes ? 4 : 0);
         }
         const int bk = c >> 5, bn = (c & 31) * 4;
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_topk_kernel(const C
       if (kt + KNT_STAGES - 1 < ntile) issue(kt + KNT_STAGES - 1);
       cp_async_commit();
       const int st = kt % KNT_STAGES;
-      const float* A = As + st * CH_BM * KN_ALD;
+      const float* A = As + st * CH_BM * KNT_ALD;
       const float* B = Bs + st * CH_BK * CH_BN;
       auto bload = [&](int kk, unsigned long long* bv) {
         const ulonglong2 b03 = *reinterpret_cast<const ulonglong2*>(B + kk * CH_BN + tx * 4);
@@ -572,7 +580,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_topk_kernel(const C
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
-            av[i] = *reinterpret_cast<const float2*>(A + r * KN_ALD + k2);
+            av[i] = *reinterpret_cast<const float2*>(A + r * KNT_ALD + k2);
           }
           unsigned long long b0[4], b1[4];
           bload(k2, b0);
@@ -594,7 +602,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_topk_kernel(const C
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
-            const float a = A[r * KN_ALD + kk];
+            const float a = A[r * KNT_ALD + kk];
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(a, bv[j], acc[i][j]);
           }
