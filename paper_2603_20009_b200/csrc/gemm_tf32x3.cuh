@@ -69,6 +69,9 @@ constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 #ifndef SKM_GATE_LDS
 #define SKM_GATE_LDS 1       // GATE reads the staged column norms with explicit ld.shared.v4
 #endif
+#ifndef SKM_GEMM_KPAIR
+#define SKM_GEMM_KPAIR 1     // accumulate two k-blocks per TMEM partial
+#endif
 #ifndef SKM_GATE_PREFETCH
 #define SKM_GATE_PREFETCH 1  // GATE loads the next tile's column norms during the drains
 #endif
@@ -146,6 +149,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     t_end = min(n_tiles, (nr.y + BN - 1) / BN);
   }
   const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
+  // Two 32-wide k-blocks per TMEM partial (64-wide partials): half the drains, and the GATE's
+  // 4-deep partial ring then spans a whole tile's K, so the MMA issuer runs a tile ahead of the
+  // gate pass.  Every mode pairs, so DIST, ARGMIN and GATE keep identical accumulator bits.  The
+  // rigorous bound (engine.tc_kappa, paired) covers it: 24 truncating accumulations per partial
+  // cost 3 * 2^-20 of sum |x_t c_t| on top of the 3 * 2^-20 of 3xTF32.
+  constexpr int KPAIR = SKM_GEMM_KPAIR ? 2 : 1;
+  const int num_p = (num_k + KPAIR - 1) / KPAIR;  // main partials per tile
   // extension k-blocks (GATE certification): accumulated into ONE extra TMEM partial per tile
   const int num_e = (MODE == GEMM_GATE) ? (args.ext_k + GEMM_BK - 1) / GEMM_BK : 0;
 
@@ -205,8 +215,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
         for (int kb = 0; kb < num_k + num_e; ++kb) {
           // extension k-blocks after the first one keep accumulating into the same partial
-          const bool cont = kb > num_k;
-          const bool last_of_partial = kb < num_k || kb == num_k + num_e - 1;
+          const bool main_kb = kb < num_k;
+          const bool cont = main_kb ? (kb % KPAIR != 0) : kb > num_k;
+          const bool last_of_partial = main_kb ? ((kb % KPAIR == KPAIR - 1) || kb == num_k - 1)
+                                               : kb == num_k + num_e - 1;
           const int buf = kcount % NBUF;
           const uint32_t use = kcount / NBUF;
           if (!cont) mbar_wait(&tempty[buf], (use & 1) ^ 1);
@@ -314,7 +326,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         drain_release();
       }
 #pragma unroll 1
-      for (int kb = 1; kb < num_k; ++kb) {
+      for (int kb = 1; kb < num_p; ++kb) {
         const uint32_t tbase = drain_wait();
 #pragma unroll
         for (int c = 0; c < HALF / 16; ++c) tmem_ld16_add(tbase + c * 16, *reinterpret_cast<float(*)[16]>(&acc[c * 16]));

@@ -66,12 +66,12 @@ SCAN_FLAT = os.environ.get("SKM_SCAN_FLAT", "1") != "0"
 FLAT_MAX_CHANGED = float(os.environ.get("SKM_SCAN_FLAT_MAX", "0.02"))
 
 
-def cert_eps(k_dim: int) -> float:
+def cert_eps(k_dim: int, paired: bool = True) -> float:
     """Margin of the block-0 certificate over k_dim = d' + ext columns, relative to xsq + ysq
     there: the tensor-core distance D~ and the reference's running sum fl(p + block sum) each lie
     within tc_kappa * (xsq + ysq + D) <= 3 tc_kappa * (xsq + ysq) of the exact distance (D <=
     2 (xsq + ysq)), so 6 tc_kappa separates them from the threshold for certain."""
-    return 6.0 * tc_kappa(k_dim)
+    return 6.0 * tc_kappa(k_dim, paired)
 
 
 # ---------------------------------------------------------------- exact-chain policy
@@ -84,6 +84,7 @@ def cert_eps(k_dim: int) -> float:
 # winners in the scan), so the loop reproduces the reference bit for bit.
 GEMM_Q = 448
 _U = 2.0 ** -24
+GATE_KPAIR = True  # csrc/gemm_tf32x3.cuh SKM_GEMM_KPAIR: the tensor-core GEMM accumulates 64-wide TMEM partials
 
 
 def resolve_gemm_backend(backend: str = "auto") -> str:
@@ -105,14 +106,16 @@ def chain_policy(backend: str = "auto") -> tuple[int, int]:
     return (1, 0) if resolve_gemm_backend(backend) == "portable" else (0, GEMM_Q)
 
 
-def tc_kappa(k_dim: int) -> float:
+def tc_kappa(k_dim: int, paired: bool = True) -> float:
     """Rigorous bound coefficient for |p_tensor_core - p_chain| <= kappa * (xsq + ysq + p) of a
     squared distance over k_dim columns: the chain's own error
     gamma_K = K u / (1 - K u) plus the 3xTF32 error (dropped lo*lo and tf32 truncation of lo:
-    3 * 2^-20 per product, accumulator truncation of the 12 MMAs of a 32-wide k-block, fp32 adds
-    of the k-block partials), with a factor 2 of slack, plus 16 u for the expansion's roundings."""
+    3 * 2^-20 per product) and the truncating TMEM accumulation of a partial (12 MMAs of a 32-wide
+    k-block: 1.5 * 2^-20; ``paired`` = the GATE's 64-wide partials, 24 MMAs: 3 * 2^-20), then the
+    fp32 adds of the partials (inside gamma_K), with a factor 2 of slack, plus 16 u for the
+    expansion's roundings."""
     g = k_dim * _U / (1.0 - k_dim * _U)
-    return 2.0 * (g + 2.0 ** -17) + 16.0 * _U
+    return 2.0 * (g + (2.0 ** -16 if paired else 2.0 ** -17)) + 16.0 * _U
 
 
 def chain_gemm(a: torch.Tensor, b: torch.Tensor, M: int, N: int, K: int, out: torch.Tensor, flavour: int = 0,
@@ -458,7 +461,7 @@ def full_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, row0: in
           xsq=xsq, ysq=cents.ysq, top=top, n_split=split)
     assign, tau = ws.assign[row0:row0 + n], ws.tau[row0:row0 + n]
     ws.amb_count.zero_()
-    native.call("skm_argmin_merge", ptr(top), split, n, ptr(xsq), ptr(cents.ysq_max), float(tc_kappa(d)),
+    native.call("skm_argmin_merge", ptr(top), split, n, ptr(xsq), ptr(cents.ysq_max), float(tc_kappa(d, GATE_KPAIR)),
                 ptr(assign), ptr(tau), ptr(ws.amb_rows), ptr(ws.amb_count), st)
     native.call("skm_exact_pair_dist", ptr(data.x[row0:row0 + n]), data.ld, ptr(cents.c), cents.ld, ptr(assign), n,
                 d, ptr(xsq), ptr(cents.ysq), ws.chain_flavour, ws.chain_q, ptr(tau), st, nbytes=4.0 * n * d)
@@ -475,7 +478,7 @@ def resolve_ambiguous_argmin(data: DeviceData, cents: Centroids, ws: Workspace, 
     more candidates than the slab holds take the whole chain-GEMM distance row."""
     st = stream_handle()
     d, k = data.d, cents.k
-    kap = tc_kappa(d)
+    kap = tc_kappa(d, GATE_KPAIR)
     xsq_all = data.norms(d)
     glob_all = (rows_local + row0).to(torch.int32)
     for c0 in range(0, int(glob_all.numel()), ws.batch):
@@ -559,7 +562,7 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         native.call("skm_seed_thresholds", ptr(x_rows), data.ld, ptr(cents.c), cents.ld, ptr(assign), n, d,
                     ptr(tau), st, nbytes=4.0 * n * d + 8.0 * n)
     xsq = data.norms(dp)
-    kap = tc_kappa(dp)
+    kap = tc_kappa(dp, GATE_KPAIR)
     # emission threshold of the tensor-core gate: a superset of the candidates whose exact
     # (chain) distance may pass fl(tau F0); the scan settles every decision exactly
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
@@ -569,7 +572,7 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(ws.thr1[row0:row0 + n]),
                     None, None, 0.0, st)
         xsq_ext = data.norms(dp + ext)
-        ceps = cert_eps(dp + ext)
+        ceps = cert_eps(dp + ext, GATE_KPAIR)
     k = cents.k
     ordered = order is not None and row0 == 0 and n == data.n
     if ordered:
@@ -651,7 +654,7 @@ def _dense_overflow(data, cents, ws, plan, glob_rows, n_over, xsq):
         sp.theta, sp.block_dims = plan.theta.data_ptr(), plan.bdims.data_ptr()
         sp.tau, sp.assign, sp.counters = ws.tau.data_ptr(), ws.assign.data_ptr(), ws.counters.data_ptr()
         sp.dense_mode = 1
-        _scan_exact_args(sp, data, cents, ws, xsq, tc_kappa(plan.d_prime))
+        _scan_exact_args(sp, data, cents, ws, xsq, tc_kappa(plan.d_prime, GATE_KPAIR))
         native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan_dense", nbytes=4.0 * cn * k)
 
 

@@ -33,6 +33,7 @@ from .device import padded_ld, ptr, stream_handle
 from .engine import (
     CERT_EXT,
     FLAT_MAX_CHANGED,
+    GATE_KPAIR,
     SCAN_FLAT,
     Centroids,
     DeviceData,
@@ -89,7 +90,7 @@ def _grouped_full_assign(data: DeviceData, cents: Centroids, ws: Workspace, lay:
           xsq=xsq, ysq=cents.ysq, top=top, n_split=1, row_crange=crange, tile_nrange=tile_ranges(crange))
     assign, tau = ws.assign[r0:r1], ws.tau[r0:r1]
     ws.amb_count.zero_()
-    native.call("skm_argmin_merge", ptr(top), 1, n, ptr(xsq), ptr(cents.ysq_max), float(tc_kappa(d)),
+    native.call("skm_argmin_merge", ptr(top), 1, n, ptr(xsq), ptr(cents.ysq_max), float(tc_kappa(d, GATE_KPAIR)),
                 ptr(assign), ptr(tau), ptr(ws.amb_rows), ptr(ws.amb_count), st)
     native.call("skm_exact_pair_dist", ptr(data.x[r0:r1]), data.ld, ptr(cents.c), cents.ld, ptr(assign), n, d,
                 ptr(xsq), ptr(cents.ysq), ws.chain_flavour, ws.chain_q, ptr(tau), st, nbytes=4.0 * n * d)
@@ -100,7 +101,7 @@ def _grouped_full_assign(data: DeviceData, cents: Centroids, ws: Workspace, lay:
     # then the reference's chain distance of each (rows sorted so tiles stay inside few groups)
     glob_all = (torch.sort(ws.amb_rows[:n_amb]).values + r0).to(torch.int32)
     xsq_all = data.norms(d)
-    kap = tc_kappa(d)
+    kap = tc_kappa(d, GATE_KPAIR)
     for c0 in range(0, n_amb, ws.batch):
         glob = glob_all[c0:c0 + ws.batch].contiguous()
         m = int(glob.numel())
@@ -131,7 +132,7 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
     d, dp = data.d, plan.d_prime
     st = stream_handle()
     xsq = data.norms(dp)
-    kap = tc_kappa(dp)
+    kap = tc_kappa(dp, GATE_KPAIR)
     native.call("skm_gate_threshold", ptr(ws.tau), data.n, float(plan.gate[0]), int(plan.sentinel), ptr(ws.thr),
                 ptr(xsq), ptr(cents.ysq_max), float(kap), st)
     ext = CERT_EXT if (not plan.sentinel and dp % 4 == 0 and dp + CERT_EXT <= d and plan.widths[0] == 64) else 0
@@ -141,7 +142,7 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
         native.call("skm_gate_threshold", ptr(ws.tau), data.n, float(plan.gate[1]), 0, ptr(ws.thr1), None, None, 0.0,
                     st)
         xsq_ext = data.norms(dp + ext)
-        ceps = cert_eps(dp + ext)
+        ceps = cert_eps(dp + ext, GATE_KPAIR)
     fld = padded_ld(dp + ext)
     ga_hi, ga_lo = ws.front_buffers(fld)
     k = cents.k

@@ -234,7 +234,7 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_
     state) or 90% nearest.  ``cert``: the gate GEMM also certifies tail-block-0 prunes (ext_k =
     64) and the scan skips walking them.  ``dup``: the second half of the centroids duplicates
     the first (exact distance ties everywhere)."""
-    from paper_2603_20009_b200.engine import cert_eps, chain_gemm, tc_kappa
+    from paper_2603_20009_b200.engine import GATE_KPAIR, cert_eps, chain_gemm, tc_kappa
     from oracle import kernels_np as O
     from paper_2603_20009_b200 import native
     from paper_2603_20009_b200.config import pdxify, tail_block_layout
@@ -268,7 +268,7 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_
         print("tensor-core vs chain distances: %d of %d differ" % (np.count_nonzero(tc != vals), tc.size))
     else:
         vals = np.ascontiguousarray(D[:, :k].cpu().numpy())
-    kap = tc_kappa(dp) if exact else 0.0
+    kap = tc_kappa(dp, GATE_KPAIR) if exact else 0.0
     ymax = torch.tensor([float(cs.max().item())], device="cuda")
     widths, bounds = tail_block_layout(d, dp)
     f = threshold_factors(d, dp, bounds, 2.1)
