@@ -70,7 +70,7 @@ constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 #define SKM_GATE_LDS 1       // GATE reads the staged column norms with explicit ld.shared.v4
 #endif
 #ifndef SKM_GEMM_KPAIR
-#define SKM_GEMM_KPAIR 2     // k-blocks accumulated per TMEM partial
+#define SKM_GEMM_KPAIR 4     // k-blocks accumulated per TMEM partial
 #endif
 #ifndef SKM_GATE_PREFETCH
 #define SKM_GATE_PREFETCH 1  // GATE loads the next tile's column norms during the drains
@@ -149,11 +149,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     t_end = min(n_tiles, (nr.y + BN - 1) / BN);
   }
   const int num_k = (args.K + GEMM_BK - 1) / GEMM_BK;
-  // Two 32-wide k-blocks per TMEM partial (64-wide partials): half the drains, and the GATE's
-  // 4-deep partial ring then spans a whole tile's K, so the MMA issuer runs a tile ahead of the
-  // gate pass.  Every mode pairs, so DIST, ARGMIN and GATE keep identical accumulator bits.  The
-  // rigorous bound (engine.tc_kappa, paired) covers it: 24 truncating accumulations per partial
-  // cost 3 * 2^-20 of sum |x_t c_t| on top of the 3 * 2^-20 of 3xTF32.
+  // KPAIR 32-wide k-blocks per TMEM partial (4: 128-wide partials): fewer drains, and the GATE's
+  // 4-deep partial ring spans a whole tile's K, so the MMA issuer runs a tile ahead of the gate
+  // pass.  Every mode uses it, so DIST, ARGMIN and GATE keep identical accumulator bits.  The
+  // rigorous bound (engine.tc_kappa, paired) covers it: 48 truncating accumulations per partial
+  // cost 6 * 2^-20 of sum |x_t c_t| on top of the 3 * 2^-20 of 3xTF32, inside 2^-16.
   constexpr int KPAIR = SKM_GEMM_KPAIR;  // k-blocks per partial (1, 2 or 4)
   const int num_p = (num_k + KPAIR - 1) / KPAIR;  // main partials per tile
   // extension k-blocks (GATE certification): accumulated into ONE extra TMEM partial per tile

@@ -84,7 +84,7 @@ def cert_eps(k_dim: int, paired: bool = True) -> float:
 # winners in the scan), so the loop reproduces the reference bit for bit.
 GEMM_Q = 448
 _U = 2.0 ** -24
-GATE_KPAIR = True  # csrc/gemm_tf32x3.cuh SKM_GEMM_KPAIR: the tensor-core GEMM accumulates 64-wide TMEM partials
+GATE_KPAIR = True  # csrc/gemm_tf32x3.cuh SKM_GEMM_KPAIR: the tensor-core GEMM accumulates 128-wide TMEM partials
 
 
 def resolve_gemm_backend(backend: str = "auto") -> str:
@@ -111,9 +111,9 @@ def tc_kappa(k_dim: int, paired: bool = True) -> float:
     squared distance over k_dim columns: the chain's own error
     gamma_K = K u / (1 - K u) plus the 3xTF32 error (dropped lo*lo and tf32 truncation of lo:
     3 * 2^-20 per product) and the truncating TMEM accumulation of a partial (12 MMAs of a 32-wide
-    k-block: 1.5 * 2^-20; ``paired`` = the GATE's 64-wide partials, 24 MMAs: 3 * 2^-20), then the
-    fp32 adds of the partials (inside gamma_K), with a factor 2 of slack, plus 16 u for the
-    expansion's roundings."""
+    k-block: 1.5 * 2^-20; ``paired`` = the GEMM's 128-wide partials, 48 MMAs: 6 * 2^-20, so
+    9 * 2^-20 <= 2^-16 in all), then the fp32 adds of the partials (inside gamma_K), with a
+    factor 2 of slack, plus 16 u for the expansion's roundings."""
     g = k_dim * _U / (1.0 - k_dim * _U)
     return 2.0 * (g + (2.0 ** -16 if paired else 2.0 ** -17)) + 16.0 * _U
 
@@ -340,7 +340,8 @@ def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
             setattr(p, name, t.data_ptr())
     names = {native.GEMM_STORE: "gemm_store", native.GEMM_DIST: "gemm_dist", native.GEMM_ARGMIN: "gemm_argmin",
              native.GEMM_GATE: "gemm_gate"}
-    native.call("skm_gemm_tf32x3", C.byref(p), stream_handle(), flops=2.0 * M * N * K, tag=names[mode])
+    # algorithmic flops of the launch: the certification extension's columns are computed too
+    native.call("skm_gemm_tf32x3", C.byref(p), stream_handle(), flops=2.0 * M * N * (K + p.ext_k), tag=names[mode])
 
 
 def _n_split(m_rows: int, n_cols: int, sms: int = 148) -> int:

@@ -73,7 +73,9 @@ def test_gemm_store_matches_fp64(M, N, K):
     ref = a.astype(np.float64) @ b.astype(np.float64).T
     scale = np.sqrt((a.astype(np.float64) ** 2) @ (b.astype(np.float64) ** 2).T)
     err = np.abs(out - ref) / scale
-    assert err.max() < 5e-6, err.max()
+    # 128-wide TMEM partials (SKM_GEMM_KPAIR = 4): measured max 6.1e-6 of the RMS scale (32-wide:
+    # 2.9e-6); every decision is taken on engine.tc_kappa's rigorous bound, far above either
+    assert err.max() < 1e-5, err.max()
 
 
 def test_gemm_dist_argmin_gate_consistent():
