@@ -116,7 +116,9 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         cur_g = g;
       }
     }
-    // ---- stage the x tail (quad layout) and the d' front
+    // ---- stage the x tail (quad layout) and the d' front (every lane is done with the previous
+    //      row's shared-memory reads first)
+    __syncwarp();
     const float* xrow = a.x + row * a.ldx;
     if (x_aligned) {
       for (int c = lane; c < 16 * nb; c += 32) {
