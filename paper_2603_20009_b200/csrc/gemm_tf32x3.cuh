@@ -14,9 +14,11 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..17 epilogue: warp w reads TMEM lane quadrant (w%4) and column slice (w-2)/4;
 //               thread = one output row x BN/4 columns, running sums in registers.
-// The 512 TMEM columns hold 512/BN k-block partials in flight: BN = 256 for STORE / DIST /
-// ARGMIN, BN = 128 for GATE, whose per-tile gate pass would otherwise hold the MMA issuer
-// (two partials in flight) and whose 64 running sums spilled at the 96-register cap.
+// The 512 TMEM columns hold 512/BN partials in flight (BN = 256: two), each partial KPAIR
+// 32-wide k-blocks.  With 128-wide partials two of them span a tile's K at the usual d', so
+// the GATE also runs at BN = 256 (2 stages): it reads B from shared memory once per 256
+// columns instead of 128 (at N = 128 the MMA is co-limited by its shared-memory operand reads),
+// 112 -> 98 ms per c2 fit despite a few spilled registers of the 64 running sums.
 // A CTA owns one 128-row M tile and walks a contiguous range of BN-wide N tiles in
 // ascending order, so per-row reductions (argmin, candidate emission) see columns in
 // ascending index order like the reference's bank loop (core.py:183-190, 243-260).
@@ -78,7 +80,13 @@ constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 256;       // STORE / DIST / ARGMIN tile width
-constexpr int GEMM_BN_GATE = 128;  // GATE tile width: 4-deep TMEM partial ring, 32 sums per thread
+#ifndef SKM_GATE_BN
+#define SKM_GATE_BN 256
+#endif
+#ifndef SKM_GATE_STAGES
+#define SKM_GATE_STAGES 2
+#endif
+constexpr int GEMM_BN_GATE = SKM_GATE_BN;  // GATE tile width: 4-deep TMEM partial ring, 32 sums per thread
 constexpr int GEMM_BK = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int GEMM_EPI_WARPS = 16;
 constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;

@@ -608,7 +608,7 @@ int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream) {
     case SKM_GEMM_STORE: return launch_gemm<2, skm::GEMM_STORE, skm::GEMM_BN>(p, st);
     case SKM_GEMM_DIST: return launch_gemm<2, skm::GEMM_DIST, skm::GEMM_BN>(p, st);
     case SKM_GEMM_ARGMIN: return launch_gemm<2, skm::GEMM_ARGMIN, skm::GEMM_BN>(p, st);
-    case SKM_GEMM_GATE: return launch_gemm<3, skm::GEMM_GATE, skm::GEMM_BN_GATE>(p, st);
+    case SKM_GEMM_GATE: return launch_gemm<SKM_GATE_STAGES, skm::GEMM_GATE, skm::GEMM_BN_GATE>(p, st);
     default: return fail(SKM_E_ARG, "gemm: unknown mode");
   }
 }
