@@ -62,8 +62,8 @@ CERT_EXT = int(os.environ.get("SKM_CERT_EXT", "64")) if os.environ.get("SKM_CERT
 SCAN_FLAT = os.environ.get("SKM_SCAN_FLAT", "1") != "0"
 # ... used once the loop has nearly converged: rows that change assignment fall back to the exact
 # kernel after a partial flat walk, so early iterations (10-40 % changing) are faster without it
-# (c2: -3 % scan time at <= 1.4 % changed, +13 % at 40 %; profiles/r2_summary.md)
-FLAT_MAX_CHANGED = float(os.environ.get("SKM_SCAN_FLAT_MAX", "0.02"))
+# (c2: -3 % scan time per iteration at <= 4.4 % changed, +13 % at 40 %; profiles/r2_summary.md)
+FLAT_MAX_CHANGED = float(os.environ.get("SKM_SCAN_FLAT_MAX", "0.05"))
 
 
 def cert_eps(k_dim: int, paired: bool = True) -> float:
