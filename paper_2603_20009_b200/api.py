@@ -26,7 +26,7 @@ from .config import (
     pruning_supported,
     validate_vector_set,
 )
-from .device import on_device, padded_ld, ptr, require_cuda, stream_handle
+from .device import on_device, padded_ld, ptr, require_cuda, stream_handle, to_host
 from .engine import (
     Centroids,
     Comm,
@@ -469,7 +469,7 @@ def fit(x, cfg: KMeansConfig, inspect=None, device=None, comm: Comm | None = Non
     out = res.loop
     phase = dict(res.phase)
     phase["rotation_host"] = job.seconds
-    cent = res.centroids_dev[:, :d].cpu().numpy().copy()
+    cent = to_host(res.centroids_dev[:, :d])
     ld = padded_ld(d)
     peak = 3 * out.assignments.shape[0] * ld + 6 * out.assignments.shape[0] + 4 * cfg.k * ld
     return KMeansResult(
@@ -510,12 +510,12 @@ def _fit_sharded(x, cfg: KMeansConfig, inspect, device, comm: Comm) -> KMeansRes
     full = torch.zeros(n, dtype=torch.int32, device=dev)
     full[lo:hi] = out.assign_dev[:hi - lo]
     comm.allreduce_(full)
-    assignments = full.cpu().numpy()
+    assignments = to_host(full)
     ld = padded_ld(d)
     phase = dict(res.phase)
     phase["rotation_host"] = job.seconds
     return KMeansResult(
-        centroids=res.centroids_dev[:, :d].cpu().numpy().copy(), assignments=assignments, stats=out.stats,
+        centroids=to_host(res.centroids_dev[:, :d]), assignments=assignments, stats=out.stats,
         terminated_by=out.terminated_by, rotation=res.rotation, centroids_rotated=out.centroids_rotated,
         d_prime_final=out.d_prime_final, sample_indices=sidx, init_indices=out.init_indices, work=out.work,
         phase_seconds=phase, peak_aux_values=3 * (hi - lo) * ld + 6 * (hi - lo) + 4 * cfg.k * ld, n_train=n,

@@ -50,6 +50,15 @@ def stream_handle():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor (any strides) -> host NumPy array through one DMA into pinned memory (the
+    array owns the pinned storage; a pageable .cpu() runs at a fraction of the link rate)."""
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
+
+
 def padded_ld(d: int) -> int:
     """Row stride (elements) for device matrices: multiple of 4 so TMA accepts it."""
     return (d + 3) // 4 * 4
