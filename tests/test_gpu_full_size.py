@@ -100,3 +100,20 @@ def test_full_size_trajectory_bitwise(name):
     assert np.array_equal(fa, g["final"].astype(np.int32))
     meta = json.loads(str(g["meta"]))
     print(name, "reference fit on", meta["cpu_count"], "cores:", round(meta["fit_s"], 1), "s")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(HERE, "golden", "full_hier.npz")), reason="no full_hier golden")
+def test_full_size_hierarchical_bitwise():
+    """Hierarchical fit at 1M x 1024 (k_total = 4096: meso_k = 64 groups, batched fine phase)
+    against the real reference (tests/golden/make_golden_hier_full.py): achieved k, every
+    assignment and the centroids bitwise."""
+    import paper_2603_20009_b200 as skb
+    from paper_2603_20009_b200.synth import make_skewed_blobs
+    g = np.load(os.path.join(HERE, "golden", "full_hier.npz"))
+    meta = json.loads(str(g["meta"]))
+    x = make_skewed_blobs(meta["n"], meta["d"], 2 * meta["k_total"], meta["seed"])
+    r = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=meta["k_total"], seed=meta["seed"]))
+    assert r.k == int(g["k"])
+    assert np.array_equal(r.assignments, g["assign"].astype(np.int32))
+    assert np.array_equal(r.centroids[::8], g["cent_sub"])
+    print("reference hierarchical fit:", round(meta["fit_s"], 1), "s on", meta["cpu_count"], "cores")
