@@ -135,3 +135,32 @@ def test_exchange_groups_gives_owners_their_groups_in_row_order(world):
             assert np.array_equal(v["rows"][o:o + members.size], x[members])
         seen.extend(v["gids"].tolist())
     assert sorted(seen) == list(range(len(res[0]["assign"])))  # every row moved exactly once
+
+
+def test_grouped_tile_ranges_and_layout():
+    """grouped.py host helpers: each 128-row tile's N range is the union of its rows' group
+    column ranges (ragged last tile included); the layout's per-row ranges follow the groups."""
+    import numpy as np
+    import torch
+    from paper_2603_20009_b200.grouped import GroupLayout, tile_ranges
+    sizes = np.array([5, 300, 2, 129, 1000, 64], dtype=np.int64)
+    ks = np.array([2, 17, 1, 11, 32, 8], dtype=np.int64)
+    lay = GroupLayout(sizes, ks, torch.device("cpu"))
+    assert lay.n == sizes.sum() and lay.k_total == ks.sum()
+    g = np.repeat(np.arange(len(sizes)), sizes)
+    c0 = np.concatenate(([0], np.cumsum(ks)[:-1]))
+    want = np.stack([c0[g], c0[g] + ks[g]], 1)
+    assert np.array_equal(lay.row_crange.numpy(), want)
+    assert np.array_equal(lay.row_group.numpy(), g)
+    tr = tile_ranges(lay.row_crange).numpy()
+    assert tr.shape == ((lay.n + 127) // 128, 2)
+    for t in range(tr.shape[0]):
+        rows = want[t * 128:(t + 1) * 128]
+        assert tr[t, 0] == rows[:, 0].min() and tr[t, 1] == rows[:, 1].max()
+    # a subset of rows (a d' class) keeps the same contract
+    sub = lay.row_crange[torch.arange(3, 700, 3)]
+    trs = tile_ranges(sub.contiguous()).numpy()
+    s = sub.numpy()
+    for t in range(trs.shape[0]):
+        rows = s[t * 128:(t + 1) * 128]
+        assert trs[t, 0] == rows[:, 0].min() and trs[t, 1] == rows[:, 1].max()
