@@ -775,37 +775,42 @@ class Reducer:
                     cents.ld, stream_handle())
 
     def _chained_sums(self, data, ws, sums: torch.Tensor, chunks: int = 16) -> None:
-        """Rank-order f64 sums, pipelined over cluster chunks: receive rank r-1's running sums of
-        a chunk, continue them over this rank's members, send them on; ranks before the last
-        then contribute zeros to the allreduce."""
-        comm, k, d = self.comm, self.k, self.d
-        r, w = comm.rank, comm.world
-        st = stream_handle()
-        step = -(-k // chunks)
-        nccl = comm.dist.get_backend(comm.group) == "nccl"
-        pending = []
-        for c0 in range(0, k, step):
-            c1 = min(k, c0 + step)
-            seg = sums[c0 * d:c1 * d]
-            if r > 0:
-                if nccl:
-                    comm.dist.recv(seg, src=r - 1, group=comm.group)
-                else:
-                    tmp = torch.empty(seg.shape, dtype=seg.dtype)
-                    comm.dist.recv(tmp, src=r - 1, group=comm.group)
-                    seg.copy_(tmp)
-            native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets[c0:]),
-                        ptr(ws.counts[c0:]), c1 - c0, d, ptr(seg), int(r > 0), None, 0, 1, st,
-                        nbytes=4.0 * data.n * d * (c1 - c0) / k)
-            if r < w - 1:
-                if nccl:
-                    pending.append(comm.dist.isend(seg, dst=r + 1, group=comm.group))
-                else:
-                    comm.dist.send(seg.cpu(), dst=r + 1, group=comm.group)
-        for p_ in pending:
-            p_.wait()
+        chained_cluster_sums(self.comm, data, ws, sums, self.k, self.d, chunks)
+
+
+def chained_cluster_sums(comm: "Comm", data, ws, sums: torch.Tensor, k: int, d: int, chunks: int = 16) -> None:
+    """Rank-order f64 member sums, pipelined over cluster chunks: receive rank r-1's running sums
+    of a chunk, continue them over this rank's members (ascending, ws.order / offsets / counts),
+    send them on; ranks before the last then hold zeros, so an allreduce(sum) of ``sums`` leaves
+    the last rank's chain on every rank -- the reference's serial row order (_kernels.pyx:115-119)
+    when ranks hold ascending row ranges."""
+    r, w = comm.rank, comm.world
+    st = stream_handle()
+    step = -(-k // chunks)
+    nccl = comm.dist.get_backend(comm.group) == "nccl"
+    pending = []
+    for c0 in range(0, k, step):
+        c1 = min(k, c0 + step)
+        seg = sums[c0 * d:c1 * d]
+        if r > 0:
+            if nccl:
+                comm.dist.recv(seg, src=r - 1, group=comm.group)
+            else:
+                tmp = torch.empty(seg.shape, dtype=seg.dtype)
+                comm.dist.recv(tmp, src=r - 1, group=comm.group)
+                seg.copy_(tmp)
+        native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets[c0:]),
+                    ptr(ws.counts[c0:]), c1 - c0, d, ptr(seg), int(r > 0), None, 0, 1, st,
+                    nbytes=4.0 * data.n * d * (c1 - c0) / k)
         if r < w - 1:
-            sums.zero_()
+            if nccl:
+                pending.append(comm.dist.isend(seg, dst=r + 1, group=comm.group))
+            else:
+                comm.dist.send(seg.cpu(), dst=r + 1, group=comm.group)
+    for p_ in pending:
+        p_.wait()
+    if r < w - 1:
+        sums.zero_()
 
 
 # ------------------------------------------------------------------------------ the loop

@@ -41,6 +41,7 @@ from .engine import (
     Workspace,
     _gemm,
     cert_eps,
+    chained_cluster_sums,
     tc_kappa,
 )
 from .hostmath import SPLIT_EPS, adjust_d_prime, init_indices, plan_splits, prune_rate_from_totals
@@ -185,23 +186,47 @@ def ctypes_ref(obj):
 
 
 def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds: list[int], cfg: KMeansConfig,
-                      max_iters: int) -> tuple[torch.Tensor, torch.Tensor, WorkCounters]:
-    """Fit every group of ``data`` (rows laid out group by group, ``sizes[g]`` rows each, all >= 2)
-    into ``ks[g]`` centroids with seed ``seeds[g]``, ``max_iters`` iterations each, exactly as
+                      max_iters: int, comm=None, sizes_global: np.ndarray | None = None,
+                      lo_in_group: np.ndarray | None = None) -> tuple[torch.Tensor, torch.Tensor, WorkCounters]:
+    """Fit every group of ``data`` (rows laid out group by group, ``sizes[g]`` rows each) into
+    ``ks[g]`` centroids with seed ``seeds[g]``, ``max_iters`` iterations each, exactly as
     independent ``fit_rotated_device`` calls would.  Returns (centroids (sum ks, ld) with group g
-    at rows [c0_g, c0_g + k_g), assignments as global centroid rows, merged work counters)."""
+    at rows [c0_g, c0_g + k_g), assignments as global centroid rows, merged work counters).
+
+    Row-sharded (``comm`` with world > 1): this rank holds members
+    [lo_in_group[g], lo_in_group[g] + sizes[g]) of group g's ``sizes_global[g]`` (ranks hold
+    ascending row ranges, so the concatenation over ranks is the group's member list).  The Forgy
+    rows are assembled by one allreduce, and every iteration does ONE allreduce of the packed
+    [centroid sums (f64, chained in rank order with cfg.exact_reduce) | counts | per-group
+    survivors, dims touched, changed] -- the groups' d', convergence and splits are decided on
+    identical global numbers on every rank, so the result is the one-GPU batched result."""
     dev = data.x.device
     d = data.d
     lay = GroupLayout(sizes, ks, dev)
     G, n = lay.G, lay.n
-    assert n == data.n and G > 0 and int(lay.sizes.min()) >= 2
+    sharded = comm is not None and comm.world > 1
+    nglob = np.asarray(sizes_global if sharded else lay.sizes, dtype=np.int64)
+    lo_g = np.asarray(lo_in_group if sharded else np.zeros(G), dtype=np.int64)
+    assert n == data.n and G > 0 and int(nglob.min()) >= 2
     st = stream_handle()
     # Forgy rows of every group from its own stream ([seed_g, 2]), gathered in one launch
-    init = np.concatenate([init_indices(int(lay.sizes[g]), int(lay.ks[g]), [seeds[g], 2]) + lay.starts[g]
-                           for g in range(G)])
-    idx = torch.from_numpy(init.astype(np.int64)).to(dev)
+    # (sharded: each rank gathers the members it holds, one allreduce assembles the rest)
     c = torch.zeros((lay.k_total, data.ld), dtype=torch.float32, device=dev)
-    native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(idx), lay.k_total, data.ld, ptr(c), data.ld, st)
+    src_rows, dst_rows = [], []
+    for g in range(G):
+        idx_g = init_indices(int(nglob[g]), int(lay.ks[g]), [seeds[g], 2])
+        mine = np.flatnonzero((idx_g >= lo_g[g]) & (idx_g < lo_g[g] + lay.sizes[g]))
+        src_rows.append(idx_g[mine] - lo_g[g] + lay.starts[g])
+        dst_rows.append(mine + lay.c0[g])
+    src = np.concatenate(src_rows).astype(np.int64)
+    dst = np.concatenate(dst_rows).astype(np.int64)
+    if src.size:
+        tmp = torch.empty((src.size, data.ld), dtype=torch.float32, device=dev)
+        native.call("skm_gather_rows", ptr(data.x), data.ld, ptr(torch.from_numpy(src).to(dev)), int(src.size),
+                    data.ld, ptr(tmp), data.ld, st)
+        c.index_copy_(0, torch.from_numpy(dst).to(dev), tmp)
+    if sharded:
+        comm.allreduce_(c)  # every Forgy row is held by exactly one rank
     cents = Centroids(c, d)
     kmax = int(lay.ks.max())
     wcfg = KMeansConfig(k=lay.k_total, max_iters=max_iters, seed=cfg.seed, gemm_backend=cfg.gemm_backend,
@@ -217,8 +242,13 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
     final_c = torch.zeros_like(c)  # each group's centroids as its own loop ends
     pin_g = torch.empty((G, 3), dtype=torch.int64, pin_memory=True)
     pin_counts = torch.empty(lay.k_total, dtype=torch.int32, pin_memory=True)
-    nk = lay.sizes * lay.ks
+    nk = nglob * lay.ks
     last_changed = None
+    if sharded:
+        K = lay.k_total
+        red = torch.zeros(K * d + K + 3 * G, dtype=torch.float64, device=dev)
+        pin_red = torch.empty(K + 3 * G, dtype=torch.float64, pin_memory=True)
+        counts64 = torch.empty(K, dtype=torch.int64, device=dev)
 
     for it in range(1, max_iters + 1):
         act = np.flatnonzero(active)
@@ -243,7 +273,7 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
         else:
             native.call("skm_seed_thresholds", ptr(data.x), data.ld, ptr(cents.c), cents.ld, ptr(ws.assign), n, d,
                         ptr(ws.tau), st, nbytes=4.0 * n * d + 8.0 * n)
-            ws.flat = last_changed is not None and last_changed <= FLAT_MAX_CHANGED * int(lay.sizes[act].sum())
+            ws.flat = last_changed is not None and last_changed <= FLAT_MAX_CHANGED * int(nglob[act].sum())
             for dp in np.unique(dprime[act]):
                 cls = act[dprime[act] == dp]
                 plan = PrunePlan(d, int(dp), cfg.epsilon0, cfg.pruning_sentinel, dev)
@@ -259,17 +289,40 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
                 _grouped_pruned_pass(data, cents, ws, plan, lay, rmap.contiguous(), gcount)
                 work.front_pair_dims += int((nk[cls] * dp).sum())
                 if not cfg.pruning_sentinel:
-                    work.seed_dims += int((lay.sizes[cls] * d).sum())
+                    work.seed_dims += int((nglob[cls] * d).sum())
         # stable cluster sort of every row (groups own disjoint column ranges, so the order is
         # group by group, members ascending) + one readback of counts and group counters
-        native.call("skm_cluster_sort", ptr(ws.assign), n, lay.k_total, ptr(ws.order), ptr(ws.counts),
-                    ptr(ws.offsets), ptr(ws.sort_ws), ws.sort_ws.numel(), st, nbytes=32.0 * n)
-        pin_g.copy_(gcount, non_blocking=True)
-        pin_counts.copy_(ws.counts, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-        gc = pin_g.numpy().copy()
+        if n:
+            native.call("skm_cluster_sort", ptr(ws.assign), n, lay.k_total, ptr(ws.order), ptr(ws.counts),
+                        ptr(ws.offsets), ptr(ws.sort_ws), ws.sort_ws.numel(), st, nbytes=32.0 * n)
+        else:
+            ws.counts.zero_()
+            ws.offsets.zero_()
+        if sharded:
+            # the iteration's one collective: [sums | counts | group counters], sums chained in
+            # rank order (exact) or per-rank partials added by the allreduce
+            K = lay.k_total
+            sums = red[:K * d]
+            if cfg.exact_reduce:
+                chained_cluster_sums(comm, data, ws, sums, K, d)
+            else:
+                native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets),
+                            ptr(ws.counts), K, d, ptr(sums), 0, None, 0, 1, st, nbytes=4.0 * n * d)
+            red[K * d:K * d + K].copy_(ws.counts.to(torch.float64))
+            red[K * d + K:].copy_(gcount.view(-1).to(torch.float64))
+            comm.allreduce_(red)
+            pin_red.copy_(red[K * d:], non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            h = pin_red.numpy()
+            counts = np.rint(h[:K]).astype(np.int64)
+            gc = np.rint(h[K:]).astype(np.int64).reshape(G, 3)
+        else:
+            pin_g.copy_(gcount, non_blocking=True)
+            pin_counts.copy_(ws.counts, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            gc = pin_g.numpy().copy()
+            counts = pin_counts.numpy().astype(np.int64)
         last_changed = int(gc[act, 2].sum()) if it > 1 else None
-        counts = pin_counts.numpy().astype(np.int64)
         stop_now = np.zeros(G, dtype=bool)
         if it > 1:
             stop_now[act] = gc[act, 2] == 0  # converged: no update, no split (core.py:358-363)
@@ -279,9 +332,13 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
         # means after earlier splits): keep them as they are now
         _freeze(final_c, cents.c, lay, np.flatnonzero(stop_now))
         # update of every centroid (the groups that stopped are not read again)
-        native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts),
-                    lay.k_total, d, None, 0, ptr(cents.c), cents.ld, 0, st,
-                    nbytes=4.0 * n * d + 4.0 * lay.k_total * d)
+        if sharded:
+            counts64.copy_(torch.from_numpy(counts))
+            native.call("skm_finalize_centroids", ptr(red), ptr(counts64), lay.k_total, d, ptr(cents.c), cents.ld, st)
+        else:
+            native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts),
+                        lay.k_total, d, None, 0, ptr(cents.c), cents.ld, 0, st,
+                        nbytes=4.0 * n * d + 4.0 * lay.k_total * d)
         empties, donors = [], []
         for g in act:
             if stop_now[g]:
@@ -292,7 +349,7 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
                 empties += [c0 + v for v in e]
                 donors += [c0 + v for v in dn]
             if pruned_iter:
-                rate = prune_rate_from_totals(int(gc[g, 0]), int(lay.sizes[g]), int(lay.ks[g]))
+                rate = prune_rate_from_totals(int(gc[g, 0]), int(nglob[g]), int(lay.ks[g]))
                 dprime[g] = adjust_d_prime(int(dprime[g]), rate, cfg, d)
         if empties:
             e_t = torch.tensor(empties, dtype=torch.int32, device=dev)
