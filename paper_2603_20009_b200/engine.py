@@ -731,9 +731,25 @@ class Reducer:
         self.o_cnt = k * d
         self.o_scal = self.o_cnt + k
         self.o_tau = self.o_scal + 3
-        self.buf = torch.zeros(self.o_tau + self.n_chunks, dtype=torch.float64, device=dev)
-        self.pin = torch.empty(self.buf.numel() - self.o_cnt, dtype=torch.float64, pin_memory=True)
+        self.o_gt = self.o_tau + self.n_chunks
+        self.n_gt = 0
+        self.gt_slots = self.gt_rows = self.gt_assign = None
+        self.buf = torch.zeros(self.o_gt, dtype=torch.float64, device=dev)
+        self.pin = torch.empty(self.o_gt - self.o_cnt, dtype=torch.float64, pin_memory=True)
         self.counts64 = torch.empty(k, dtype=torch.int64, device=dev)
+        self.row_lo, self.n_local = row_lo, n_local
+
+    def attach_etr(self, gt_idx: torch.Tensor, top_k: int) -> None:
+        """ETR without a second collective: the assignments of the ground-truth rows (nq x top_k
+        slots, each held by exactly one rank) ride in the iteration's allreduce, so every rank
+        tallies every query's hits locally after the update (core.py:379-399)."""
+        gi = gt_idx[:, :top_k].reshape(-1).to(torch.int64)
+        mine = (gi >= self.row_lo) & (gi < self.row_lo + self.n_local)
+        self.gt_slots = torch.nonzero(mine).flatten()
+        self.gt_rows = gi[self.gt_slots] - self.row_lo
+        self.n_gt = int(gi.numel())
+        extra = torch.zeros(self.n_gt, dtype=torch.float64, device=self.buf.device)
+        self.buf = torch.cat([self.buf[:self.o_gt], extra])
 
     def reduce(self, data: "DeviceData", ws: "Workspace", n_local: int) -> tuple[np.ndarray, float, float, float, float]:
         """Local stats + sorted sums -> one allreduce -> (counts, wcss, n_changed, survivors, touched)."""
@@ -751,6 +767,10 @@ class Reducer:
         buf[self.o_scal + 1] = ws.counters[0].to(torch.float64)
         buf[self.o_scal + 2] = ws.counters[1].to(torch.float64)
         buf[self.o_cnt:self.o_scal].copy_(ws.counts.to(torch.float64))
+        if self.n_gt:
+            gt = buf[self.o_gt:]
+            gt.zero_()
+            gt[self.gt_slots] = ws.assign[self.gt_rows].to(torch.float64)
         sums = buf[:self.o_cnt]
         if self.exact and self.comm.world > 1:
             self._chained_sums(data, ws, sums)
@@ -758,7 +778,9 @@ class Reducer:
             native.call("skm_cluster_sums", ptr(data.x), data.ld, ptr(ws.order), ptr(ws.offsets), ptr(ws.counts), k,
                         d, ptr(sums), 0, None, 0, 1, st, nbytes=4.0 * data.n * d)
         self.comm.allreduce_(buf)
-        self.pin.copy_(buf[self.o_cnt:], non_blocking=True)
+        if self.n_gt:
+            self.gt_assign = buf[self.o_gt:].to(torch.int32)  # every GT row's assignment, all ranks
+        self.pin.copy_(buf[self.o_cnt:self.o_gt], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         h = self.pin.numpy()
         counts = np.rint(h[:k]).astype(np.int64)
@@ -864,6 +886,8 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         etr.setup(data, comm, n_global=n, row_lo=row_lo)
         timer.stop("ground_truth")
     reducer = Reducer(comm, k, d, n, row_lo, n_local, dev, cfg.exact_reduce) if comm.world > 1 else None
+    if reducer is not None and etr is not None:
+        reducer.attach_etr(etr.gt_idx, etr.top_k)
     scal = torch.zeros(4, dtype=torch.float64, device=dev)
     pin_scal = torch.empty(4, dtype=torch.float64, pin_memory=True)
     pin_counts = torch.empty(k, dtype=torch.int32, pin_memory=True)
@@ -961,7 +985,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
         recall = None
         if etr is not None:
             timer.start("etr")
-            recall = etr.probe(data, cents, ws, comm)
+            recall = etr.probe(data, cents, ws, comm, gt_assign=reducer.gt_assign if reducer is not None else None)
             timer.stop("etr")
             recall_history.append(recall)
         stats.append(IterationStats(iter_index=it, wcss=wcss, n_empty_splits=n_splits,

@@ -188,14 +188,25 @@ class EtrState:
         self.gt_idx, self.gt_val = gi.contiguous(), gv.contiguous()
         self.hits = torch.zeros(nq, dtype=torch.int32, device=dev)
 
-    def probe(self, data, cents, ws, comm) -> float:
+    def probe(self, data, cents, ws, comm, gt_assign: torch.Tensor | None = None) -> float:
+        """Recall of this iteration (evaluation.py:142-170).  ``gt_assign``: the assignments of
+        every ground-truth slot, delivered by the iteration's one allreduce at N > 1 (engine.Reducer)
+        -- the tally is then local on every rank and needs no collective of its own."""
         nq = self.q.shape[0]
         c_sq = _norms(cents.c, cents.d)
         pi, _ = device_topk_distances(self.q, None, None, self.q_sq, cents.c, None, None, c_sq, cents.d, self.nprobe)
-        native.call("skm_etr_hits", ptr(self.gt_idx), self.gt_idx.shape[1], self.top_k, ptr(pi), pi.shape[1],
-                    pi.shape[1], ptr(ws.assign), self.row_lo, self.row_hi, cents.k, nq, ptr(self.hits),
-                    stream_handle())
-        h = comm.allreduce_(self.hits.to(torch.int64)) if comm.world > 1 else self.hits
+        if gt_assign is not None:
+            # slots as rows: slot s of query q holds gt_assign[q * top_k + t]
+            if getattr(self, "_slots", None) is None:
+                self._slots = torch.arange(nq * self.top_k, dtype=torch.int32, device=self.q.device).view(nq, -1)
+            native.call("skm_etr_hits", ptr(self._slots), self.top_k, self.top_k, ptr(pi), pi.shape[1], pi.shape[1],
+                        ptr(gt_assign), 0, nq * self.top_k, cents.k, nq, ptr(self.hits), stream_handle())
+            h = self.hits
+        else:
+            native.call("skm_etr_hits", ptr(self.gt_idx), self.gt_idx.shape[1], self.top_k, ptr(pi), pi.shape[1],
+                        pi.shape[1], ptr(ws.assign), self.row_lo, self.row_hi, cents.k, nq, ptr(self.hits),
+                        stream_handle())
+            h = comm.allreduce_(self.hits.to(torch.int64)) if comm.world > 1 else self.hits
         hits = h.cpu().numpy()
         total = 0.0
         for v in hits:  # the reference's accumulation order (evaluation.py:169-170)
