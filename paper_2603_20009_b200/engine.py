@@ -536,8 +536,18 @@ class PrunePlan:
         self.nb = len(widths)
         self.d_prime = d_prime
         self.sentinel = sentinel
-        self.theta = torch.tensor(self.gate, dtype=torch.float32, device=dev)
-        self.bdims = torch.tensor(widths, dtype=torch.int32, device=dev)
+        key = (str(dev), d, d_prime, float(eps0), bool(sentinel))
+        cached = _PLAN_TENSORS.get(key)
+        if cached is None:  # device copies of the constants, uploaded once per (d, d', mode)
+            cached = (torch.tensor(self.gate, dtype=torch.float32, device=dev),
+                      torch.tensor(widths, dtype=torch.int32, device=dev))
+            if len(_PLAN_TENSORS) > 256:
+                _PLAN_TENSORS.clear()
+            _PLAN_TENSORS[key] = cached
+        self.theta, self.bdims = cached
+
+
+_PLAN_TENSORS: dict = {}
 
 
 def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: PrunePlan, seed_tau: bool = True,
