@@ -419,10 +419,6 @@ def main():
                        "contract) beside the copy, fit, D2H of centroids + assignments" if world == 1 else
                        "per rank: H2D of the shard, host QR beside it, sharded fit, D2H of centroids + assignments"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(args, x_host)
-
     extra = None
     if world == 1 and not args.no_extra:
         extra = {}
@@ -464,6 +460,12 @@ def main():
 
     if world == 1 and not args.no_extra and "c5" in args.extra.split(","):
         extra["c5"] = run_c5(dev)
+
+    # the host-CPU reference sample runs last: its BLAS threads must not compete with the host
+    # orchestration of the (launch-bound) small secondary configs above
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args, x_host)
 
     if rank == 0:
         line = {
