@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(CH_THREADS, SKM_CHAIN_MINB) sgemm_chain_kernel
 #ifndef SKM_KN_BK
 #define SKM_KN_BK 32
 #endif
+#ifndef SKM_KN_PREFETCH
+#define SKM_KN_PREFETCH 1
+#endif
 constexpr int KN_STAGES = SKM_KN_STAGES;
 constexpr int KN_BK = SKM_KN_BK;   // k depth of one pipeline stage
 constexpr int KN_ALD = KN_BK + 4;  // A row stride in floats (80 B: 16-B aligned chunks, rows 4 apart hit other banks)
@@ -390,6 +393,34 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
       bv[0] = b03.x; bv[1] = b03.y; bv[2] = b47.x; bv[3] = b47.y;
     };
     if (kt < kfull) {
+#if SKM_KN_PREFETCH
+      // fragments of step k2 + 2 are loaded while step k2's FFMA2s run
+      float2 fa[2][8];
+      unsigned long long fb0[2][4], fb1[2][4];
+      auto frag = [&](int k2, float2* av, unsigned long long* b0, unsigned long long* b1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+          av[i] = *reinterpret_cast<const float2*>(A + r * KN_ALD + k2);
+        }
+        bload(k2, b0);
+        bload(k2 + 1, b1);
+      };
+      frag(0, fa[0], fb0[0], fb1[0]);
+#pragma unroll
+      for (int k2 = 0; k2 < KN_BK; k2 += 2) {
+        const int cb = (k2 >> 1) & 1;
+        if (k2 + 2 < KN_BK) frag(k2 + 2, fa[cb ^ 1], fb0[cb ^ 1], fb1[cb ^ 1]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(fa[cb][i].x, fb0[cb][j], acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(fa[cb][i].y, fb1[cb][j], acc[i][j]);
+      }
+#else
 #pragma unroll
       for (int k2 = 0; k2 < KN_BK; k2 += 2) {
         float2 av[8];
@@ -410,6 +441,7 @@ __global__ void __launch_bounds__(CH_THREADS, 2) sgemm_chain_kn_kernel(const Cha
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = chain_step_bcast<FLAVOUR>(av[i].y, b1[j], acc[i][j]);
       }
+#endif
     } else {
       // ragged last tile: the zero-filled columns past K must not enter the chain
 #pragma unroll 1
