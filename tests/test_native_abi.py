@@ -56,3 +56,21 @@ def test_no_cpu_fallback_without_library(monkeypatch):
     monkeypatch.setattr(native, "LIB_PATH", "/nonexistent/libskm_b200.so")
     with pytest.raises(native.NativeUnavailable):
         native.load()
+
+
+def test_drop_in_names_cover_the_reference_api():
+    """Every public name of the reference package (its __all__, pkg/src/superkmeans/__init__.py)
+    exists in ours (checked against the unmodified install in baseline/_ref when present)."""
+    import importlib
+    import os
+    import subprocess
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "superkmeans")):
+        pytest.skip("reference not installed (baseline/_ref)")
+    out = subprocess.run([sys.executable, "-c", "import superkmeans as s; print(' '.join(s.__all__))"],
+                         capture_output=True, text=True, env=dict(os.environ, PYTHONPATH=ref), check=True)
+    names = out.stdout.split()
+    ours = importlib.import_module("paper_2603_20009_b200")
+    assert len(names) >= 40
+    assert [n for n in names if not hasattr(ours, n)] == []
