@@ -204,6 +204,51 @@ def cpu_baseline_sample(args, x: np.ndarray) -> dict | None:
                       f"--impl reference arm times all iterations"}
 
 
+def run_extra(name: str, dev) -> dict:
+    """One secondary BASELINE config (EXTRA[name]) at N = 1: the reference generator's rows,
+    one warm-up fit, the median of 2 timed fits (CUDA events)."""
+    import torch
+    from paper_2603_20009_b200 import api
+    from paper_2603_20009_b200.config import EtrConfig, KMeansConfig
+    from paper_2603_20009_b200.device import to_device_matrix
+    from paper_2603_20009_b200.hostmath import generate_rotation
+    gen, n, d, centers, k, iters, etr = EXTRA[name]
+    t0 = time.perf_counter()
+    xh = make_rows(gen, n, d, centers, 0)
+    xd = to_device_matrix(xh, device=dev)
+    del xh
+    gs = time.perf_counter() - t0
+    ccfg = KMeansConfig(k=k, max_iters=iters, seed=0,
+                        etr=EtrConfig(n_queries=etr[0], top_k=etr[1]) if etr else None)
+    rot = generate_rotation(d, 0)
+    r = api.fit_device(xd, d, ccfg, rot)  # warm-up
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(2):
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        r = api.fit_device(xd, d, ccfg, rot)
+        a1.record()
+        torch.cuda.synchronize()
+        times.append(a0.elapsed_time(a1))
+    s2 = r.loop.stats
+    ms = float(np.median(times))
+    out = {
+        "workload": f"{'make_blobs' if gen == 'blobs' else 'make_skewed_blobs'}({n}, {d}, {centers}, seed=0), "
+                    f"k={k}, max_iters={iters}" + (f", ETR(n_queries={etr[0]}, top_k={etr[1]})" if etr else ""),
+        "ms_per_fit": round(ms, 2), "iterations": len(s2), "iter_per_s": round(len(s2) / (ms * 1e-3), 2),
+        "terminated_by": r.loop.terminated_by, "d_prime": [s.d_prime for s in s2],
+        "prune_rate": [None if s.prune_rate_after_gemm is None else round(s.prune_rate_after_gemm, 5)
+                       for s in s2],
+        "pruned_dim_fraction": [None if s.d_prime is None else
+                                round(1.0 - s.tail_dims_touched / (n * k * (d - s.d_prime)), 6) for s in s2],
+        "recall_history": [round(v, 4) for v in r.loop.recall_history], "data_gen_s": round(gs, 1),
+    }
+    del xd
+    return out
+
+
 def run_c5(dev) -> dict:
     """BASELINE c5: hierarchical k-means of 10M x 1024 into k_total = 65536 with meso_k = 430
     (the reference's rule caps near 50.7K at meso_k = 256), rows generated on the GPU
@@ -389,77 +434,55 @@ def main():
     # ---- end to end through the public entry (api.fit) with pinned host input ----
     e2e = None
     if not args.no_e2e:
-        host = torch.empty((hi - lo, args.d), dtype=torch.float32, pin_memory=True)
-        host.numpy()[:] = x_host
-        ee0 = torch.cuda.Event(enable_timing=True)
-        ee1 = torch.cuda.Event(enable_timing=True)
-        barrier()
-        ee0.record()
-        d2h = 0
-        iters_e2e = 0
-        for _ in range(args.steps):
-            if world == 1:
-                r = api.fit(host, cfg)  # H2D (one DMA) + host QR beside it + fit + D2H of the result
-                d2h = r.centroids.nbytes + r.assignments.nbytes + r.centroids_rotated.nbytes
-                iters_e2e += len(r.stats)
-            else:
-                job = api._RotationJob(args.d, args.seed)
-                xe = torch.zeros_like(x)
-                xe[:, :args.d].copy_(host, non_blocking=True)
-                r = api.fit_device(xe, args.d, cfg, job, comm=comm, n_global=args.n, row_lo=lo, consume_input=True)
-                cent = r.centroids_dev[:, :args.d].cpu()
-                d2h = cent.numel() * 4 + r.loop.assignments.nbytes
-                iters_e2e += len(r.loop.stats)
-        ee1.record()
-        barrier()
-        e2e_s = max_over_ranks(ee0.elapsed_time(ee1) / 1e3)
-        e2e = {"value": iters_e2e / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": int(host.numel() * 4) * world, "d2h_bytes_per_step": int(d2h) * world,
-               "note": "api.fit on a pinned host matrix: H2D (one DMA), host QR of R (LAPACK, the persisted-model "
-                       "contract) beside the copy, fit, D2H of centroids + assignments" if world == 1 else
-                       "per rank: H2D of the shard, host QR beside it, sharded fit, D2H of centroids + assignments"}
+        try:
+            host = torch.empty((hi - lo, args.d), dtype=torch.float32, pin_memory=True)
+            host.numpy()[:] = x_host
+            ee0 = torch.cuda.Event(enable_timing=True)
+            ee1 = torch.cuda.Event(enable_timing=True)
+            barrier()
+            ee0.record()
+            d2h = 0
+            iters_e2e = 0
+            for _ in range(args.steps):
+                if world == 1:
+                    r = api.fit(host, cfg)  # H2D (one DMA) + host QR beside it + fit + D2H of the result
+                    d2h = r.centroids.nbytes + r.assignments.nbytes + r.centroids_rotated.nbytes
+                    iters_e2e += len(r.stats)
+                else:
+                    job = api._RotationJob(args.d, args.seed)
+                    xe = torch.zeros_like(x)
+                    xe[:, :args.d].copy_(host, non_blocking=True)
+                    r = api.fit_device(xe, args.d, cfg, job, comm=comm, n_global=args.n, row_lo=lo, consume_input=True)
+                    cent = r.centroids_dev[:, :args.d].cpu()
+                    d2h = cent.numel() * 4 + r.loop.assignments.nbytes
+                    iters_e2e += len(r.loop.stats)
+            ee1.record()
+            barrier()
+            e2e_s = max_over_ranks(ee0.elapsed_time(ee1) / 1e3)
+            e2e = {"value": iters_e2e / e2e_s, "unit": UNIT,
+                   "h2d_bytes_per_step": int(host.numel() * 4) * world, "d2h_bytes_per_step": int(d2h) * world,
+                   "note": "api.fit on a pinned host matrix: H2D (one DMA), host QR of R (LAPACK, the persisted-model "
+                           "contract) beside the copy, fit, D2H of centroids + assignments" if world == 1 else
+                           "per rank: H2D of the shard, host QR beside it, sharded fit, D2H of centroids + assignments"}
+
+        except Exception as exc:  # reported in the line instead of losing the device-timed value
+            e2e = {"value": None, "unit": UNIT, "error": f"{type(exc).__name__}: {exc}"[:300]}
 
     extra = None
     if world == 1 and not args.no_extra:
         extra = {}
         for name in [c for c in args.extra.split(",") if c in EXTRA]:
-            gen, n, d, centers, k, iters, etr = EXTRA[name]
-            t0 = time.perf_counter()
-            xh = make_rows(gen, n, d, centers, 0)
-            xd = to_device_matrix(xh, device=dev)
-            del xh
-            gs = time.perf_counter() - t0
-            ccfg = KMeansConfig(k=k, max_iters=iters, seed=0,
-                                etr=EtrConfig(n_queries=etr[0], top_k=etr[1]) if etr else None)
-            rot = generate_rotation(d, 0)
-            r = api.fit_device(xd, d, ccfg, rot)  # warm-up
-            torch.cuda.synchronize()
-            times = []
-            for _ in range(2):
-                a0 = torch.cuda.Event(enable_timing=True)
-                a1 = torch.cuda.Event(enable_timing=True)
-                a0.record()
-                r = api.fit_device(xd, d, ccfg, rot)
-                a1.record()
-                torch.cuda.synchronize()
-                times.append(a0.elapsed_time(a1))
-            s2 = r.loop.stats
-            ms = float(np.median(times))
-            extra[name] = {
-                "workload": f"{'make_blobs' if gen == 'blobs' else 'make_skewed_blobs'}({n}, {d}, {centers}, seed=0), "
-                            f"k={k}, max_iters={iters}" + (f", ETR(n_queries={etr[0]}, top_k={etr[1]})" if etr else ""),
-                "ms_per_fit": round(ms, 2), "iterations": len(s2), "iter_per_s": round(len(s2) / (ms * 1e-3), 2),
-                "terminated_by": r.loop.terminated_by, "d_prime": [s.d_prime for s in s2],
-                "prune_rate": [None if s.prune_rate_after_gemm is None else round(s.prune_rate_after_gemm, 5)
-                               for s in s2],
-                "pruned_dim_fraction": [None if s.d_prime is None else
-                                        round(1.0 - s.tail_dims_touched / (n * k * (d - s.d_prime)), 6) for s in s2],
-                "recall_history": [round(v, 4) for v in r.loop.recall_history], "data_gen_s": round(gs, 1),
-            }
-            del xd
+            try:
+                extra[name] = run_extra(name, dev)
+            except Exception as exc:  # one config failing must not cost the headline line
+                extra[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                torch.cuda.empty_cache()
 
     if world == 1 and not args.no_extra and "c5" in args.extra.split(","):
-        extra["c5"] = run_c5(dev)
+        try:
+            extra["c5"] = run_c5(dev)
+        except Exception as exc:
+            extra["c5"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     # the host-CPU reference sample runs last: its BLAS threads must not compete with the host
     # orchestration of the (launch-bound) small secondary configs above
