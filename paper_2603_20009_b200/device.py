@@ -47,7 +47,10 @@ def ptr(t: torch.Tensor | None):
 
 
 def stream_handle():
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    """The current CUDA stream of the current device as a raw handle (the fast path of
+    torch.cuda.current_stream().cuda_stream: ~15x cheaper per call, which matters for the
+    launch-bound small fits and the per-group host work)."""
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
