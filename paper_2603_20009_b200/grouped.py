@@ -11,15 +11,17 @@ kernel per iteration ("batched K2/K3/K4 over groups"):
     columns (``row_crange``) and each 128-row tile walks only the N tiles its rows' groups cover
     (``tile_nrange``); the exact settle of near-ties runs on the same grouped ranges;
   * pruned iterations run one grouped GATE GEMM + scan per distinct d' among the active groups
-    (every group starts at the same d', the controller moves them in 64-wide steps, so there are
-    one to three classes); the scan adds each row's survivors / dims touched / changed into its
-    group's counters;
-  * the update is the ordinary stable cluster sort + ordered member sums over all centroids (a
-    group that stopped keeps its assignment, so its centroids are recomputed bit-identically),
+    (every group starts at the same d' and the controller moves each by +-20 %, so there are a
+    few classes); the scan adds each row's survivors / dims touched / changed into its group's
+    counters;
+  * the update is the ordinary stable cluster sort + ordered member sums over all centroids;
+    a group that stops (converged, or its last iteration) has its centroids frozen at that
+    point, exactly where its own loop would have left them, and its rows leave the passes;
     splits and d' are decided per group on the host from one readback per iteration.
 
 Every per-row operation is the single-group loop's (engine.py), so each group's centroids and
-assignments are bitwise those of its own fit -- and of the reference.
+assignments are bitwise those of its own fit -- and of the reference.  Row-sharded
+every rank runs the same loop on its members, with one packed allreduce per iteration.
 """
 
 from __future__ import annotations

@@ -38,6 +38,8 @@ FULL_CASES = {
     "c1": ("blobs", (100_000, 128, 256, 0), dict(k=256, max_iters=10, seed=0), 1, 1),
     "c2": ("skewed", (1_000_000, 1536, 8192, 0), dict(k=4096, max_iters=10, seed=0), 10, 8),
     "c4k1024": ("skewed", (1_000_000, 768, 2048, 0), dict(k=1024, max_iters=10, seed=0), 10, 4),
+    "c4k4096": ("skewed", (1_000_000, 768, 8192, 0), dict(k=4096, max_iters=10, seed=0), 10, 8),
+    "c4k16384": ("skewed", (1_000_000, 768, 32768, 0), dict(k=16384, max_iters=10, seed=0), 10, 16),
     # BASELINE c3: ETR on 1000 queries, recall@10; "etr" = (n_queries, top_k)
     "c3": ("skewed", (1_000_000, 1024, 32768, 0), dict(k=16384, max_iters=25, seed=0, etr=(1000, 10)), 10, 16),
 }

@@ -39,7 +39,7 @@ def _input(name):
     return make_blobs(*args) if gen == "blobs" else make_skewed_blobs(*args)
 
 
-@pytest.mark.parametrize("name", [c for c in ["c1", "c2", "c4k1024", "c3"]
+@pytest.mark.parametrize("name", [c for c in ["c1", "c2", "c4k1024", "c4k4096", "c4k16384", "c3"]
                                   if os.path.exists(os.path.join(HERE, "golden", f"full_{c}.npz"))])
 def test_full_size_trajectory_bitwise(name):
     import paper_2603_20009_b200 as skb
