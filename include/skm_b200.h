@@ -37,6 +37,8 @@ extern "C" {
 #define SKM_E_WORKSPACE (-4)
 
 const char* skm_last_error(void);
+/* cumulative count of kernels this library has launched (all devices) */
+long long skm_kernel_launches(void);
 int skm_abi_version(void);
 
 /* ---- layout / preprocessing --------------------------------------------------------- */

@@ -1,3 +1,4 @@
+#include <atomic>
 // extern "C" entry points of libskm_b200.so (declared in include/skm_b200.h).
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -29,6 +30,9 @@ int cuda_fail(cudaError_t e, const char* where) {
   g_err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
   return SKM_E_CUDA;
 }
+// every kernel launch of the library is counted (skm_kernel_launches: bench.py's gpu_launches)
+static std::atomic<long long> g_kernel_launches{0};
+#define SKM_COUNT_LAUNCH() g_kernel_launches.fetch_add(1, std::memory_order_relaxed)
 #define SKM_LAUNCH_CHECK(where)                         \
   do {                                                  \
     cudaError_t _e = cudaGetLastError();                \
@@ -160,7 +164,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   const long long blocks = static_cast<long long>((p->M + skm::GEMM_BM - 1) / skm::GEMM_BM) * split;
   if (blocks > 0x7fffffffLL) return fail(SKM_E_ARG, "gemm: grid too large");
   dim3 grid(static_cast<unsigned>(blocks));
-  kern<<<grid, skm::GEMM_THREADS, L::TOTAL, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, te_a_hi, te_a_lo, te_b_hi, te_b_lo, a);
+  { kern<<<grid, skm::GEMM_THREADS, L::TOTAL, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, te_a_hi, te_a_lo, te_b_hi, te_b_lo, a); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("gemm_tf32x3 launch");
   return SKM_OK;
 }
@@ -180,7 +184,7 @@ int launch_chain(const skm::ChainArgs& g, cudaStream_t st) {
   }
   dim3 grid((g.N + skm::CH_BN - 1) / skm::CH_BN, (g.M + skm::CH_BM - 1) / skm::CH_BM);
   if (grid.y > 65535) return fail(SKM_E_ARG, "chain_gemm: too many row tiles for one launch");
-  kern<<<grid, skm::CH_THREADS, skm::chain_smem_bytes(), st>>>(g);
+  { kern<<<grid, skm::CH_THREADS, skm::chain_smem_bytes(), st>>>(g); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("chain_gemm launch");
   return SKM_OK;
 }
@@ -196,7 +200,7 @@ int launch_chain_kn(const skm::ChainArgs& g, cudaStream_t st) {
   }
   dim3 grid((g.N + skm::CH_BN - 1) / skm::CH_BN, (g.M + skm::CH_BM - 1) / skm::CH_BM);
   if (grid.y > 65535) return fail(SKM_E_ARG, "chain_gemm: too many row tiles for one launch");
-  kern<<<grid, skm::CH_THREADS, skm::chain_kn_smem_bytes(), st>>>(g);
+  { kern<<<grid, skm::CH_THREADS, skm::chain_kn_smem_bytes(), st>>>(g); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("chain_gemm_kn launch");
   return SKM_OK;
 }
@@ -261,7 +265,7 @@ static int launch_chain_topk(const skm::ChainTopkArgs& g, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "chain_topk smem attribute");
   }
   dim3 grid(static_cast<unsigned>(g.n_tiles), static_cast<unsigned>((g.N + skm::CH_BN - 1) / skm::CH_BN));
-  kern<<<grid, skm::CH_THREADS, skm::chain_topk_smem_bytes(), st>>>(g);
+  { kern<<<grid, skm::CH_THREADS, skm::chain_topk_smem_bytes(), st>>>(g); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("chain_topk launch");
   return SKM_OK;
 }
@@ -288,6 +292,7 @@ extern "C" int skm_chain_topk_tiles(const float* rows, long long ldr, const floa
 extern "C" {
 
 const char* skm_last_error(void) { return g_err.c_str(); }
+long long skm_kernel_launches(void) { return g_kernel_launches.load(std::memory_order_relaxed); }
 int skm_abi_version(void) { return 1; }
 
 int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi, float* lo, long long ldo,
@@ -298,22 +303,22 @@ int skm_split_hilo(const float* x, long long ldx, int rows, int cols, float* hi,
       (reinterpret_cast<uintptr_t>(hi) & 15) == 0 && (reinterpret_cast<uintptr_t>(lo) & 15) == 0) {
     const long long ldo4 = ldo / 4;
     dim3 grid(static_cast<unsigned>((ldo4 + 127) / 128), static_cast<unsigned>(std::min(rows, 16384)));
-    skm::split_hilo_vec_kernel<<<grid, 128, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(x), ldx / 4, rows,
+    { skm::split_hilo_vec_kernel<<<grid, 128, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(x), ldx / 4, rows,
                                                                      cols, reinterpret_cast<float4*>(hi),
-                                                                     reinterpret_cast<float4*>(lo), ldo4);
+                                                                     reinterpret_cast<float4*>(lo), ldo4); SKM_COUNT_LAUNCH(); }
     SKM_LAUNCH_CHECK("split_hilo");
     return SKM_OK;
   }
-  skm::split_hilo_kernel<<<grid_for((long long)rows * ldo, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, hi,
-                                                                                             lo, ldo);
+  { skm::split_hilo_kernel<<<grid_for((long long)rows * ldo, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, hi,
+                                                                                             lo, ldo); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("split_hilo");
   return SKM_OK;
 }
 
 int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* out, void* stream) {
   if (rows <= 0) return SKM_OK;
-  skm::row_sq_norms_einsum_kernel<<<grid_for(rows, 128, 148 * 64), 128, 0, as_stream(stream)>>>(x, ldx, rows, dims,
-                                                                                                out);
+  { skm::row_sq_norms_einsum_kernel<<<grid_for(rows, 128, 148 * 64), 128, 0, as_stream(stream)>>>(x, ldx, rows, dims,
+                                                                                                out); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("row_sq_norms");
   return SKM_OK;
 }
@@ -321,8 +326,8 @@ int skm_row_sq_norms(const float* x, long long ldx, int rows, int dims, float* o
 int skm_gather_rows(const float* in, long long ldi, const long long* idx, int rows, int cols, float* out,
                     long long ldo, void* stream) {
   if (rows <= 0) return SKM_OK;
-  skm::gather_rows_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
-                                                                                              cols, out, ldo);
+  { skm::gather_rows_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
+                                                                                              cols, out, ldo); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("gather_rows");
   return SKM_OK;
 }
@@ -332,8 +337,8 @@ int skm_gather_front(const float* hi, const float* lo, long long ldi, const int*
                      const float* xsq_ext, const float* thr1, float* oxsq_ext, float* othr1, void* stream) {
   if (rows <= 0) return SKM_OK;
   if (cols > ldo || cols > ldi) return fail(SKM_E_ARG, "gather_front: cols exceeds a stride");
-  skm::gather_front_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(
-      hi, lo, ldi, idx, rows, cols, ohi, olo, ldo, xsq, thr, oxsq, othr, xsq_ext, oxsq_ext, thr1, othr1);
+  { skm::gather_front_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(
+      hi, lo, ldi, idx, rows, cols, ohi, olo, ldo, xsq, thr, oxsq, othr, xsq_ext, oxsq_ext, thr1, othr1); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("gather_front");
   return SKM_OK;
 }
@@ -343,8 +348,8 @@ int skm_ingest_records(const void* raw, long long rows, int d, int rec_words, in
                        void* stream) {
   if (rows <= 0) return SKM_OK;
   if (d <= 0 || ldo < d || rec_words < d + header_words) return fail(SKM_E_ARG, "ingest_records: bad shape");
-  skm::ingest_records_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint32_t*>(raw), rows, d, rec_words, header_words, row0, out, ldo, bad_dim, bad_val);
+  { skm::ingest_records_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uint32_t*>(raw), rows, d, rec_words, header_words, row0, out, ldo, bad_dim, bad_val); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("ingest_records");
   return SKM_OK;
 }
@@ -359,9 +364,9 @@ int skm_wcss(const float* x, long long ldx, const float* centroids, long long ld
   }
   const int parts = static_cast<int>(std::min<long long>(1024, (n + 7) / 8));
   double* part = reinterpret_cast<double*>(workspace);
-  skm::wcss_partial_kernel<<<parts, skm::WCSS_THREADS, 0, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d,
-                                                                               part);
-  skm::wcss_final_kernel<<<1, 32, 0, as_stream(stream)>>>(part, parts, out);
+  { skm::wcss_partial_kernel<<<parts, skm::WCSS_THREADS, 0, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d,
+                                                                               part); SKM_COUNT_LAUNCH(); }
+  { skm::wcss_final_kernel<<<1, 32, 0, as_stream(stream)>>>(part, parts, out); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("wcss");
   return SKM_OK;
 }
@@ -371,7 +376,7 @@ int skm_first_nonfinite(const float* x, long long ldx, long long rows, int cols,
   cudaError_t e = cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "first_nonfinite reset");
   if (rows <= 0 || cols <= 0) return SKM_OK;
-  skm::first_nonfinite_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, first);
+  { skm::first_nonfinite_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(x, ldx, rows, cols, first); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("first_nonfinite");
   return SKM_OK;
 }
@@ -379,22 +384,22 @@ int skm_first_nonfinite(const float* x, long long ldx, long long rows, int cols,
 int skm_gather_rows_i32(const float* in, long long ldi, const int* idx, int rows, int cols, float* out,
                         long long ldo, void* stream) {
   if (rows <= 0) return SKM_OK;
-  skm::gather_rows_i32_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
-                                                                                                  cols, out, ldo);
+  { skm::gather_rows_i32_kernel<<<grid_for((long long)rows * cols, 256), 256, 0, as_stream(stream)>>>(in, ldi, idx, rows,
+                                                                                                  cols, out, ldo); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("gather_rows_i32");
   return SKM_OK;
 }
 
 int skm_fill_f32(float* p, long long n, float v, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::fill_f32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, v);
+  { skm::fill_f32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, v); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("fill_f32");
   return SKM_OK;
 }
 
 int skm_copy_i32(const int* src, int* dst, int n, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::copy_i32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(src, dst, n);
+  { skm::copy_i32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(src, dst, n); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("copy_i32");
   return SKM_OK;
 }
@@ -411,11 +416,11 @@ int skm_seed_thresholds(const float* x, long long ldx, const float* centroids, l
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SEEDA_SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "seed_thresholds smem attribute");
     }
-    skm::seed_thresholds_async_kernel<0><<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, skm::SEEDA_SMEM,
-                                        as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out);
+    { skm::seed_thresholds_async_kernel<0><<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, skm::SEEDA_SMEM,
+                                        as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out); SKM_COUNT_LAUNCH(); }
   } else {
-    skm::seed_thresholds_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, 0, as_stream(stream)>>>(
-        x, ldx, centroids, ldc, assign, n, d, out);
+    { skm::seed_thresholds_kernel<<<(n + skm::SEED_ROWS - 1) / skm::SEED_ROWS, skm::SEED_ROWS, 0, as_stream(stream)>>>(
+        x, ldx, centroids, ldc, assign, n, d, out); SKM_COUNT_LAUNCH(); }
   }
   SKM_LAUNCH_CHECK("seed_thresholds");
   return SKM_OK;
@@ -426,9 +431,9 @@ int skm_scan_bank(const float* partial_dists, int n, int kb, const float* x, lon
                   int d_prime, int bank_offset, float* tau, int* assign, int sentinel,
                   unsigned long long* counters, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::scan_bank_pdx_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
+  { skm::scan_bank_pdx_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
       partial_dists, n, kb, x, ldx, tail, block_offsets, block_dims, n_blocks, theta_factors, d_prime, bank_offset,
-      tau, assign, sentinel, counters);
+      tau, assign, sentinel, counters); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("scan_bank");
   return SKM_OK;
 }
@@ -436,8 +441,8 @@ int skm_scan_bank(const float* partial_dists, int n, int kb, const float* x, lon
 int skm_portable_matmul(const float* a, long long lda, const float* b, long long ldb, int n, int m, int dims,
                         float* out, long long ldo, void* stream) {
   if ((long long)n * m <= 0) return SKM_OK;
-  skm::portable_matmul_kernel<<<(int)(((long long)n * m + 255) / 256), 256, 0, as_stream(stream)>>>(
-      a, lda, b, ldb, n, m, dims, out, ldo);
+  { skm::portable_matmul_kernel<<<(int)(((long long)n * m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      a, lda, b, ldb, n, m, dims, out, ldo); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("portable_matmul");
   return SKM_OK;
 }
@@ -480,7 +485,7 @@ int skm_cluster_sort(const int* assign, int n, int k, int* order, int* counts, i
   if (e != cudaSuccess) return cuda_fail(e, "cluster_sort copy");
   // values start as the identity permutation
   int* v0 = (passes % 2 == 1) ? vals_a : order;
-  skm::iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(v0, n);
+  { skm::iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(v0, n); SKM_COUNT_LAUNCH(); }
   vin = v0;
   int* kbuf[2] = {keys_a, keys_b};
   int* vbuf[2] = {v0, (v0 == order) ? vals_a : order};
@@ -489,16 +494,16 @@ int skm_cluster_sort(const int* assign, int n, int k, int* order, int* counts, i
     int* kout = kbuf[(p + 1) & 1];
     vin = vbuf[p & 1];
     vout = vbuf[(p + 1) & 1];
-    skm::radix_hist_kernel<<<nb, skm::RADIX_THREADS, 0, st>>>(kin, n, 8 * p, hist, nb);
-    skm::exclusive_scan_kernel<<<1, 1024, 0, st>>>(hist, 256 * nb, total);
-    skm::radix_scatter_kernel<<<nb, skm::RADIX_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * p, hist, nb);
+    { skm::radix_hist_kernel<<<nb, skm::RADIX_THREADS, 0, st>>>(kin, n, 8 * p, hist, nb); SKM_COUNT_LAUNCH(); }
+    { skm::exclusive_scan_kernel<<<1, 1024, 0, st>>>(hist, 256 * nb, total); SKM_COUNT_LAUNCH(); }
+    { skm::radix_scatter_kernel<<<nb, skm::RADIX_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * p, hist, nb); SKM_COUNT_LAUNCH(); }
   }
   SKM_LAUNCH_CHECK("cluster_sort radix");
   if (vout != order) return fail(SKM_E_ARG, "cluster_sort: internal ping-pong error");
-  skm::count_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(assign, n, counts);
+  { skm::count_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(assign, n, counts); SKM_COUNT_LAUNCH(); }
   e = cudaMemcpyAsync(offsets, counts, sizeof(int) * k, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "cluster_sort copy");
-  skm::exclusive_scan_kernel<<<1, 1024, 0, st>>>(offsets, k, total);
+  { skm::exclusive_scan_kernel<<<1, 1024, 0, st>>>(offsets, k, total); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("cluster_sort counts");
   return SKM_OK;
 }
@@ -515,12 +520,12 @@ int skm_cluster_sums(const float* x, long long ldx, const int* order, const int*
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, skm::SUMV_RING * 768 * 16);
       if (e != cudaSuccess) return cuda_fail(e, "cluster_sums smem attribute");
     }
-    skm::ordered_cluster_sums_vec_kernel<<<k, threads, skm::SUMV_RING * threads * 16, as_stream(stream)>>>(
-        x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
+    { skm::ordered_cluster_sums_vec_kernel<<<k, threads, skm::SUMV_RING * threads * 16, as_stream(stream)>>>(
+        x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode); SKM_COUNT_LAUNCH(); }
   } else {
     dim3 grid(k, (d + skm::SUM_THREADS - 1) / skm::SUM_THREADS);
-    skm::ordered_cluster_sums_kernel<<<grid, skm::SUM_THREADS, 0, as_stream(stream)>>>(
-        x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode);
+    { skm::ordered_cluster_sums_kernel<<<grid, skm::SUM_THREADS, 0, as_stream(stream)>>>(
+        x, ldx, order, offsets, counts, d, sums, accumulate, centroids, ldc, mode); SKM_COUNT_LAUNCH(); }
   }
   SKM_LAUNCH_CHECK("cluster_sums");
   return SKM_OK;
@@ -529,15 +534,15 @@ int skm_cluster_sums(const float* x, long long ldx, const int* order, const int*
 int skm_finalize_centroids(const double* sums, const long long* counts, int k, int d, float* centroids,
                            long long ldc, void* stream) {
   if ((long long)k * d <= 0) return SKM_OK;
-  skm::finalize_centroids_kernel<<<grid_for((long long)k * d, 256), 256, 0, as_stream(stream)>>>(sums, counts, k, d,
-                                                                                               centroids, ldc);
+  { skm::finalize_centroids_kernel<<<grid_for((long long)k * d, 256), 256, 0, as_stream(stream)>>>(sums, counts, k, d,
+                                                                                               centroids, ldc); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("finalize_centroids");
   return SKM_OK;
 }
 
 int skm_counts_to_i64(const int* c32, long long* c64, int k, int accumulate, void* stream) {
   if (k <= 0) return SKM_OK;
-  skm::counts_to_i64_kernel<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(c32, c64, k, accumulate);
+  { skm::counts_to_i64_kernel<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(c32, c64, k, accumulate); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("counts_to_i64");
   return SKM_OK;
 }
@@ -563,7 +568,7 @@ int skm_accumulate_centroid_sums(const float* x, long long ldx, const int* assig
 int skm_apply_splits(float* centroids, long long ldc, int d, const int* empties, const int* donors, int n_splits,
                      float eps, void* stream) {
   if (n_splits <= 0) return SKM_OK;
-  skm::apply_splits_kernel<<<1, 256, 0, as_stream(stream)>>>(centroids, ldc, d, empties, donors, n_splits, eps);
+  { skm::apply_splits_kernel<<<1, 256, 0, as_stream(stream)>>>(centroids, ldc, d, empties, donors, n_splits, eps); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("apply_splits");
   return SKM_OK;
 }
@@ -576,7 +581,7 @@ long long skm_stats_workspace_bytes(int n) {
 int skm_tau_chunk_sums(const float* tau, long long n, double* out, void* stream) {
   if (n <= 0) return SKM_OK;
   const long long chunks = (n + skm::NP_SUM_BUF - 1) / skm::NP_SUM_BUF;
-  skm::np_sum_chunks_kernel<<<static_cast<unsigned>(chunks), 64, 0, as_stream(stream)>>>(tau, n, out);
+  { skm::np_sum_chunks_kernel<<<static_cast<unsigned>(chunks), 64, 0, as_stream(stream)>>>(tau, n, out); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("tau_chunk_sums");
   return SKM_OK;
 }
@@ -591,9 +596,9 @@ int skm_assign_stats(const float* tau, const int* assign, const int* prev, int n
   unsigned long long* pc = reinterpret_cast<unsigned long long*>(ws + align256(16LL * 1024));
   double* cs = reinterpret_cast<double*>(ws + 2 * align256(16LL * 1024));
   cudaStream_t st = as_stream(stream);
-  skm::assign_stats_partial_kernel<<<parts, skm::STAT_THREADS, 0, st>>>(tau, assign, prev, n, ps, pc);
-  if (chunks > 0) skm::np_sum_chunks_kernel<<<chunks, 64, 0, st>>>(tau, n, cs);
-  skm::assign_stats_final_kernel<<<1, 32, 0, st>>>(cs, chunks, pc, parts, out_sum, out_changed);
+  { skm::assign_stats_partial_kernel<<<parts, skm::STAT_THREADS, 0, st>>>(tau, assign, prev, n, ps, pc); SKM_COUNT_LAUNCH(); }
+  if (chunks > 0) { skm::np_sum_chunks_kernel<<<chunks, 64, 0, st>>>(tau, n, cs); SKM_COUNT_LAUNCH(); }
+  { skm::assign_stats_final_kernel<<<1, 32, 0, st>>>(cs, chunks, pc, parts, out_sum, out_changed); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("assign_stats");
   return SKM_OK;
 }
@@ -616,8 +621,8 @@ int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream) {
 int skm_argmin_merge(const int* top, int n_split, int n, const float* xsq, const float* ysq_max, float kap,
                      int* assign, float* tau, int* amb_rows, unsigned int* amb_count, void* stream) {
   if (n <= 0) return SKM_OK;
-  skm::argmin_merge_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const int4*>(top), n_split, n, xsq, ysq_max, kap, assign, tau, amb_rows, amb_count);
+  { skm::argmin_merge_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const int4*>(top), n_split, n, xsq, ysq_max, kap, assign, tau, amb_rows, amb_count); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("argmin_merge");
   return SKM_OK;
 }
@@ -625,8 +630,8 @@ int skm_argmin_merge(const int* top, int n_split, int n, const float* xsq, const
 int skm_dense_argmin(const float* dist, long long ld, int rows, int cols, const int* row_ids, int* assign,
                      float* tau, void* stream) {
   if (rows <= 0) return SKM_OK;
-  skm::dense_argmin_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(dist, ld, rows, cols,
-                                                                                             row_ids, assign, tau);
+  { skm::dense_argmin_kernel<<<grid_for((long long)rows * 32, 256), 256, 0, as_stream(stream)>>>(dist, ld, rows, cols,
+                                                                                             row_ids, assign, tau); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("dense_argmin");
   return SKM_OK;
 }
@@ -634,8 +639,8 @@ int skm_dense_argmin(const float* dist, long long ld, int rows, int cols, const 
 int skm_argmin_candidates(const int* rows, int n_rows, const float* tau, const float* xsq, const float* ysq_max,
                           float kap, float* thr, float* xs_out, void* stream) {
   if (n_rows <= 0) return SKM_OK;
-  skm::argmin_cand_threshold_kernel<<<(n_rows + 255) / 256, 256, 0, as_stream(stream)>>>(rows, n_rows, tau, xsq,
-                                                                                      ysq_max, kap, thr, xs_out);
+  { skm::argmin_cand_threshold_kernel<<<(n_rows + 255) / 256, 256, 0, as_stream(stream)>>>(rows, n_rows, tau, xsq,
+                                                                                      ysq_max, kap, thr, xs_out); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("argmin_candidates");
   return SKM_OK;
 }
@@ -644,15 +649,15 @@ int skm_cand_exact_argmin(const int* rows, int n_rows, const int* cand, const in
                           long long ldx, const float* centroids, long long ldc, int d, const float* xsq,
                           const float* ysq, int flavour, int q, int* assign, float* tau, void* stream) {
   if (n_rows <= 0) return SKM_OK;
-  skm::cand_exact_argmin_kernel<<<grid_for((long long)n_rows * 32, 256), 256, 0, as_stream(stream)>>>(
+  { skm::cand_exact_argmin_kernel<<<grid_for((long long)n_rows * 32, 256), 256, 0, as_stream(stream)>>>(
       rows, n_rows, reinterpret_cast<const int2*>(cand), cand_cnt, cap, x, ldx, centroids, ldc, d, xsq, ysq, flavour,
-      q, assign, tau);
+      q, assign, tau); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("cand_exact_argmin");
   return SKM_OK;
 }
 
 int skm_max_f32(const float* v, int n, float* out, void* stream) {
-  skm::max_f32_kernel<<<1, 1024, 0, as_stream(stream)>>>(v, n, out);
+  { skm::max_f32_kernel<<<1, 1024, 0, as_stream(stream)>>>(v, n, out); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("max_f32");
   return SKM_OK;
 }
@@ -674,11 +679,11 @@ int skm_exact_pair_dist(const float* x, long long ldx, const float* centroids, l
   }
   const int grid = (n + skm::SEED_ROWS - 1) / skm::SEED_ROWS;
   if (flavour == 0)
-    k1<<<grid, skm::SEED_ROWS, skm::SEEDA_SMEM, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out, xsq,
-                                                                     ysq, q);
+    { k1<<<grid, skm::SEED_ROWS, skm::SEEDA_SMEM, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out, xsq,
+                                                                     ysq, q); SKM_COUNT_LAUNCH(); }
   else
-    k2<<<grid, skm::SEED_ROWS, skm::SEEDA_SMEM, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out, xsq,
-                                                                     ysq, 0);
+    { k2<<<grid, skm::SEED_ROWS, skm::SEEDA_SMEM, as_stream(stream)>>>(x, ldx, centroids, ldc, assign, n, d, out, xsq,
+                                                                     ysq, 0); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("exact_pair_dist");
   return SKM_OK;
 }
@@ -688,8 +693,8 @@ int skm_exact_pair_dist(const float* x, long long ldx, const float* centroids, l
 int skm_build_tails(const float* centroids, long long ldc, int k, int d, int d_prime, float* tails, void* stream) {
   const int nb = (d - d_prime + 63) / 64;
   if (k <= 0 || nb <= 0) return SKM_OK;
-  skm::build_tails_kernel<<<grid_for((long long)k * 64 * nb, 256), 256, 0, as_stream(stream)>>>(centroids, ldc, k, d,
-                                                                                              d_prime, nb, tails);
+  { skm::build_tails_kernel<<<grid_for((long long)k * 64 * nb, 256), 256, 0, as_stream(stream)>>>(centroids, ldc, k, d,
+                                                                                              d_prime, nb, tails); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("build_tails");
   return SKM_OK;
 }
@@ -698,8 +703,8 @@ int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* t
                        const float* ysq_max, float kap, void* stream) {
   if (n <= 0) return SKM_OK;
   if (kap > 0.0f && (!xsq || !ysq_max)) return fail(SKM_E_ARG, "gate_threshold: kap needs xsq and ysq_max");
-  skm::gate_threshold_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(tau, n, f0, sentinel, thr, xsq, ysq_max,
-                                                                             kap);
+  { skm::gate_threshold_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(tau, n, f0, sentinel, thr, xsq, ysq_max,
+                                                                             kap); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("gate_threshold");
   return SKM_OK;
 }
@@ -805,7 +810,7 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
         std::max(1, std::min((p->n_rows + skm::SCAN_WARPS - 1) / skm::SCAN_WARPS, sms * std::max(per_sm_f, 1)));
     cudaError_t e = cudaMemsetAsync(p->fb_count, 0, sizeof(unsigned int), st);
     if (e != cudaSuccess) return cuda_fail(e, "pruned_scan fallback reset");
-    skm::flat_scan_kernel<<<fblocks, skm::SCAN_WARPS * 32, fsm, st>>>(a, p->fb_rows, p->fb_count);
+    { skm::flat_scan_kernel<<<fblocks, skm::SCAN_WARPS * 32, fsm, st>>>(a, p->fb_rows, p->fb_count); SKM_COUNT_LAUNCH(); }
     SKM_LAUNCH_CHECK("flat_scan");
     // the fallback rows through the exact kernel (row count read on the device)
     e = cudaMemsetAsync(p->work, 0, sizeof(unsigned int), st);
@@ -814,9 +819,9 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
     a.n_rows_dev = p->fb_count;
   }
   if (p->dense_mode)
-    skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
+    { skm::pruned_scan_kernel<true><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a); SKM_COUNT_LAUNCH(); }
   else
-    skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a);
+    { skm::pruned_scan_kernel<false><<<blocks, skm::SCAN_WARPS * 32, smem, st>>>(a); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("pruned_scan");
   return SKM_OK;
 }
@@ -827,8 +832,8 @@ int skm_topk_rows(const float* d, long long ld, int rows, int cols, int k, int* 
                   long long out_ld, int col_offset, void* stream) {
   if (rows <= 0 || k <= 0) return SKM_OK;
   if (k > skm::TOPK_MAX) return fail(SKM_E_ARG, "topk_rows: k too large (max 2048)");
-  skm::topk_rows_kernel<<<rows, skm::TOPK_THREADS, 0, as_stream(stream)>>>(d, ld, cols, k, out_idx, out_val, out_ld,
-                                                                           col_offset);
+  { skm::topk_rows_kernel<<<rows, skm::TOPK_THREADS, 0, as_stream(stream)>>>(d, ld, cols, k, out_idx, out_val, out_ld,
+                                                                           col_offset); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("topk_rows");
   return SKM_OK;
 }
@@ -837,8 +842,8 @@ int skm_topk_merge(const int* in_idx, const float* in_val, int shards, int k, in
                    void* stream) {
   if (rows <= 0) return SKM_OK;
   if (shards > 8) return fail(SKM_E_ARG, "topk_merge: at most 8 shards");
-  skm::topk_merge_kernel<<<(rows + 127) / 128, 128, 0, as_stream(stream)>>>(in_idx, in_val, shards, k, rows, out_idx,
-                                                                            out_val);
+  { skm::topk_merge_kernel<<<(rows + 127) / 128, 128, 0, as_stream(stream)>>>(in_idx, in_val, shards, k, rows, out_idx,
+                                                                            out_val); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("topk_merge");
   return SKM_OK;
 }
@@ -852,8 +857,8 @@ int skm_etr_hits(const int* gt, int gt_ld, int top_k, const int* probe, int prob
   if (first_use_on_device(set_mask)) {
     cudaFuncSetAttribute(skm::etr_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
-  skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, row_lo,
-                                                             row_hi, k, hits);
+  { skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, row_lo,
+                                                             row_hi, k, hits); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("etr_hits");
   return SKM_OK;
 }
@@ -869,8 +874,8 @@ int skm_probe_tally(const int* gt, int gt_ld, int top_k, const int* probe, int p
   if (first_use_on_device(set_mask)) {
     cudaFuncSetAttribute(skm::etr_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
-  skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, 0, n,
-                                                             k, hits, sizes, explored);
+  { skm::etr_hits_kernel<<<nq, 256, smem, as_stream(stream)>>>(gt, gt_ld, top_k, probe, probe_ld, nprobe, assign, 0, n,
+                                                             k, hits, sizes, explored); SKM_COUNT_LAUNCH(); }
   SKM_LAUNCH_CHECK("probe_tally");
   return SKM_OK;
 }

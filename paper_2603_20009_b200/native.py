@@ -81,6 +81,7 @@ class ScanParams(C.Structure):
 GEMM_STORE, GEMM_DIST, GEMM_ARGMIN, GEMM_GATE = 0, 1, 2, 3
 
 _SIGS = {
+    "skm_kernel_launches": ([], _ll),
     "skm_last_error": ([], C.c_char_p),
     "skm_abi_version": ([], _i),
     "skm_split_hilo": ([_vp, _ll, _i, _i, _vp, _vp, _ll, _vp], _i),
