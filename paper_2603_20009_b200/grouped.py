@@ -342,10 +342,12 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
                         lay.k_total, d, None, 0, ptr(cents.c), cents.ld, 0, st,
                         nbytes=4.0 * n * d + 4.0 * lay.k_total * d)
         empties, donors = [], []
+        # groups with an empty cluster (only they draw from their split RNG, core.py:103-128)
+        has_empty = np.minimum.reduceat(counts, lay.c0) == 0 if cfg.split_empty else np.zeros(G, dtype=bool)
         for g in act:
             if stop_now[g]:
                 continue
-            if cfg.split_empty:
+            if has_empty[g]:
                 c0, k = int(lay.c0[g]), int(lay.ks[g])
                 e, dn = plan_splits(counts[c0:c0 + k].copy(), rngs[g])
                 empties += [c0 + v for v in e]
