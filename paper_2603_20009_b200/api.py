@@ -560,7 +560,9 @@ def final_assign(x_full, result: KMeansResult, cfg: KMeansConfig, device=None, b
         ws.assign[: e0 - s0].copy_(torch.from_numpy(assign[s0:e0]))
         if pruned:
             ws.counters.zero_()
-            ws.flat = True  # rows keep their fitted assignment almost always
+            # rows keep their fitted assignment almost always -- unless most rows were outside the
+            # training sample (seeded at centroid 0, so nearly all of them change: exact kernel)
+            ws.flat = result.sample_indices is None
             pruned_assign_pass(data, cents, ws, plan)
             result.work.seed_dims += (e0 - s0) * d
             result.work.front_pair_dims += (e0 - s0) * k * plan.d_prime
