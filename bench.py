@@ -249,7 +249,7 @@ def run_extra(name: str, dev) -> dict:
     return out
 
 
-def run_c5(dev) -> dict:
+def run_c5(dev, exact_work_stats: bool = True) -> dict:
     """BASELINE c5: hierarchical k-means of 10M x 1024 into k_total = 65536 with meso_k = 430
     (the reference's rule caps near 50.7K at meso_k = 256), rows generated on the GPU
     with the skewed-blob distribution (the host generator would take minutes at 41 GB).  Device-
@@ -269,13 +269,15 @@ def run_c5(dev) -> dict:
     gen_s = time.perf_counter() - t0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    r = hierarchical_fit_device(x, d, HierarchicalConfig(k_total=k_total, meso_k=meso_k, seed=0), rotation=rot)
+    r = hierarchical_fit_device(x, d, HierarchicalConfig(k_total=k_total, meso_k=meso_k, seed=0,
+                                                         exact_work_stats=exact_work_stats), rotation=rot)
     e1.record()
     torch.cuda.synchronize()
     del x
     return {"workload": f"hierarchical_fit_device: {n} x {d} skewed blobs generated on the GPU (same distribution as "
                         f"make_skewed_blobs, not its values), HierarchicalConfig(k_total={k_total}, meso_k={meso_k}, "
-                        f"seed=0), meso 3 + fine 5 iterations, groups batched in one loop",
+                        f"seed=0{'' if exact_work_stats else ', exact_work_stats=False'}), meso 3 + fine 5 "
+                        f"iterations, groups batched in one loop",
             "s_per_fit": round(e0.elapsed_time(e1) / 1e3, 3), "achieved_k": int(r.k),
             "phase_s": {k_: round(v_, 3) for k_, v_ in r.phase_seconds.items()}, "data_gen_s": round(gen_s, 1)}
 

@@ -64,6 +64,14 @@ SCAN_FLAT = os.environ.get("SKM_SCAN_FLAT", "1") != "0"
 # kernel after a partial flat walk, so early iterations (10-40 % changing) are faster without it
 # (c2: -3 % scan time per iteration at <= 4.4 % changed, +13 % at 40 %; profiles/r2_summary.md)
 FLAT_MAX_CHANGED = float(os.environ.get("SKM_SCAN_FLAT_MAX", "0.05"))
+# exact_work_stats = False: candidates that cannot win skip the tail walk.  The gate GEMM's
+# certification partial then runs over the whole tail (K = d' front + d - d' extension columns),
+# a dense pass over k x d per row (c2: ~56 ms); the walk it removes pays off only while the walk
+# covers more than ~2 % of k x d (c2 it2 3.5 %: 207 -> 162 ms; it3 1.3 %: 91 -> 117 ms; c5's meso
+# loop ~50 %: 1.8 -> 0.36 s per iteration).  That fraction is highest in the first pruned
+# iteration and falls as tau tightens, and survivors track it, so the full certificate runs in
+# the first pruned iteration and while the previous one kept > NOWIN_SURV_FRAC of k.
+NOWIN_SURV_FRAC = 0.25
 
 
 def cert_eps(k_dim: int, paired: bool = True) -> float:
@@ -72,6 +80,37 @@ def cert_eps(k_dim: int, paired: bool = True) -> float:
     within tc_kappa * (xsq + ysq + D) <= 3 tc_kappa * (xsq + ysq) of the exact distance (D <=
     2 (xsq + ysq)), so 6 tc_kappa separates them from the threshold for certain."""
     return 6.0 * tc_kappa(k_dim, paired)
+
+
+def nowin_cert_eps(d: int, ext: int) -> float:
+    """Margin of the full-d certificate (exact_work_stats = False), relative to xsq + ysq over d:
+    cert_eps's argument over all d columns -- the tensor-core distance and the reference's
+    complete running sum (front chain + 64-dim block sums, each within gamma_d (xsq + ysq + D) of
+    the exact distance) both lie within 3 kappa (xsq + ysq) of it -- with the extension partial's
+    truncating TMEM accumulation taken at 12 MMAs per 32-wide k-block, all ext / 32 blocks in one
+    partial."""
+    g = d * _U / (1.0 - d * _U)
+    acc = max(2.0 ** -16, 12.0 * ((ext + 31) // 32) * 2.0 ** -23)
+    return 6.0 * (2.0 * (g + acc) + 16.0 * _U)
+
+
+def cert_extension(data, cents, plan, tau: torch.Tensor, thr1: torch.Tensor, n: int, nowin: bool):
+    """(ext_k, xsq_ext, ysq_ext, cert_eps) of the gate GEMM's certification partial, with thr1[:n]
+    filled.  Default: the block-0 certificate (CERT_EXT columns after d', thr1 = fl(tau F1)).
+    ``nowin`` (exact_work_stats = False): the partial covers all d columns and thr1 = tau, so a
+    flagged column's complete distance lies above the seed tau -- it never replaces the best (tau
+    only decreases) and the scan settles only its survivor decision, as for a block-0 prune."""
+    d, dp = data.d, plan.d_prime
+    if plan.sentinel or dp % 4:
+        return 0, None, None, 0.0
+    st = stream_handle()
+    if nowin and dp < d:
+        native.call("skm_gate_threshold", ptr(tau), n, 1.0, 0, ptr(thr1), None, None, 0.0, st)
+        return d - dp, data.norms(d), cents.full_norms()[0], nowin_cert_eps(d, d - dp)
+    if dp + CERT_EXT > d or plan.widths[0] != 64:
+        return 0, None, None, 0.0
+    native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(thr1), None, None, 0.0, st)
+    return CERT_EXT, data.norms(dp + CERT_EXT), cents.ysq_ext, cert_eps(dp + CERT_EXT, GATE_KPAIR)
 
 
 # ---------------------------------------------------------------- exact-chain policy
@@ -300,6 +339,15 @@ class Centroids:
         self.ysq_ext = None
         self.ysq_max = torch.zeros(1, dtype=torch.float32, device=c.device)  # max_j ysq (error bounds)
 
+    def full_norms(self):
+        """(ysq over all d columns, its max) for the full-d gate (exact_work_stats = False)."""
+        if getattr(self, "ysq_full", None) is None:
+            self.ysq_full = torch.empty(self.k, dtype=torch.float32, device=self.c.device)
+            self.ysq_full_max = torch.zeros(1, dtype=torch.float32, device=self.c.device)
+        native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, self.d, ptr(self.ysq_full), stream_handle())
+        native.call("skm_max_f32", ptr(self.ysq_full), self.k, ptr(self.ysq_full_max), stream_handle())
+        return self.ysq_full, self.ysq_full_max
+
     def refresh(self, dims: int, d_prime: int | None):
         """Recompute split + norms over `dims` (+ tails at d_prime) after an update."""
         native.call("skm_split_hilo", ptr(self.c), self.ld, self.k, self.d, ptr(self.hi), ptr(self.lo), self.ld,
@@ -407,6 +455,7 @@ class Workspace:
         # scan diagnostics: spec blocks, spec waves, exact blocks, exact waves, rows routed to the exact phase
         self.diag = torch.zeros(8, dtype=torch.int64, device=dev)
         self.flat = False  # this pass uses the flat scan (the loop decides per iteration)
+        self.nowin = False  # this pass certifies the candidates that cannot win (full-d partial)
         self.fb_rows = torch.empty(b, dtype=i32, device=dev)  # flat scan: fallback rows of a batch
         self.fb_count = torch.zeros(1, dtype=i32, device=dev)
         self.bx = torch.empty(b, dtype=f32, device=dev)
@@ -578,12 +627,8 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
     # (chain) distance may pass fl(tau F0); the scan settles every decision exactly
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
                 ptr(ws.thr[row0:row0 + n]), ptr(xsq[row0:row0 + n]), ptr(cents.ysq_max), float(kap), st)
-    ext = CERT_EXT if (not plan.sentinel and dp % 4 == 0 and dp + CERT_EXT <= d and plan.widths[0] == 64) else 0
-    if ext:
-        native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(ws.thr1[row0:row0 + n]),
-                    None, None, 0.0, st)
-        xsq_ext = data.norms(dp + ext)
-        ceps = cert_eps(dp + ext, GATE_KPAIR)
+    ext, xsq_ext, ysq_ext, ceps = cert_extension(data, cents, plan, tau, ws.thr1[row0:row0 + n], n,
+                                                 ws.nowin and seed_tau)
     k = cents.k
     ordered = order is not None and row0 == 0 and n == data.n
     if ordered:
@@ -601,14 +646,14 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
                         ptr(xsq_ext) if ext else None, ptr(ws.thr1) if ext else None,
                         ptr(ws.bx_ext) if ext else None, ptr(ws.bthr1) if ext else None, st,
                         nbytes=16.0 * bn * (dp + ext) + 24.0 * bn)
-            cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=cents.ysq_ext, thr1=ws.bthr1[:bn],
+            cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=ysq_ext, thr1=ws.bthr1[:bn],
                         cert_eps=ceps) if ext else {}
             _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
                   ysq=cents.ysq, thr=ws.bthr[:bn], cand=ws.cand, cand_cnt=ws.cand_cnt,
                   cand_cap=ws.cap, **cert)
             sp.row_map = rmap.data_ptr()
         else:
-            cert = dict(ext_k=ext, xsq_ext=xsq_ext[r:r + bn], ysq_ext=cents.ysq_ext, thr1=ws.thr1[r:r + bn],
+            cert = dict(ext_k=ext, xsq_ext=xsq_ext[r:r + bn], ysq_ext=ysq_ext, thr1=ws.thr1[r:r + bn],
                         cert_eps=ceps) if ext else {}
             _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE,
                   xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand=ws.cand,
@@ -903,6 +948,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
     pin_counts = torch.empty(k, dtype=torch.int32, pin_memory=True)
     have_order = False
     last_changed = None  # n_changed of the previous iteration (flat-scan policy)
+    last_surv_row = None  # survivors per row of the previous pruned iteration (exact_work_stats policy)
     scan_blocks: list[int] = []
     scan_waves: list[int] = []
     scan_diag: list[list[int]] = []
@@ -929,6 +975,8 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
             ws.counters.zero_()
             ws.diag.zero_()
             ws.flat = last_changed is not None and last_changed <= FLAT_MAX_CHANGED * n
+            ws.nowin = (not cfg.exact_work_stats and not cfg.pruning_sentinel and not ws.flat
+                        and (last_surv_row is None or last_surv_row > NOWIN_SURV_FRAC * k))
             pruned_assign_pass(data, cents, ws, plan, order=ws.order[:n_local] if have_order else None)
             timer.stop("pruning")
             work.front_pair_dims += n * k * d_prime
@@ -966,6 +1014,7 @@ def fit_rotated_device(data: DeviceData, cfg: KMeansConfig, inspect=None, comm: 
                 scan_diag.append([int(v) for v in dg[:6]])
             survivors, touched = int(round(sv)), int(round(td))
             prune_rate = prune_rate_from_totals(survivors, n, k)
+            last_surv_row = survivors / max(n, 1)
             work.tail_dims += touched
         if inspect is not None:
             inspect(it, {

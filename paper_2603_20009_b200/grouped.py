@@ -33,16 +33,16 @@ from . import native
 from .config import KMeansConfig, WorkCounters, initial_d_prime, pruning_supported
 from .device import padded_ld, ptr, stream_handle
 from .engine import (
-    CERT_EXT,
     FLAT_MAX_CHANGED,
     GATE_KPAIR,
+    NOWIN_SURV_FRAC,
     SCAN_FLAT,
     Centroids,
     DeviceData,
     PrunePlan,
     Workspace,
     _gemm,
-    cert_eps,
+    cert_extension,
     chained_cluster_sums,
     tc_kappa,
 )
@@ -138,14 +138,7 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
     kap = tc_kappa(dp, GATE_KPAIR)
     native.call("skm_gate_threshold", ptr(ws.tau), data.n, float(plan.gate[0]), int(plan.sentinel), ptr(ws.thr),
                 ptr(xsq), ptr(cents.ysq_max), float(kap), st)
-    ext = CERT_EXT if (not plan.sentinel and dp % 4 == 0 and dp + CERT_EXT <= d and plan.widths[0] == 64) else 0
-    ceps = 0.0
-    xsq_ext = None
-    if ext:
-        native.call("skm_gate_threshold", ptr(ws.tau), data.n, float(plan.gate[1]), 0, ptr(ws.thr1), None, None, 0.0,
-                    st)
-        xsq_ext = data.norms(dp + ext)
-        ceps = cert_eps(dp + ext, GATE_KPAIR)
+    ext, xsq_ext, ysq_ext, ceps = cert_extension(data, cents, plan, ws.tau, ws.thr1, data.n, ws.nowin)
     fld = padded_ld(dp + ext)
     ga_hi, ga_lo = ws.front_buffers(fld)
     k = cents.k
@@ -158,7 +151,7 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
                     ptr(ws.bx_ext) if ext else None, ptr(ws.bthr1) if ext else None, st,
                     nbytes=16.0 * bn * (dp + ext) + 24.0 * bn)
         cr = lay.row_crange[rm.long()].contiguous()
-        cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=cents.ysq_ext, thr1=ws.bthr1[:bn],
+        cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=ysq_ext, thr1=ws.bthr1[:bn],
                     cert_eps=ceps) if ext else {}
         _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
               ysq=cents.ysq, thr=ws.bthr[:bn], cand=ws.cand, cand_cnt=ws.cand_cnt, cand_cap=ws.cap,
@@ -246,6 +239,7 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
     pin_counts = torch.empty(lay.k_total, dtype=torch.int32, pin_memory=True)
     nk = nglob * lay.ks
     last_changed = None
+    last_surv = None
     if sharded:
         K = lay.k_total
         red = torch.zeros(K * d + K + 3 * G, dtype=torch.float64, device=dev)
@@ -276,6 +270,8 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
             native.call("skm_seed_thresholds", ptr(data.x), data.ld, ptr(cents.c), cents.ld, ptr(ws.assign), n, d,
                         ptr(ws.tau), st, nbytes=4.0 * n * d + 8.0 * n)
             ws.flat = last_changed is not None and last_changed <= FLAT_MAX_CHANGED * int(nglob[act].sum())
+            ws.nowin = (not cfg.exact_work_stats and not cfg.pruning_sentinel and not ws.flat
+                        and (last_surv is None or last_surv > NOWIN_SURV_FRAC * int(nk[act].sum())))
             for dp in np.unique(dprime[act]):
                 cls = act[dprime[act] == dp]
                 plan = PrunePlan(d, int(dp), cfg.epsilon0, cfg.pruning_sentinel, dev)
@@ -325,6 +321,8 @@ def fit_groups_device(data: DeviceData, sizes: np.ndarray, ks: np.ndarray, seeds
             gc = pin_g.numpy().copy()
             counts = pin_counts.numpy().astype(np.int64)
         last_changed = int(gc[act, 2].sum()) if it > 1 else None
+        if pruned_iter:
+            last_surv = int(gc[act, 0].sum())  # survivors of the active groups (exact_work_stats policy)
         stop_now = np.zeros(G, dtype=bool)
         if it > 1:
             stop_now[act] = gc[act, 2] == 0  # converged: no update, no split (core.py:358-363)

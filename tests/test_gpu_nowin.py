@@ -1,0 +1,78 @@
+"""exact_work_stats = False (engine.cert_extension over all d columns): candidates whose full-d
+distance interval lies above the seed tau skip the tail walk.  Everything the reference's loop decides --
+every assignment, tau, survivors, the d' trajectory, n_changed, wcss, splits, the centroids --
+must be bitwise the exact-stats fit; only tail_dims_touched may drop (it counts the walks made)."""
+
+import numpy as np
+import pytest
+
+from conftest import make_blobs, make_skewed_blobs
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1_shape": ("blobs", 100_000, 128, 256, 0, 256, 10),
+    "skew768": ("skew", 200_000, 768, 2048, 0, 1024, 8),
+    "skew1536": ("skew", 100_000, 1536, 1024, 1, 512, 6),
+    "skew1024_small_k": ("skew", 300_000, 1024, 4096, 2, 64, 5),
+}
+
+
+def _data(kind, n, d, centers, seed):
+    return make_blobs(n, d, centers, seed=seed) if kind == "blobs" else make_skewed_blobs(n, d, centers, seed=seed)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_nowin_fit_matches_exact_stats(name):
+    import paper_2603_20009_b200 as skb
+    from paper_2603_20009_b200 import engine
+    from paper_2603_20009_b200.config import KMeansConfig
+    kind, n, d, centers, seed, k, iters = CASES[name]
+    x = _data(kind, n, d, centers, seed)
+    snaps = {}
+
+    def grab(tag):
+        def f(it, info):
+            snaps[(tag, it)] = (info["assignments"], info["best_sq_dist"])
+        return f
+
+    ref = skb.fit(x, KMeansConfig(k=k, max_iters=iters, seed=seed), inspect=grab("exact"))
+    calls = []
+    orig = engine.cert_extension
+
+    def spy(data, cents, plan, *a, **kw):
+        out = orig(data, cents, plan, *a, **kw)
+        if out[0] == data.d - plan.d_prime:
+            calls.append(1)
+        return out
+
+    engine.cert_extension = spy
+    try:
+        fast = skb.fit(x, KMeansConfig(k=k, max_iters=iters, seed=seed, exact_work_stats=False), inspect=grab("fast"))
+    finally:
+        engine.cert_extension = orig
+    assert calls, "the full-d certificate never ran"
+    assert len(ref.stats) == len(fast.stats)
+    for key in ("d_prime", "survivors", "n_changed", "wcss", "n_empty_splits", "prune_rate_after_gemm"):
+        assert [getattr(s, key) for s in fast.stats] == [getattr(s, key) for s in ref.stats], key
+    assert all(f.tail_dims_touched <= r.tail_dims_touched for f, r in zip(fast.stats, ref.stats))
+    assert sum(f.tail_dims_touched for f in fast.stats) < sum(r.tail_dims_touched for r in ref.stats)
+    for it in range(1, len(ref.stats) + 1):
+        a0, t0 = snaps[("exact", it)]
+        a1, t1 = snaps[("fast", it)]
+        assert np.array_equal(a0, a1), it
+        assert np.array_equal(t0.view(np.uint32), t1.view(np.uint32)), it
+    assert np.array_equal(fast.assignments, ref.assignments)
+    assert np.array_equal(fast.centroids.view(np.uint32), ref.centroids.view(np.uint32))
+    assert fast.terminated_by == ref.terminated_by
+
+
+def test_nowin_hierarchical_matches_exact_stats():
+    import paper_2603_20009_b200 as skb
+    x = make_skewed_blobs(200_000, 512, 4096, seed=3)
+    a = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=2048, seed=3))
+    b = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=2048, seed=3, exact_work_stats=False))
+    assert a.k == b.k
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids.view(np.uint32), b.centroids.view(np.uint32))
+    assert [s.survivors for s in a.stats] == [s.survivors for s in b.stats]
