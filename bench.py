@@ -234,6 +234,21 @@ def run_extra(name: str, dev) -> dict:
         times.append(a0.elapsed_time(a1))
     s2 = r.loop.stats
     ms = float(np.median(times))
+    import dataclasses
+    fcfg = dataclasses.replace(ccfg, exact_work_stats=False)
+    api.fit_device(xd, d, fcfg, rot)  # warm-up
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record()
+    rf = api.fit_device(xd, d, fcfg, rot)
+    a1.record()
+    torch.cuda.synchronize()
+    fms = a0.elapsed_time(a1)
+    wso = {"ms_per_fit": round(fms, 2), "iter_per_s": round(len(rf.loop.stats) / (fms * 1e-3), 2),
+           "bitwise_equal_to_exact_fit": bool(np.array_equal(rf.loop.assignments, r.loop.assignments)
+                                              and torch.equal(rf.centroids_dev, r.centroids_dev)
+                                              and [s.survivors for s in rf.loop.stats] == [s.survivors for s in s2])}
+    del rf
     out = {
         "workload": f"{'make_blobs' if gen == 'blobs' else 'make_skewed_blobs'}({n}, {d}, {centers}, seed=0), "
                     f"k={k}, max_iters={iters}" + (f", ETR(n_queries={etr[0]}, top_k={etr[1]})" if etr else ""),
@@ -244,6 +259,7 @@ def run_extra(name: str, dev) -> dict:
         "pruned_dim_fraction": [None if s.d_prime is None else
                                 round(1.0 - s.tail_dims_touched / (n * k * (d - s.d_prime)), 6) for s in s2],
         "recall_history": [round(v, 4) for v in r.loop.recall_history], "data_gen_s": round(gs, 1),
+        "exact_work_stats_off": wso,
     }
     del xd
     return out
@@ -274,12 +290,17 @@ def run_c5(dev, exact_work_stats: bool = True) -> dict:
     e1.record()
     torch.cuda.synchronize()
     del x
+    import hashlib
+    asg = r.assignments.cpu().numpy() if hasattr(r.assignments, "cpu") else np.asarray(r.assignments)
+    cen = r.centroids.cpu().numpy() if hasattr(r.centroids, "cpu") else np.asarray(r.centroids)
+    digest = hashlib.sha256(asg.tobytes() + cen.tobytes()).hexdigest()[:16]
     return {"workload": f"hierarchical_fit_device: {n} x {d} skewed blobs generated on the GPU (same distribution as "
                         f"make_skewed_blobs, not its values), HierarchicalConfig(k_total={k_total}, meso_k={meso_k}, "
                         f"seed=0{'' if exact_work_stats else ', exact_work_stats=False'}), meso 3 + fine 5 "
                         f"iterations, groups batched in one loop",
             "s_per_fit": round(e0.elapsed_time(e1) / 1e3, 3), "achieved_k": int(r.k),
-            "phase_s": {k_: round(v_, 3) for k_, v_ in r.phase_seconds.items()}, "data_gen_s": round(gen_s, 1)}
+            "phase_s": {k_: round(v_, 3) for k_, v_ in r.phase_seconds.items()}, "data_gen_s": round(gen_s, 1),
+            "assignments_centroids_sha256_16": digest}
 
 
 # ----------------------------------------------------------------------------- roofline
@@ -436,6 +457,39 @@ def main():
         parity = {"golden": "tests/golden/full_c2.npz (the real reference, 632.7 s on 8 cores)",
                   "bitwise_equal": checks, "all": all(checks.values())}
 
+    # ---- the same fit with exact_work_stats=False (option: candidates that cannot win skip the
+    #      tail walk; everything but tail_dims_touched stays bitwise) ----
+    wso = None
+    if world == 1 and not args.no_extra:
+        try:
+            import dataclasses
+            fcfg = dataclasses.replace(cfg, exact_work_stats=False)
+            api.fit_device(x, args.d, fcfg, rotation)  # warm-up
+            ftimes = []
+            for _ in range(2):
+                f0 = torch.cuda.Event(enable_timing=True)
+                f1 = torch.cuda.Event(enable_timing=True)
+                f0.record()
+                rf = api.fit_device(x, args.d, fcfg, rotation)
+                f1.record()
+                torch.cuda.synchronize()
+                ftimes.append(f0.elapsed_time(f1))
+            fst = rf.loop.stats
+            fms = float(np.median(ftimes))
+            wso = {"ms_per_fit": round(fms, 2), "iter_per_s": round(len(fst) / (fms * 1e-3), 3),
+                   "tail_dims_touched": [s.tail_dims_touched for s in fst],
+                   "pruning_ms": [round(1e3 * s.timings.get("pruning", 0.0), 1) for s in fst],
+                   "exact_pruning_ms": [round(1e3 * s.timings.get("pruning", 0.0), 1) for s in st],
+                   "all_ms": [round(v, 1) for v in ftimes],
+                   "bitwise_equal_to_exact_fit": {
+                       "assignments": bool(np.array_equal(rf.loop.assignments, res.loop.assignments)),
+                       "centroids": bool(torch.equal(rf.centroids_dev, res.centroids_dev)),
+                       "d_prime_survivors_changed_wcss": [(s.d_prime, s.survivors, s.n_changed, s.wcss) for s in fst]
+                       == [(s.d_prime, s.survivors, s.n_changed, s.wcss) for s in st]}}
+            del rf
+        except Exception as exc:
+            wso = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # ---- end to end through the public entry (api.fit) with pinned host input ----
     e2e = None
     if not args.no_e2e:
@@ -488,6 +542,14 @@ def main():
             extra["c5"] = run_c5(dev)
         except Exception as exc:
             extra["c5"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        torch.cuda.empty_cache()
+        try:
+            c5f = run_c5(dev, exact_work_stats=False)
+            c5f["bitwise_equal_to_exact_fit"] = \
+                c5f["assignments_centroids_sha256_16"] == extra["c5"].get("assignments_centroids_sha256_16")
+            extra["c5_exact_work_stats_off"] = c5f
+        except Exception as exc:
+            extra["c5_exact_work_stats_off"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     # the host-CPU reference sample runs last: its BLAS threads must not compete with the host
     # orchestration of the (launch-bound) small secondary configs above
@@ -512,7 +574,7 @@ def main():
                                         for s in st],
                 "phase_ms_last_step": {k_: round(v_ * 1e3, 2) for k_, v_ in res.phase.items()}}),
             "parity": parity, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks.summary(), "configs": extra,
+            "clocks": clocks.summary(), "exact_work_stats_off": wso, "configs": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
