@@ -15,6 +15,7 @@ CASES = {
     "skew768": ("skew", 200_000, 768, 2048, 0, 1024, 8),
     "skew1536": ("skew", 100_000, 1536, 1024, 1, 512, 6),
     "skew1024_small_k": ("skew", 300_000, 1024, 4096, 2, 64, 5),
+    "skew768_portable": ("skew", 100_000, 768, 1024, 4, 256, 6, "portable"),
 }
 
 
@@ -27,7 +28,8 @@ def test_nowin_fit_matches_exact_stats(name):
     import paper_2603_20009_b200 as skb
     from paper_2603_20009_b200 import engine
     from paper_2603_20009_b200.config import KMeansConfig
-    kind, n, d, centers, seed, k, iters = CASES[name]
+    kind, n, d, centers, seed, k, iters = CASES[name][:7]
+    backend = CASES[name][7] if len(CASES[name]) > 7 else "auto"
     x = _data(kind, n, d, centers, seed)
     snaps = {}
 
@@ -36,7 +38,7 @@ def test_nowin_fit_matches_exact_stats(name):
             snaps[(tag, it)] = (info["assignments"], info["best_sq_dist"])
         return f
 
-    ref = skb.fit(x, KMeansConfig(k=k, max_iters=iters, seed=seed), inspect=grab("exact"))
+    ref = skb.fit(x, KMeansConfig(k=k, max_iters=iters, seed=seed, gemm_backend=backend), inspect=grab("exact"))
     calls = []
     orig = engine.cert_extension
 
@@ -48,7 +50,8 @@ def test_nowin_fit_matches_exact_stats(name):
 
     engine.cert_extension = spy
     try:
-        fast = skb.fit(x, KMeansConfig(k=k, max_iters=iters, seed=seed, exact_work_stats=False), inspect=grab("fast"))
+        fast = skb.fit(x, KMeansConfig(k=k, max_iters=iters, seed=seed, gemm_backend=backend, exact_work_stats=False),
+                       inspect=grab("fast"))
     finally:
         engine.cert_extension = orig
     assert calls, "the full-d certificate never ran"
@@ -76,3 +79,52 @@ def test_nowin_hierarchical_matches_exact_stats():
     assert np.array_equal(a.assignments, b.assignments)
     assert np.array_equal(a.centroids.view(np.uint32), b.centroids.view(np.uint32))
     assert [s.survivors for s in a.stats] == [s.survivors for s in b.stats]
+
+
+def _run_ws(rank, world, port, q, exact_work_stats):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_20009_b200 import api
+        from paper_2603_20009_b200.config import KMeansConfig
+        from paper_2603_20009_b200.engine import Comm
+        from paper_2603_20009_b200.hostmath import generate_rotation
+        torch.cuda.set_device(0)
+        x = make_skewed_blobs(60_000, 256, 1024, seed=6)
+        n, d = x.shape
+        comm = Comm()
+        lo, hi = comm.shard(n)
+        xd = api._h2d(x[lo:hi], torch.device("cuda", 0))
+        cfg = KMeansConfig(k=300, max_iters=6, seed=6, exact_work_stats=exact_work_stats)
+        res = api.fit_device(xd, d, cfg, generate_rotation(d, 6), comm=comm, n_global=n, row_lo=lo)
+        st = res.loop.stats
+        q.put((rank, {"assign": res.loop.assignments, "lo": lo, "cent": res.centroids_dev[:, :d].cpu().numpy(),
+                      "stats": [(s.d_prime, s.survivors, s.n_changed, s.wcss) for s in st],
+                      "tail": [s.tail_dims_touched for s in st]}))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nowin_two_ranks_match_single_rank_exact():
+    """Row-sharded (2 ranks over gloo on one GPU): the option's decisions are per row and its
+    policy reads the allreduced survivors, so the ranks agree and match the 1-GPU exact fit."""
+    import os
+
+    from test_gpu_multirank import _spawn
+    port = 29900 + (os.getpid() % 400)
+    one = _spawn(1, port, _run_ws, (True,))[0]
+    two = _spawn(2, port + 1, _run_ws, (False,))
+    a2 = np.concatenate([two[r]["assign"] for r in sorted(two, key=lambda r: two[r]["lo"])])
+    assert np.array_equal(a2, one["assign"])
+    for r in two:
+        assert two[r]["stats"] == one["stats"]
+        assert np.array_equal(two[r]["cent"], one["cent"])
+        assert sum(two[r]["tail"]) < sum(one["tail"])
