@@ -119,6 +119,9 @@ typedef struct skm_gemm_params {
    * [row_crange[i].x, row_crange[i].y) (its group's centroids); M tile t walks only the N tiles
    * covering [tile_nrange[t].x, tile_nrange[t].y) (the union of its rows' ranges).  Both int2. */
   const int* row_crange; const int* tile_nrange;
+  /* GATE extension as one TF32 product (hi x hi): a third of its MMAs, for a certificate whose
+   * cert_eps covers 2^-9 of xsq_ext + ysq_ext (exact_work_stats = false) */
+  int ext_hi_only;
 } skm_gemm_params;
 int skm_gemm_tf32x3(const skm_gemm_params* p, void* stream);
 /* Merge the ARGMIN top-2 records: assign = lowest index among the smallest distances, tau = its

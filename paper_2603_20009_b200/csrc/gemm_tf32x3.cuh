@@ -65,6 +65,10 @@ struct GemmArgs {
   // for every group: each group's rows against its own centroid block)
   const int2* row_crange;
   const int2* tile_nrange;
+  // 1: the extension k-blocks run as one TF32 product (hi x hi) instead of 3xTF32 -- a third
+  // of their MMAs and half their TMA bytes -- for a certificate whose margin covers 2^-9 of
+  // xsq_ext + ysq_ext (engine.nowin_cert_eps)
+  int ext_hi_only;
 };
 constexpr int CAND_CERT0 = static_cast<int>(0x80000000u);
 
@@ -199,14 +203,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
         for (int kb = 0; kb < num_k + num_e; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
-          uint8_t* base = smem + s * L::STAGE_BYTES;
           const bool ext = kb >= num_k;
+          const bool hi_only = ext && args.ext_hi_only;
+          mbar_arrive_expect_tx(&full[s], hi_only ? L::A_BYTES + L::B_BYTES : L::STAGE_BYTES);
+          uint8_t* base = smem + s * L::STAGE_BYTES;
           const int k0 = (ext ? kb - num_k : kb) * GEMM_BK;
           tma_load_2d(base, ext ? &tE_A_hi : &tA_hi, &full[s], k0, m0);
-          tma_load_2d(base + L::A_BYTES, ext ? &tE_A_lo : &tA_lo, &full[s], k0, m0);
+          if (!hi_only) tma_load_2d(base + L::A_BYTES, ext ? &tE_A_lo : &tA_lo, &full[s], k0, m0);
           tma_load_2d(base + 2 * L::A_BYTES, ext ? &tE_B_hi : &tB_hi, &full[s], k0, n0);
-          tma_load_2d(base + 2 * L::A_BYTES + L::B_BYTES, ext ? &tE_B_lo : &tB_lo, &full[s], k0, n0);
+          if (!hi_only) tma_load_2d(base + 2 * L::A_BYTES + L::B_BYTES, ext ? &tE_B_lo : &tB_lo, &full[s], k0, n0);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -238,16 +243,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint64_t a_lo = sw128_kmajor_desc(base + L::A_BYTES);
           const uint64_t b_hi = sw128_kmajor_desc(base + 2 * L::A_BYTES);
           const uint64_t b_lo = sw128_kmajor_desc(base + 2 * L::A_BYTES + L::B_BYTES);
+          if (main_kb || !args.ext_hi_only) {
 #pragma unroll
-          for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
-            const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);  // 8 tf32 = 32 bytes
-            mma_tf32(d_tmem, a_lo + adv, b_hi + adv, idesc, (kk != 0 || cont) ? 1u : 0u);
-            mma_tf32(d_tmem, a_hi + adv, b_lo + adv, idesc, 1u);
-          }
+            for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+              const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);  // 8 tf32 = 32 bytes
+              mma_tf32(d_tmem, a_lo + adv, b_hi + adv, idesc, (kk != 0 || cont) ? 1u : 0u);
+              mma_tf32(d_tmem, a_hi + adv, b_lo + adv, idesc, 1u);
+            }
 #pragma unroll
-          for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
-            const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);
-            mma_tf32(d_tmem, a_hi + adv, b_hi + adv, idesc, 1u);
+            for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+              const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);
+              mma_tf32(d_tmem, a_hi + adv, b_hi + adv, idesc, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+              const uint64_t adv = static_cast<uint64_t>((kk * 32) >> 4);
+              mma_tf32(d_tmem, a_hi + adv, b_hi + adv, idesc, (kk != 0 || cont) ? 1u : 0u);
+            }
           }
           mma_commit(&empty[s]);
           if (last_of_partial) {

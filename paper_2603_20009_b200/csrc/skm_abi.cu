@@ -143,6 +143,7 @@ int launch_gemm(const skm_gemm_params* p, cudaStream_t st) {
   a.ysq_ext = p->ysq_ext;
   a.thr1 = p->thr1;
   a.cert_eps = p->cert_eps;
+  a.ext_hi_only = ext_k > 0 ? p->ext_hi_only : 0;
   a.row_crange = reinterpret_cast<const int2*>(p->row_crange);
   a.tile_nrange = reinterpret_cast<const int2*>(p->tile_nrange);
   if ((a.row_crange != nullptr) != (a.tile_nrange != nullptr))

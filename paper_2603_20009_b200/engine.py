@@ -65,13 +65,14 @@ SCAN_FLAT = os.environ.get("SKM_SCAN_FLAT", "1") != "0"
 # (c2: -3 % scan time per iteration at <= 4.4 % changed, +13 % at 40 %; profiles/r2_summary.md)
 FLAT_MAX_CHANGED = float(os.environ.get("SKM_SCAN_FLAT_MAX", "0.05"))
 # exact_work_stats = False: candidates that cannot win skip the tail walk.  The gate GEMM's
-# certification partial then runs over the whole tail (K = d' front + d - d' extension columns),
-# a dense pass over k x d per row (c2: ~56 ms); the walk it removes pays off only while the walk
-# covers more than ~2 % of k x d (c2 it2 3.5 %: 207 -> 162 ms; it3 1.3 %: 91 -> 117 ms; c5's meso
-# loop ~50 %: 1.8 -> 0.36 s per iteration).  That fraction is highest in the first pruned
-# iteration and falls as tau tightens, and survivors track it, so the full certificate runs in
-# the first pruned iteration and while the previous one kept > NOWIN_SURV_FRAC of k.
-NOWIN_SURV_FRAC = 0.25
+# certification partial then runs over the whole tail (d' front + d - d' extension columns, the
+# extension as one TF32 product), about 2.2x the gate's tensor work; the walk it removes pays
+# off only while the walk is long.  c2 per pruned iteration (exact -> option, ms): it2 209 -> 97
+# (14.8 % of k survived the gate), it3 91 -> 72 (5.6 %), it4 53 -> 66 (2.8 %), it5 50 -> 60; c5's
+# meso loop (k = 430) 1.8 -> 0.31 s.  The previous iteration's survivor fraction predicts the
+# walk, so the full certificate runs in the first pruned iteration and while the previous
+# one kept more than NOWIN_SURV_FRAC of k.
+NOWIN_SURV_FRAC = float(os.environ.get("SKM_NOWIN_SURV_FRAC", "0.12"))
 
 
 def cert_eps(k_dim: int, paired: bool = True) -> float:
@@ -82,35 +83,49 @@ def cert_eps(k_dim: int, paired: bool = True) -> float:
     return 6.0 * tc_kappa(k_dim, paired)
 
 
-def nowin_cert_eps(d: int, ext: int) -> float:
-    """Margin of the full-d certificate (exact_work_stats = False), relative to xsq + ysq over d:
-    cert_eps's argument over all d columns -- the tensor-core distance and the reference's
-    complete running sum (front chain + 64-dim block sums, each within gamma_d (xsq + ysq + D) of
-    the exact distance) both lie within 3 kappa (xsq + ysq) of it -- with the extension partial's
-    truncating TMEM accumulation taken at 12 MMAs per 32-wide k-block, all ext / 32 blocks in one
-    partial."""
+def nowin_cert_eps(d: int, ext: int, hi_only: bool = True) -> float:
+    """Margin of the full-d certificate (exact_work_stats = False), relative to xsq + ysq over d.
+    The reference's complete running sum (front chain + 64-dim block sums) lies within
+    3 kappa_ref (xsq + ysq) of the exact distance, kappa_ref = 2 gamma_d + 16 u (as in cert_eps).
+    The tensor-core distance: ``hi_only`` (NOWIN_HI_ONLY) runs the ext / 32 extension k-blocks as
+    one TF32 product -- truncated operands, |x c - x_h c_h| <= (2^-9 + 2^-20) |x c|, so the inner
+    product is off by <= 2^-10 (xsq + ysq) and the distance by twice that -- plus 4 truncating
+    TMEM accumulations per k-block and the 3xTF32 front (2^-16); else 3xTF32 throughout (12 MMAs
+    per k-block).  A quarter more on top for slack."""
     g = d * _U / (1.0 - d * _U)
-    acc = max(2.0 ** -16, 12.0 * ((ext + 31) // 32) * 2.0 ** -23)
-    return 6.0 * (2.0 * (g + acc) + 16.0 * _U)
+    blocks = (ext + 31) // 32
+    ref = 3.0 * (2.0 * g + 16.0 * _U)
+    if hi_only:
+        tc = 2.0 * ((2.0 ** -10) * (1.0 + 2.0 ** -9) + 4.0 * blocks * 2.0 ** -23 + 2.0 ** -16 + g) + 16.0 * _U
+    else:
+        tc = 3.0 * (2.0 * (g + max(2.0 ** -16, 12.0 * blocks * 2.0 ** -23)) + 16.0 * _U)
+    return 1.25 * (tc + ref)
 
 
-def cert_extension(data, cents, plan, tau: torch.Tensor, thr1: torch.Tensor, n: int, nowin: bool):
-    """(ext_k, xsq_ext, ysq_ext, cert_eps) of the gate GEMM's certification partial, with thr1[:n]
-    filled.  Default: the block-0 certificate (CERT_EXT columns after d', thr1 = fl(tau F1)).
-    ``nowin`` (exact_work_stats = False): the partial covers all d columns and thr1 = tau, so a
-    flagged column's complete distance lies above the seed tau -- it never replaces the best (tau
-    only decreases) and the scan settles only its survivor decision, as for a block-0 prune."""
+NOWIN_HI_ONLY = os.environ.get("SKM_NOWIN_HI_ONLY", "1") != "0"
+
+
+def cert_extension(data, cents, plan, tau: torch.Tensor, thr1: torch.Tensor, n: int, nowin: bool) -> dict:
+    """The gate GEMM's certification-partial arguments ({} = none), with thr1[:n] filled.
+    Default: the block-0 certificate (CERT_EXT columns after d', thr1 = fl(tau F1)).  ``nowin``
+    (exact_work_stats = False): the partial covers all d columns (one TF32 product with
+    NOWIN_HI_ONLY) and thr1 = tau, so a flagged column's complete distance lies above the seed
+    tau -- it never replaces the best (tau only decreases) and the scan settles only its
+    survivor decision, as for a block-0 prune.  ``xsq_ext`` is the full-height row-norm vector
+    (callers slice or gather it)."""
     d, dp = data.d, plan.d_prime
     if plan.sentinel or dp % 4:
-        return 0, None, None, 0.0
+        return {}
     st = stream_handle()
     if nowin and dp < d:
         native.call("skm_gate_threshold", ptr(tau), n, 1.0, 0, ptr(thr1), None, None, 0.0, st)
-        return d - dp, data.norms(d), cents.full_norms()[0], nowin_cert_eps(d, d - dp)
+        return dict(ext_k=d - dp, xsq_ext=data.norms(d), ysq_ext=cents.full_norms()[0],
+                    cert_eps=nowin_cert_eps(d, d - dp, NOWIN_HI_ONLY), ext_hi_only=NOWIN_HI_ONLY)
     if dp + CERT_EXT > d or plan.widths[0] != 64:
-        return 0, None, None, 0.0
+        return {}
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(thr1), None, None, 0.0, st)
-    return CERT_EXT, data.norms(dp + CERT_EXT), cents.ysq_ext, cert_eps(dp + CERT_EXT, GATE_KPAIR)
+    return dict(ext_k=CERT_EXT, xsq_ext=data.norms(dp + CERT_EXT), ysq_ext=cents.ysq_ext,
+                cert_eps=cert_eps(dp + CERT_EXT, GATE_KPAIR), ext_hi_only=False)
 
 
 # ---------------------------------------------------------------- exact-chain policy
@@ -383,6 +398,7 @@ def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
     p.row_offset = kw.pop("row_offset", 0)
     p.ext_k = kw.pop("ext_k", 0)
     p.cert_eps = kw.pop("cert_eps", 0.0)
+    p.ext_hi_only = int(kw.pop("ext_hi_only", 0))
     for name, t in kw.items():
         if t is not None:
             setattr(p, name, t.data_ptr())
@@ -627,8 +643,9 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
     # (chain) distance may pass fl(tau F0); the scan settles every decision exactly
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[0]), int(plan.sentinel),
                 ptr(ws.thr[row0:row0 + n]), ptr(xsq[row0:row0 + n]), ptr(cents.ysq_max), float(kap), st)
-    ext, xsq_ext, ysq_ext, ceps = cert_extension(data, cents, plan, tau, ws.thr1[row0:row0 + n], n,
-                                                 ws.nowin and seed_tau)
+    cx = cert_extension(data, cents, plan, tau, ws.thr1[row0:row0 + n], n, ws.nowin and seed_tau)
+    ext = cx.get("ext_k", 0)
+    xsq_ext = cx.get("xsq_ext")
     k = cents.k
     ordered = order is not None and row0 == 0 and n == data.n
     if ordered:
@@ -646,15 +663,13 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
                         ptr(xsq_ext) if ext else None, ptr(ws.thr1) if ext else None,
                         ptr(ws.bx_ext) if ext else None, ptr(ws.bthr1) if ext else None, st,
                         nbytes=16.0 * bn * (dp + ext) + 24.0 * bn)
-            cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=ysq_ext, thr1=ws.bthr1[:bn],
-                        cert_eps=ceps) if ext else {}
+            cert = dict(cx, xsq_ext=ws.bx_ext[:bn], thr1=ws.bthr1[:bn]) if ext else {}
             _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
                   ysq=cents.ysq, thr=ws.bthr[:bn], cand=ws.cand, cand_cnt=ws.cand_cnt,
                   cand_cap=ws.cap, **cert)
             sp.row_map = rmap.data_ptr()
         else:
-            cert = dict(ext_k=ext, xsq_ext=xsq_ext[r:r + bn], ysq_ext=ysq_ext, thr1=ws.thr1[r:r + bn],
-                        cert_eps=ceps) if ext else {}
+            cert = dict(cx, xsq_ext=xsq_ext[r:r + bn], thr1=ws.thr1[r:r + bn]) if ext else {}
             _gemm(data.hi[r:r + bn], data.lo[r:r + bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE,
                   xsq=xsq[r:r + bn], ysq=cents.ysq, thr=ws.thr[r:r + bn], cand=ws.cand,
                   cand_cnt=ws.cand_cnt, cand_cap=ws.cap, **cert)

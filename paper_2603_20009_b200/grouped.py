@@ -138,7 +138,9 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
     kap = tc_kappa(dp, GATE_KPAIR)
     native.call("skm_gate_threshold", ptr(ws.tau), data.n, float(plan.gate[0]), int(plan.sentinel), ptr(ws.thr),
                 ptr(xsq), ptr(cents.ysq_max), float(kap), st)
-    ext, xsq_ext, ysq_ext, ceps = cert_extension(data, cents, plan, ws.tau, ws.thr1, data.n, ws.nowin)
+    cx = cert_extension(data, cents, plan, ws.tau, ws.thr1, data.n, ws.nowin)
+    ext = cx.get("ext_k", 0)
+    xsq_ext = cx.get("xsq_ext")
     fld = padded_ld(dp + ext)
     ga_hi, ga_lo = ws.front_buffers(fld)
     k = cents.k
@@ -151,8 +153,7 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
                     ptr(ws.bx_ext) if ext else None, ptr(ws.bthr1) if ext else None, st,
                     nbytes=16.0 * bn * (dp + ext) + 24.0 * bn)
         cr = lay.row_crange[rm.long()].contiguous()
-        cert = dict(ext_k=ext, xsq_ext=ws.bx_ext[:bn], ysq_ext=ysq_ext, thr1=ws.bthr1[:bn],
-                    cert_eps=ceps) if ext else {}
+        cert = dict(cx, xsq_ext=ws.bx_ext[:bn], thr1=ws.bthr1[:bn]) if ext else {}
         _gemm(ga_hi[:bn], ga_lo[:bn], cents.hi, cents.lo, bn, k, dp, native.GEMM_GATE, xsq=ws.bx[:bn],
               ysq=cents.ysq, thr=ws.bthr[:bn], cand=ws.cand, cand_cnt=ws.cand_cnt, cand_cap=ws.cap,
               row_crange=cr, tile_nrange=tile_ranges(cr), **cert)

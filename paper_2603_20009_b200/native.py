@@ -42,6 +42,7 @@ class GemmParams(C.Structure):
         ("row_offset", _ll),
         ("ext_k", _i), ("xsq_ext", _vp), ("ysq_ext", _vp), ("thr1", _vp), ("cert_eps", _f),
         ("row_crange", _vp), ("tile_nrange", _vp),
+        ("ext_hi_only", _i),
     ]
 
 

@@ -44,7 +44,7 @@ def test_nowin_fit_matches_exact_stats(name):
 
     def spy(data, cents, plan, *a, **kw):
         out = orig(data, cents, plan, *a, **kw)
-        if out[0] == data.d - plan.d_prime:
+        if out.get("ext_k") == data.d - plan.d_prime:
             calls.append(1)
         return out
 
