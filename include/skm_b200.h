@@ -239,8 +239,19 @@ typedef struct skm_scan_params {
    * fb_rows, count in *fb_count -- both device workspace, fb_rows >= n_rows entries) are then
    * scanned by the exact kernel.  Same outputs as flat = 0. */
   int flat; int* fb_rows; unsigned int* fb_count;
+  /* deferred certified entries (exact_work_stats = false, list mode, flat = 0): rows with
+   * skip_cert[i] != 0 (skm_defer_cert_flags) leave their CAND_CERT0 entries out of the scan and
+   * record each tau improvement {centroid, tau bits} in imp[i * 32 + t] (count imp_cnt[i]);
+   * skm_deferred_cert_count then settles those entries' survivor decisions.  Batch-local i. */
+  const int* skip_cert; int* imp; int* imp_cnt;
 } skm_scan_params;
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
+/* skip[i] = 1 iff batch row i's candidate list holds certified entries and at most 32 others. */
+int skm_defer_cert_flags(const int* cand, const int* cand_cnt, int cap, int n_rows, int* skip, void* stream);
+/* After skm_pruned_scan with skip_cert: survivors (+ block_dims[0] dims each) of the deferred
+ * entries, taken under the tau each would have met in the in-order walk (tau_seed: the rows'
+ * tau before the scan, global rows); counters or group_counters as the scan's. */
+int skm_deferred_cert_count(const skm_scan_params* p, const float* tau_seed, void* stream);
 
 /* ---- exact top-k + ETR tally ------------------------------------------------------- */
 /* k smallest of each row by (value, column) ascending, ties to the lower column (stable

@@ -97,7 +97,16 @@ struct ScanArgs {
   unsigned long long* group_counters;
   // optional: the row count is read from the device (the flat pass's fallback list length)
   const unsigned int* n_rows_dev;
+  // deferred certified entries (exact_work_stats = false, full-d certificate): rows with
+  // skip_cert[rl] != 0 leave their CAND_CERT0 entries out of the queue -- such a column never
+  // replaces the best -- and record each tau improvement {j, tau bits} in imp[rl][SCAN_IMP_MAX]
+  // (count imp_cnt[rl]); deferred_cert_count_kernel then settles the entries' survivor decisions
+  // under the tau each would have met (the last improvement at a lower index, else the seed)
+  const int* skip_cert;
+  int2* imp;
+  int* imp_cnt;
 };
+constexpr int SCAN_IMP_MAX = 32;  // improvements recorded per row (one per lane)
 
 // T[j][q][b][r] = C[j][d' + 64b + 4q + r] (0 beyond d)
 __global__ void build_tails_kernel(const float* __restrict__ cent, long long ldc, int k, int d, int d_prime, int nb,
@@ -365,6 +374,8 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     const float dl_base = a.kap > 0.0f ? __ldg(a.xsq + row) + *a.ysq_max : 0.0f;
     const float xs_row = a.kap > 0.0f ? __ldg(a.xsq + row) : 0.0f;
     const int best0 = best;
+    const bool skip = !DENSE && a.skip_cert != nullptr && a.skip_cert[rl] != 0;
+    int nimp = 0;
     int ver = 0;  // bumped whenever tau tightens
     int src = 0, F = 0, D = 0, R = 0;
     // slot state: all lanes of a slot hold spos/snxt; the leader also walks (srun, sb, sver)
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
           }
         }
         const float dl = a.kap * (dl_base + p);
-        if (ok) ok = !(__fsub_rn(p, dl) > __fmul_rn(tcur, f0));
+        if (ok) ok = !(__fsub_rn(p, dl) > __fmul_rn(tcur, f0)) && !(skip && cert);
         const unsigned m = __ballot_sync(FULL, ok);
         if (ok) {
           const int qs = (F + __popc(m & ((1u << lane) - 1u))) % SCAN_WINDOW;
@@ -601,6 +612,11 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
         if (!ev) {
           R += min(32, D - R);
         } else if (ev_improve) {
+          if (skip) {  // at most one improvement per queued (uncertified) entry: <= SCAN_IMP_MAX
+            if (lane == 0 && nimp < SCAN_IMP_MAX)
+              a.imp[static_cast<long long>(rl) * SCAN_IMP_MAX + nimp] = make_int2(ev_j, __float_as_int(ev_run));
+            ++nimp;
+          }
           tcur = ev_run;
           best = ev_j;
           ++ver;
@@ -704,6 +720,7 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
       a.tau[row] = tcur;
       a.assign[row] = best;
       changed_acc += (best != best0);
+      if (skip) a.imp_cnt[rl] = nimp;
     }
     __syncwarp();
   }
@@ -718,6 +735,81 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
     warp_add_u64(blocks_acc, &a.counters_ext[0]);  // speculative block sums computed
     if (lane == 0 && waves_acc) atomicAdd(&a.counters_ext[1], waves_acc);  // warp waves executed
     warp_add_u64(exact_acc, &a.counters_ext[3]);  // candidates re-evaluated with the exact chain
+  }
+}
+
+// skip[rl] = 1 when row rl's list holds certified entries and at most SCAN_IMP_MAX uncertified
+// ones (so its improvements fit the record), 0 otherwise (the scan then queues every entry).
+__global__ void defer_cert_flags_kernel(const int2* __restrict__ cand, const int* __restrict__ cand_cnt, int cap,
+                                        int n_rows, int* __restrict__ skip) {
+  const int rl = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (rl >= n_rows) return;
+  const int cnt = cand_cnt[rl];
+  int u = 0, c = 0;
+  if (cnt <= cap) {
+    const int2* row = cand + static_cast<long long>(rl) * cap;
+    for (int e = lane; e < cnt; e += 32) {
+      const bool cert = row[e].x < 0;
+      u += !cert;
+      c += cert;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if (lane == 0) skip[rl] = (cnt <= cap && c > 0 && u <= SCAN_IMP_MAX) ? 1 : 0;
+}
+
+// The survivor decisions of the entries a skip row left out of its scan, exactly as the scan's
+// in-order resolver takes them for a certified entry: under the tau in force at index j (the
+// last recorded improvement at a lower index, else the seed tau), p +- D settles the front
+// gate fl(tau F0), and an unsettled one takes the reference's chain p.  A survivor is a
+// certified block-0 prune: dims touched += block_dims[0].  One warp per batch row.
+__global__ void deferred_cert_count_kernel(const ScanArgs a, const float* __restrict__ tau_seed) {
+  const int rl = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  if (rl >= a.n_rows || !a.skip_cert[rl]) return;
+  const int cnt = a.cand_cnt[rl];
+  const long long row = a.row_map ? static_cast<long long>(a.row_map[rl]) : a.row0 + rl;
+  const int nimp = a.imp_cnt[rl];
+  const int2 im = lane < nimp ? a.imp[static_cast<long long>(rl) * SCAN_IMP_MAX + lane] : make_int2(0x7fffffff, 0);
+  const float ts = tau_seed[row];
+  const float f0 = __ldg(a.theta);
+  const float xs_row = __ldg(a.xsq + row);
+  const float dl_base = xs_row + *a.ysq_max;
+  const int2* lrec = a.cand + static_cast<long long>(rl) * a.cap;
+  int surv = 0;
+  for (int e0 = 0; e0 < cnt; e0 += 32) {
+    const int e = e0 + lane;
+    const int2 r = e < cnt ? lrec[e] : make_int2(0, 0);
+    const bool cert = e < cnt && r.x < 0;
+    const int j = r.x & 0x7fffffff;
+    int c = 0;
+    for (int t = 0; t < nimp; ++t) c += __shfl_sync(FULL, im.x, t) < j;
+    const float ti = __int_as_float(__shfl_sync(FULL, im.y, c > 0 ? c - 1 : 0));
+    if (!cert) continue;
+    const float thr0 = __fmul_rn(c > 0 ? ti : ts, f0);
+    const float p = __int_as_float(r.y);
+    const float dl = a.kap * (dl_base + p);
+    if (__fsub_rn(p, dl) > thr0) continue;
+    if (!(__fadd_rn(p, dl) > thr0)) {
+      ++surv;
+      continue;
+    }
+    const float pe = exact_front_dist(a.x + row * a.ldx, a.cent + static_cast<long long>(j) * a.ldc, a.d_prime,
+                                      a.chain_flavour, a.chain_q, xs_row, __ldg(a.ysq + j));
+    surv += !(pe > thr0);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) surv += __shfl_xor_sync(FULL, surv, o);
+  if (lane == 0 && surv) {
+    unsigned long long* ctr = a.group_counters ? a.group_counters + 3LL * __ldg(a.row_group + row) : a.counters;
+    atomicAdd(&ctr[0], static_cast<unsigned long long>(surv));
+    atomicAdd(&ctr[1], static_cast<unsigned long long>(surv) * static_cast<unsigned long long>(__ldg(a.block_dims)));
   }
 }
 

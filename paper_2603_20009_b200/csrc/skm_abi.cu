@@ -710,6 +710,55 @@ int skm_gate_threshold(const float* tau, int n, float f0, int sentinel, float* t
   return SKM_OK;
 }
 
+int skm_defer_cert_flags(const int* cand, const int* cand_cnt, int cap, int n_rows, int* skip, void* stream) {
+  if (n_rows <= 0) return SKM_OK;
+  if (!cand || !cand_cnt || !skip || cap <= 0) return fail(SKM_E_ARG, "defer_cert_flags: null argument");
+  { skm::defer_cert_flags_kernel<<<(n_rows + 7) / 8, 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const int2*>(cand), cand_cnt, cap, n_rows, skip); SKM_COUNT_LAUNCH(); }
+  SKM_LAUNCH_CHECK("defer_cert_flags");
+  return SKM_OK;
+}
+
+int skm_deferred_cert_count(const skm_scan_params* p, const float* tau_seed, void* stream) {
+  if (!p || !tau_seed) return fail(SKM_E_ARG, "deferred_cert_count: null argument");
+  if (p->n_rows <= 0) return SKM_OK;
+  if (!p->skip_cert || !p->imp || !p->imp_cnt || !p->cand || !p->cand_cnt || p->kap <= 0.0f || !p->xsq ||
+      !p->ysq || !p->ysq_max || !p->cent || !p->theta || !p->block_dims)
+    return fail(SKM_E_ARG, "deferred_cert_count: needs the scan's list, skip/imp records and exact-chain inputs");
+  if ((p->row_group != nullptr) != (p->group_counters != nullptr) || (!p->group_counters && !p->counters))
+    return fail(SKM_E_ARG, "deferred_cert_count: counters or row_group + group_counters");
+  skm::ScanArgs a{};
+  a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
+  a.cand_cnt = p->cand_cnt;
+  a.cap = p->cap;
+  a.n_rows = p->n_rows;
+  a.row0 = p->row0;
+  a.row_map = p->row_map;
+  a.x = p->x;
+  a.ldx = p->ldx;
+  a.d_prime = p->d_prime;
+  a.theta = p->theta;
+  a.block_dims = p->block_dims;
+  a.counters = p->counters;
+  a.kap = p->kap;
+  a.xsq = p->xsq;
+  a.ysq = p->ysq;
+  a.ysq_max = p->ysq_max;
+  a.cent = p->cent;
+  a.ldc = p->ldc;
+  a.chain_flavour = p->chain_flavour;
+  a.chain_q = p->chain_q;
+  a.row_group = p->row_group;
+  a.group_counters = p->group_counters;
+  a.skip_cert = p->skip_cert;
+  a.imp = reinterpret_cast<int2*>(p->imp);
+  a.imp_cnt = p->imp_cnt;
+  { skm::deferred_cert_count_kernel<<<(p->n_rows + 7) / 8, 256, 0, as_stream(stream)>>>(a, tau_seed);
+    SKM_COUNT_LAUNCH(); }
+  SKM_LAUNCH_CHECK("deferred_cert_count");
+  return SKM_OK;
+}
+
 int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   if (!p) return fail(SKM_E_ARG, "pruned_scan: null params");
   if (p->n_rows <= 0) return SKM_OK;
@@ -756,6 +805,11 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   a.chain_q = p->chain_q;
   a.row_group = p->row_group;
   a.group_counters = p->group_counters;
+  a.skip_cert = p->skip_cert;
+  a.imp = reinterpret_cast<int2*>(p->imp);
+  a.imp_cnt = p->imp_cnt;
+  if (a.skip_cert && (!a.imp || !a.imp_cnt || p->flat || p->dense_mode || a.kap <= 0.0f))
+    return fail(SKM_E_ARG, "pruned_scan: skip_cert needs imp/imp_cnt, list mode, flat = 0 and kap > 0");
   if ((a.row_group != nullptr) != (a.group_counters != nullptr))
     return fail(SKM_E_ARG, "pruned_scan: row_group and group_counters go together");
   if (a.kap > 0.0f && (!a.xsq || !a.ysq || !a.ysq_max || !a.cent))

@@ -103,6 +103,9 @@ def nowin_cert_eps(d: int, ext: int, hi_only: bool = True) -> float:
 
 
 NOWIN_HI_ONLY = os.environ.get("SKM_NOWIN_HI_ONLY", "1") != "0"
+# the certified entries of a full-d certificate leave the in-order scan: it records each row's
+# tau improvements and skm_deferred_cert_count settles their survivor decisions in parallel
+DEFER_CERT = os.environ.get("SKM_DEFER_CERT", "1") != "0"
 
 
 def cert_extension(data, cents, plan, tau: torch.Tensor, thr1: torch.Tensor, n: int, nowin: bool) -> dict:
@@ -489,6 +492,16 @@ class Workspace:
         self.wcss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.changed = torch.zeros(1, dtype=torch.int64, device=dev)
 
+    def defer_buffers(self):
+        """Deferred certified entries (exact_work_stats = False): seed-tau copy (global rows),
+        per-batch-row skip flags, improvement records [batch][32] {j, tau bits} and counts."""
+        if getattr(self, "_defer", None) is None:
+            b = self.batch
+            self._defer = (torch.empty_like(self.tau), torch.empty(b, dtype=torch.int32, device=self.dev),
+                           torch.empty((b, 32, 2), dtype=torch.int32, device=self.dev),
+                           torch.empty(b, dtype=torch.int32, device=self.dev))
+        return self._defer
+
     def front_buffers(self, fld: int):
         """Gathered (hi, lo) front rows of one cluster-ordered batch."""
         if self._front is None or self._front[0].shape[1] < fld:
@@ -646,6 +659,11 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
     cx = cert_extension(data, cents, plan, tau, ws.thr1[row0:row0 + n], n, ws.nowin and seed_tau)
     ext = cx.get("ext_k", 0)
     xsq_ext = cx.get("xsq_ext")
+    # full-d certificate: the certified entries leave the in-order scan (DEFER_CERT)
+    defer = DEFER_CERT and ext > 0 and ext == d - dp and not ws.flat
+    if defer:
+        tau_seed, skip, imp, imp_cnt = ws.defer_buffers()
+        tau_seed[row0:row0 + n].copy_(tau)
     k = cents.k
     ordered = order is not None and row0 == 0 and n == data.n
     if ordered:
@@ -684,7 +702,12 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
         if PRUNE_HIST is not None:
             sp.prune_hist = PRUNE_HIST.data_ptr()
         _scan_exact_args(sp, data, cents, ws, xsq, kap, plan.sentinel)
+        if defer:
+            native.call("skm_defer_cert_flags", ptr(ws.cand), ptr(ws.cand_cnt), ws.cap, bn, ptr(skip), st)
+            sp.skip_cert, sp.imp, sp.imp_cnt = skip.data_ptr(), imp.data_ptr(), imp_cnt.data_ptr()
         native.call("skm_pruned_scan", C.byref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        if defer:
+            native.call("skm_deferred_cert_count", C.byref(sp), ptr(tau_seed), st)
         if ws.cap < k:
             # rows whose candidate list overflowed the slab: dense distance rows, same kernel
             over = torch.nonzero(ws.cand_cnt[:bn] > ws.cap).flatten()

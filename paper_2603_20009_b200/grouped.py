@@ -33,6 +33,7 @@ from . import native
 from .config import KMeansConfig, WorkCounters, initial_d_prime, pruning_supported
 from .device import padded_ld, ptr, stream_handle
 from .engine import (
+    DEFER_CERT,
     FLAT_MAX_CHANGED,
     GATE_KPAIR,
     NOWIN_SURV_FRAC,
@@ -141,6 +142,10 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
     cx = cert_extension(data, cents, plan, ws.tau, ws.thr1, data.n, ws.nowin)
     ext = cx.get("ext_k", 0)
     xsq_ext = cx.get("xsq_ext")
+    defer = DEFER_CERT and ext > 0 and ext == d - dp and not ws.flat
+    if defer:
+        tau_seed, skip, imp, imp_cnt = ws.defer_buffers()
+        tau_seed.copy_(ws.tau)
     fld = padded_ld(dp + ext)
     ga_hi, ga_lo = ws.front_buffers(fld)
     k = cents.k
@@ -173,7 +178,12 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
         sp.row_group, sp.group_counters = lay.row_group.data_ptr(), gcount.data_ptr()
         if SCAN_FLAT and ws.flat and not plan.sentinel:
             sp.flat, sp.fb_rows, sp.fb_count = 1, ws.fb_rows.data_ptr(), ws.fb_count.data_ptr()
+        if defer:
+            native.call("skm_defer_cert_flags", ptr(ws.cand), ptr(ws.cand_cnt), ws.cap, bn, ptr(skip), st)
+            sp.skip_cert, sp.imp, sp.imp_cnt = skip.data_ptr(), imp.data_ptr(), imp_cnt.data_ptr()
         native.call("skm_pruned_scan", ctypes_ref(sp), st, tag="pruned_scan", nbytes=4.0 * bn * (d - dp) + 16.0 * bn)
+        if defer:
+            native.call("skm_deferred_cert_count", ctypes_ref(sp), ptr(tau_seed), st)
 
 
 def ctypes_ref(obj):

@@ -76,6 +76,7 @@ class ScanParams(C.Structure):
         ("cent", _vp), ("ldc", _ll), ("chain_flavour", _i), ("chain_q", _i),
         ("row_group", _vp), ("group_counters", _vp),
         ("flat", _i), ("fb_rows", _vp), ("fb_count", _vp),
+        ("skip_cert", _vp), ("imp", _vp), ("imp_cnt", _vp),
     ]
 
 
@@ -115,6 +116,8 @@ _SIGS = {
     "skm_assign_stats": ([_vp, _vp, _vp, _i, _vp, _vp, _vp, _ll, _vp], _i),
     "skm_build_tails": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
     "skm_gate_threshold": ([_vp, _i, _f, _i, _vp, _vp, _vp, _f, _vp], _i),
+    "skm_defer_cert_flags": ([_vp, _vp, _i, _i, _vp, _vp], _i),
+    "skm_deferred_cert_count": ([_vp, _vp, _vp], _i),
     "skm_pruned_scan": ([C.POINTER(ScanParams), _vp], _i),
     "skm_first_nonfinite": ([_vp, _ll, _ll, _i, _vp, _vp], _i),
     "skm_wcss_workspace_bytes": ([], _ll),
