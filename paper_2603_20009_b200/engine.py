@@ -121,9 +121,12 @@ def cert_extension(data, cents, plan, tau: torch.Tensor, thr1: torch.Tensor, n: 
         return {}
     st = stream_handle()
     if nowin and dp < d:
+        # the whole tail: a prefix would certify too (block sums >= 0, the running sum only
+        # grows), but measured on c2 a 256-768 column prefix certified almost nothing
+        ext = d - dp
         native.call("skm_gate_threshold", ptr(tau), n, 1.0, 0, ptr(thr1), None, None, 0.0, st)
-        return dict(ext_k=d - dp, xsq_ext=data.norms(d), ysq_ext=cents.full_norms()[0],
-                    cert_eps=nowin_cert_eps(d, d - dp, NOWIN_HI_ONLY), ext_hi_only=NOWIN_HI_ONLY)
+        return dict(ext_k=ext, xsq_ext=data.norms(dp + ext), ysq_ext=cents.ext_norms(dp + ext),
+                    cert_eps=nowin_cert_eps(d, ext, NOWIN_HI_ONLY), ext_hi_only=NOWIN_HI_ONLY, nowin=True)
     if dp + CERT_EXT > d or plan.widths[0] != 64:
         return {}
     native.call("skm_gate_threshold", ptr(tau), n, float(plan.gate[1]), 0, ptr(thr1), None, None, 0.0, st)
@@ -357,14 +360,12 @@ class Centroids:
         self.ysq_ext = None
         self.ysq_max = torch.zeros(1, dtype=torch.float32, device=c.device)  # max_j ysq (error bounds)
 
-    def full_norms(self):
-        """(ysq over all d columns, its max) for the full-d gate (exact_work_stats = False)."""
-        if getattr(self, "ysq_full", None) is None:
-            self.ysq_full = torch.empty(self.k, dtype=torch.float32, device=self.c.device)
-            self.ysq_full_max = torch.zeros(1, dtype=torch.float32, device=self.c.device)
-        native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, self.d, ptr(self.ysq_full), stream_handle())
-        native.call("skm_max_f32", ptr(self.ysq_full), self.k, ptr(self.ysq_full_max), stream_handle())
-        return self.ysq_full, self.ysq_full_max
+    def ext_norms(self, dims: int) -> torch.Tensor:
+        """ysq over the first ``dims`` columns for the full-d certificate (exact_work_stats = False)."""
+        if getattr(self, "ysq_cert", None) is None:
+            self.ysq_cert = torch.empty(self.k, dtype=torch.float32, device=self.c.device)
+        native.call("skm_row_sq_norms", ptr(self.c), self.ld, self.k, dims, ptr(self.ysq_cert), stream_handle())
+        return self.ysq_cert
 
     def refresh(self, dims: int, d_prime: int | None):
         """Recompute split + norms over `dims` (+ tails at d_prime) after an update."""
@@ -402,6 +403,7 @@ def _gemm(a_hi, a_lo, b_hi, b_lo, M, N, K, mode, **kw):
     p.ext_k = kw.pop("ext_k", 0)
     p.cert_eps = kw.pop("cert_eps", 0.0)
     p.ext_hi_only = int(kw.pop("ext_hi_only", 0))
+    kw.pop("nowin", None)
     for name, t in kw.items():
         if t is not None:
             setattr(p, name, t.data_ptr())
@@ -660,7 +662,7 @@ def pruned_assign_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan: 
     ext = cx.get("ext_k", 0)
     xsq_ext = cx.get("xsq_ext")
     # full-d certificate: the certified entries leave the in-order scan (DEFER_CERT)
-    defer = DEFER_CERT and ext > 0 and ext == d - dp and not ws.flat
+    defer = DEFER_CERT and cx.get("nowin", False) and not ws.flat
     if defer:
         tau_seed, skip, imp, imp_cnt = ws.defer_buffers()
         tau_seed[row0:row0 + n].copy_(tau)

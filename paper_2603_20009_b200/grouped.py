@@ -142,7 +142,7 @@ def _grouped_pruned_pass(data: DeviceData, cents: Centroids, ws: Workspace, plan
     cx = cert_extension(data, cents, plan, ws.tau, ws.thr1, data.n, ws.nowin)
     ext = cx.get("ext_k", 0)
     xsq_ext = cx.get("xsq_ext")
-    defer = DEFER_CERT and ext > 0 and ext == d - dp and not ws.flat
+    defer = DEFER_CERT and cx.get("nowin", False) and not ws.flat
     if defer:
         tau_seed, skip, imp, imp_cnt = ws.defer_buffers()
         tau_seed.copy_(ws.tau)
