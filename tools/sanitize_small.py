@@ -23,4 +23,9 @@ r3 = skb.fit(x, skb.KMeansConfig(k=40, max_iters=6, seed=4, etr=skb.EtrConfig(n_
 q = x[:100]
 gt = skb.brute_force_topk(x, q, 10)
 pe = skb.probe_eval(r.centroids, skb.build_cluster_lists(r.assignments, r.k), x, q, gt, 5, top_ks=(10,))
-print("ok", r.k, r2.k, int(a.max()), h.k, r3.terminated_by, round(pe["recall_at_10"], 3))
+# exact_work_stats=False: full-d certificate (hi x hi extension) + deferred certified entries, flat
+# and grouped paths included
+r4 = skb.fit(x, skb.KMeansConfig(k=48, max_iters=4, seed=1, exact_work_stats=False))
+h2 = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=60, seed=3, exact_work_stats=False))
+assert np.array_equal(r4.assignments, r.assignments) and np.array_equal(h2.assignments, h.assignments)
+print("ok", r.k, r2.k, int(a.max()), h.k, r3.terminated_by, round(pe["recall_at_10"], 3), "nowin ok")
