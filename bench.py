@@ -206,7 +206,7 @@ def cpu_baseline_sample(args, x: np.ndarray) -> dict | None:
 
 def run_extra(name: str, dev) -> dict:
     """One secondary BASELINE config (EXTRA[name]) at N = 1: the reference generator's rows,
-    one warm-up fit, the median of 2 timed fits (CUDA events)."""
+    one warm-up fit, the median of 2 timed fits (5 for the small, host-bound c1; CUDA events)."""
     import torch
     from paper_2603_20009_b200 import api
     from paper_2603_20009_b200.config import EtrConfig, KMeansConfig
@@ -224,7 +224,8 @@ def run_extra(name: str, dev) -> dict:
     r = api.fit_device(xd, d, ccfg, rot)  # warm-up
     torch.cuda.synchronize()
     times = []
-    for _ in range(2):
+    # small configs are host/launch-bound and their fit time moves with host noise: more samples
+    for _ in range(5 if n * d < 50_000_000 else 2):
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()

@@ -43,8 +43,9 @@ namespace skm {
 constexpr int SCAN_DEPTH = SKM_SCAN_DEPTH;     // consecutive blocks per candidate per wave
 constexpr int SCAN_SLOTS = 32 / SCAN_DEPTH;    // candidates in flight per wave
 constexpr int SCAN_WINDOW = SKM_SCAN_WINDOW;   // in-flight queue positions per warp
-constexpr int SCAN_NB_MAX = 104;               // tail blocks supported (d - d' <= 6656): 4 warps x
-                                               // 512 B per block of x tail + records fit in 227 KB
+constexpr int SCAN_NB_MAX = 104;               // tail blocks of the default 4-warp CTA (d - d' <= 6656):
+                                               // 4 warps x 512 B per block of x tail + records fit in 227 KB
+constexpr int SCAN_NB_MAX_WIDE = 432;          // one warp per CTA (longer tails, d - d' <= 27648)
 constexpr int SCAN_WARPS = SKM_SCAN_WARPS;     // warps per CTA
 
 struct ScanArgs {
@@ -269,17 +270,21 @@ constexpr int SCAN_EXS = 2;  // centroid fronts staged per cooperative re-evalua
 #ifndef SKM_SCAN_MINB
 #define SKM_SCAN_MINB 3  // 12 warps per SM: caps registers at 168 (the exact-chain call site raised it to 231)
 #endif
-template <bool DENSE>
-__global__ void __launch_bounds__(SCAN_WARPS * 32, SKM_SCAN_MINB)
+// WARPS: warps per CTA.  The default SCAN_WARPS instantiation serves tails up to SCAN_NB_MAX
+// blocks; the one-warp instantiation (shared memory of a whole CTA for one row's tail) serves
+// longer tails up to SCAN_NB_MAX_WIDE.  The per-row algorithm is the same.
+template <bool DENSE, int WARPS = SCAN_WARPS>
+__global__ void __launch_bounds__(WARPS * 32, WARPS == SCAN_WARPS ? SKM_SCAN_MINB : 1)
     pruned_scan_kernel(const ScanArgs a) {
+  constexpr int NBMAX = WARPS == SCAN_WARPS ? SCAN_NB_MAX : SCAN_NB_MAX_WIDE;
   extern __shared__ float scan_smem[];
-  __shared__ ScanWarpSmem wsm[SCAN_WARPS];
-  __shared__ float s_theta[SCAN_NB_MAX + 1];
-  __shared__ int s_bdcum[SCAN_NB_MAX + 1];  // dims touched through block b (prefix at b+1)
+  __shared__ ScanWarpSmem wsm[WARPS];
+  __shared__ float s_theta[NBMAX + 1];
+  __shared__ int s_bdcum[NBMAX + 1];  // dims touched through block b (prefix at b+1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = a.nb;
-  if (threadIdx.x <= nb) s_theta[threadIdx.x] = a.theta[threadIdx.x];
+  for (int i = threadIdx.x; i <= nb; i += WARPS * 32) s_theta[i] = a.theta[i];
   if (threadIdx.x == 0) {
     int c = 0;
     s_bdcum[0] = 0;
@@ -813,9 +818,9 @@ __global__ void deferred_cert_count_kernel(const ScanArgs a, const float* __rest
   }
 }
 
-inline size_t scan_dyn_smem(int nb, int d_prime = 0, bool ex_stage = false) {
+inline size_t scan_dyn_smem(int nb, int d_prime = 0, bool ex_stage = false, int warps = SCAN_WARPS) {
   const int dpp = (d_prime + 3) & ~3;
-  return static_cast<size_t>(SCAN_WARPS) * (64 * nb + SCAN_WINDOW * nb + (ex_stage ? (1 + SCAN_EXS) * dpp : 0)) * 4;
+  return static_cast<size_t>(warps) * (64 * nb + SCAN_WINDOW * nb + (ex_stage ? (1 + SCAN_EXS) * dpp : 0)) * 4;
 }
 
 }  // namespace skm

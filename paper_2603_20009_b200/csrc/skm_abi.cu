@@ -759,10 +759,51 @@ int skm_deferred_cert_count(const skm_scan_params* p, const float* tau_seed, voi
   return SKM_OK;
 }
 
+// One warp per CTA: the scan for tails of SCAN_NB_MAX < nb <= SCAN_NB_MAX_WIDE blocks (d - d' up
+// to 27648).  Same per-row algorithm and results as the 4-warp kernel; exact re-evaluations read
+// the fronts from global memory when they do not fit beside the tail staging.
+static int launch_pruned_scan_wide(skm::ScanArgs a, const skm_scan_params* p, void* stream) {
+  static int dyn_wide = -1;
+  if (dyn_wide < 0) {
+    int dv = 0, optin = 0;
+    cudaGetDevice(&dv);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dv);
+    cudaFuncAttributes fa{}, fb{};
+    cudaFuncGetAttributes(&fa, skm::pruned_scan_kernel<false, 1>);
+    cudaFuncGetAttributes(&fb, skm::pruned_scan_kernel<true, 1>);
+    dyn_wide = optin - static_cast<int>(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes));
+  }
+  if (skm::scan_dyn_smem(p->nb, 0, false, 1) > static_cast<size_t>(dyn_wide))
+    return fail(SKM_E_ARG, "pruned_scan: tail too long for the shared-memory staging");
+  a.ex_stage = (a.kap > 0.0f && skm::scan_dyn_smem(p->nb, p->d_prime, true, 1) <= static_cast<size_t>(dyn_wide)) ? 1 : 0;
+  const size_t smem = skm::scan_dyn_smem(p->nb, p->d_prime, a.ex_stage != 0, 1);
+  cudaStream_t st = as_stream(stream);
+  static unsigned long long set_mask_d = 0, set_mask_l = 0;
+  if (first_use_on_device(set_mask_d))
+    cudaFuncSetAttribute(skm::pruned_scan_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_wide);
+  if (first_use_on_device(set_mask_l))
+    cudaFuncSetAttribute(skm::pruned_scan_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_wide);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (p->dense_mode)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skm::pruned_scan_kernel<true, 1>, 32, smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skm::pruned_scan_kernel<false, 1>, 32, smem);
+  const int blocks = std::max(1, std::min(p->n_rows, sms * std::max(per_sm, 1)));
+  if (p->dense_mode)
+    { skm::pruned_scan_kernel<true, 1><<<blocks, 32, smem, st>>>(a); SKM_COUNT_LAUNCH(); }
+  else
+    { skm::pruned_scan_kernel<false, 1><<<blocks, 32, smem, st>>>(a); SKM_COUNT_LAUNCH(); }
+  SKM_LAUNCH_CHECK("pruned_scan_wide");
+  return SKM_OK;
+}
+
 int skm_pruned_scan(const skm_scan_params* p, void* stream) {
   if (!p) return fail(SKM_E_ARG, "pruned_scan: null params");
   if (p->n_rows <= 0) return SKM_OK;
-  if (p->nb <= 0 || p->nb > skm::SCAN_NB_MAX) return fail(SKM_E_ARG, "pruned_scan: tail block count out of range");
+  if (p->nb <= 0 || p->nb > skm::SCAN_NB_MAX_WIDE)
+    return fail(SKM_E_ARG, "pruned_scan: tail block count out of range (d - d' > 27648)");
   skm::ScanArgs a{};
   a.cand = reinterpret_cast<decltype(a.cand)>(p->cand);
   a.cand_cnt = p->cand_cnt;
@@ -826,8 +867,9 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
     cudaFuncGetAttributes(&fb, skm::pruned_scan_kernel<true>);
     dyn_limit = optin - static_cast<int>(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes));
   }
-  if (skm::scan_dyn_smem(p->nb) > static_cast<size_t>(dyn_limit))
-    return fail(SKM_E_ARG, "pruned_scan: tail too long for the shared-memory staging");
+  // tails longer than the 4-warp CTA's staging: the one-warp instantiation (no flat pass)
+  const bool wide = p->nb > skm::SCAN_NB_MAX || skm::scan_dyn_smem(p->nb) > static_cast<size_t>(dyn_limit);
+  if (wide) return launch_pruned_scan_wide(a, p, stream);
   // exact re-evaluations from shared memory when the row's front + SCAN_EXS centroid fronts fit
   a.ex_stage = (a.kap > 0.0f && skm::scan_dyn_smem(p->nb, p->d_prime, true) <= static_cast<size_t>(dyn_limit)) ? 1 : 0;
   if (getenv("SKM_SCAN_EXSTAGE") && atoi(getenv("SKM_SCAN_EXSTAGE")) == 0) a.ex_stage = 0;

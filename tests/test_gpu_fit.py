@@ -322,10 +322,10 @@ def test_fit_edge_shapes_vs_oracle(n, d, k):
         assert not res.assignments.any()
 
 
-@pytest.mark.parametrize("d", [3072, 4096])
+@pytest.mark.parametrize("d", [3072, 4096, 8192])
 def test_fit_large_d_vs_oracle(d):
     """Embedding sizes beyond c2 (d' = 384 / 512, 42 / 56 tail blocks: the scan's shared-memory
-    staging sized at run time) against the oracle: same d' trajectory, >= 99.9% assignment
+    staging sized at run time; d = 8192: 112-118 tail blocks, the one-warp scan) against the oracle: same d' trajectory, >= 99.9% assignment
     agreement every iteration, centroids within 1e-4."""
     import paper_2603_20009_b200 as skb
     from conftest import make_skewed_blobs

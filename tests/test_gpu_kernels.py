@@ -213,7 +213,9 @@ def test_portable_matmul_bitwise():
 
 SCAN_CASES = [
     (0, 123, 77, 200, 25, False), (1, 123, 77, 200, 25, True), (2, 600, 900, 256, 32, False),
-    (3, 400, 1500, 1536, 192, False), (4, 300, 64, 96, 16, False), (5, 257, 300, 130, 40, True)]
+    (3, 400, 1500, 1536, 192, False), (4, 300, 64, 96, 16, False), (5, 257, 300, 130, 40, True),
+    # 120 tail blocks: beyond the 4-warp CTA's staging, served by the one-warp instantiation
+    (6, 64, 48, 8192, 512, False)]
 
 
 @pytest.mark.parametrize("seed,n,k,d,dp,sentinel", SCAN_CASES)
@@ -318,8 +320,10 @@ def test_pruned_scan_bitwise_vs_oracle(seed, n, k, d, dp, sentinel, exact, prev_
         valid = torch.arange(cap, device="cuda")[None, :] < cc.clamp(max=cap)[:, None]
         n_cert = int(((ci < 0) & valid).sum().item())
         print(f"certified block-0 prunes: {n_cert} of {int(valid.sum().item())} candidates")
-        if prev_mode == "mixed" and d >= 1024:
-            assert n_cert > 0  # re-assigning rows have far candidates: the extension must fire
+        if prev_mode == "mixed" and d >= 1024 and n >= 256:
+            # re-assigning rows have far candidates: the extension must fire (the 64-row d = 8192
+            # case has too few re-assigning rows to guarantee one)
+            assert n_cert > 0
         # certified entries carry the same centroid index (bit 31 aside) and partial distance
         assert int((ci & 0x7fffffff)[valid].max().item()) < k
     nb = len(widths)
