@@ -245,6 +245,8 @@ typedef struct skm_scan_params {
    * skm_deferred_cert_count then settles those entries' survivor decisions.  Batch-local i. */
   const int* skip_cert; int* imp; int* imp_cnt;
 } skm_scan_params;
+/* nb <= 104: 4-warp CTAs (flat pass available); 104 < nb <= 432 (d - d' <= 27648): one-warp CTAs
+ * with the same results, flat ignored; larger nb returns SKM_E_ARG. */
 int skm_pruned_scan(const skm_scan_params* p, void* stream);
 /* skip[i] = 1 iff batch row i's candidate list holds certified entries and at most 32 others. */
 int skm_defer_cert_flags(const int* cand, const int* cand_cnt, int cap, int n_rows, int* skip, void* stream);

@@ -1,6 +1,6 @@
 """Small end-to-end runs for compute-sanitizer (memcheck / racecheck; initcheck takes > 18 min
 once the ETR part runs): fit (pruned path with certification), sampled fit + final_assign,
-hierarchical, ETR fit, IVF probe evaluation."""
+hierarchical, ETR fit, IVF probe evaluation, a d = 8192 fit (one-warp scan)."""
 import os
 import sys
 
@@ -28,4 +28,9 @@ pe = skb.probe_eval(r.centroids, skb.build_cluster_lists(r.assignments, r.k), x,
 r4 = skb.fit(x, skb.KMeansConfig(k=48, max_iters=4, seed=1, exact_work_stats=False))
 h2 = skb.hierarchical_fit(x, skb.HierarchicalConfig(k_total=60, seed=3, exact_work_stats=False))
 assert np.array_equal(r4.assignments, r.assignments) and np.array_equal(h2.assignments, h.assignments)
+# long tail (d = 8192: 112+ tail blocks): the one-warp scan instantiation
+xw = make_skewed_blobs(400, 8192, 12, 5)
+r5 = skb.fit(xw, skb.KMeansConfig(k=16, max_iters=3, seed=1))
+r6 = skb.fit(xw, skb.KMeansConfig(k=16, max_iters=3, seed=1, exact_work_stats=False))
+assert np.array_equal(r5.assignments, r6.assignments)
 print("ok", r.k, r2.k, int(a.max()), h.k, r3.terminated_by, round(pe["recall_at_10"], 3), "nowin ok")
