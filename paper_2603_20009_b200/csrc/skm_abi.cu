@@ -868,7 +868,9 @@ int skm_pruned_scan(const skm_scan_params* p, void* stream) {
     dyn_limit = optin - static_cast<int>(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes));
   }
   // tails longer than the 4-warp CTA's staging: the one-warp instantiation (no flat pass)
-  const bool wide = p->nb > skm::SCAN_NB_MAX || skm::scan_dyn_smem(p->nb) > static_cast<size_t>(dyn_limit);
+  // (SKM_SCAN_FORCE_WIDE=1: every tail, for cross-checking the two instantiations)
+  static const bool force_wide = getenv("SKM_SCAN_FORCE_WIDE") && atoi(getenv("SKM_SCAN_FORCE_WIDE")) != 0;
+  const bool wide = force_wide || p->nb > skm::SCAN_NB_MAX || skm::scan_dyn_smem(p->nb) > static_cast<size_t>(dyn_limit);
   if (wide) return launch_pruned_scan_wide(a, p, stream);
   // exact re-evaluations from shared memory when the row's front + SCAN_EXS centroid fronts fit
   a.ex_stage = (a.kap > 0.0f && skm::scan_dyn_smem(p->nb, p->d_prime, true) <= static_cast<size_t>(dyn_limit)) ? 1 : 0;
