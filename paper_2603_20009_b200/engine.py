@@ -604,6 +604,9 @@ def exact_rows_argmin(data: DeviceData, cents: Centroids, ws: Workspace, rows_lo
                     ptr(ws.tau[row0:]), st)
 
 
+SCAN_TAIL_BLOCKS_MAX = 432  # csrc/scan.cuh SCAN_NB_MAX_WIDE (the one-warp instantiation)
+
+
 class PrunePlan:
     """Per-iteration constants of the pruned pass at a given d'."""
 
@@ -614,6 +617,11 @@ class PrunePlan:
         self.gate = sentinel_factors(f) if sentinel else f
         self.widths = widths
         self.nb = len(widths)
+        if self.nb > SCAN_TAIL_BLOCKS_MAX:
+            from .config import SuperKMeansError
+            raise SuperKMeansError(
+                f"tail of {d - d_prime} dims ({self.nb} blocks of 64) exceeds the device scan's "
+                f"{SCAN_TAIL_BLOCKS_MAX} blocks (d - d' <= {64 * SCAN_TAIL_BLOCKS_MAX})")
         self.d_prime = d_prime
         self.sentinel = sentinel
         key = (str(dev), d, d_prime, float(eps0), bool(sentinel))

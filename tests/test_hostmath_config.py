@@ -147,3 +147,17 @@ def test_chunked_generators_bitwise_reference_generators():
     from paper_2603_20009_b200 import synth
     assert np.array_equal(synth.make_blobs(5000, 37, 11, 3, chunk_rows=777), mb(5000, 37, 11, 3))
     assert np.array_equal(synth.make_skewed_blobs(4000, 96, 64, 0, chunk_rows=1000), msb(4000, 96, 64, 0))
+
+
+def test_scan_tail_limit_is_checked_on_the_host():
+    """Tails beyond the one-warp scan's staging raise a SuperKMeansError before any launch, and the
+    host limit equals the kernel's SCAN_NB_MAX_WIDE."""
+    import os
+    import re
+    from paper_2603_20009_b200.config import SuperKMeansError
+    from paper_2603_20009_b200.engine import SCAN_TAIL_BLOCKS_MAX, PrunePlan
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2603_20009_b200", "csrc", "scan.cuh")).read()
+    assert int(re.search(r"SCAN_NB_MAX_WIDE = (\d+);", src).group(1)) == SCAN_TAIL_BLOCKS_MAX
+    d = 16 + 64 * SCAN_TAIL_BLOCKS_MAX + 1
+    with pytest.raises(SuperKMeansError, match="exceeds the device scan"):
+        PrunePlan(d, 16, 2.1, False, "cpu")
