@@ -149,6 +149,27 @@ __global__ void gate_threshold_kernel(const float* __restrict__ tau, int n, floa
   }
 }
 
+#ifndef SKM_SCAN_TAIL_NOALLOC
+#define SKM_SCAN_TAIL_NOALLOC 0
+#endif
+// centroid tail loads (L2-resident, read once per wave).  A/B variants: 1 = no L1 allocation
+// (measured 5 % slower per c2 fit: L1 hits matter), 2 = L1::evict_last
+__device__ __forceinline__ float4 scan_tail_load(const float4* p) {
+#if SKM_SCAN_TAIL_NOALLOC == 2
+  float4 v;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+#elif SKM_SCAN_TAIL_NOALLOC
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 struct ScanWarpSmem {
   // per queue position (ring of SCAN_WINDOW)
   int qj[SCAN_WINDOW];
@@ -508,7 +529,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == SCAN_WARPS ? SKM_SCAN_MIN
         my_qs = spos % SCAN_WINDOW;
         const float4* cb = a.tails + static_cast<long long>(W.qj[my_qs]) * 16 * nb + myb;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) c4[q] = __ldg(cb + q * nb);
+        for (int q = 0; q < 16; ++q) c4[q] = scan_tail_load(cb + q * nb);
       }
       // ---- 4. in-order resolution, 32 positions per round; outcomes already decided under
       //         the current tau version are O(1), older ones are re-walked from the records
