@@ -419,7 +419,7 @@ def main():
         one_fit()
     barrier()
     # ---- timed region: K device-resident fits ----
-    prof = profiling.KernelTimer()
+    prof = profiling.KernelTimer(reserve=2 * 800 * args.steps)  # > 2 events per native call of a c2 fit
     lib = native.load()
     with ClockSampler(local) as clocks:
         barrier()

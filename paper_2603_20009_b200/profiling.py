@@ -63,19 +63,25 @@ def traffic_per_launch(kernel: str, rows_per_launch: float) -> float | None:
 
 
 class KernelTimer:
-    def __init__(self):
+    def __init__(self, reserve: int = 0):
         import torch
         self.torch = torch
         self.records = []  # (name, ev0, ev1, flops, bytes)
         self.launches = 0
+        # events created up front: creating two per launch inside the timed region costs host
+        # time at every post-sync relaunch
+        self._pool = [torch.cuda.Event(enable_timing=True) for _ in range(reserve)]
+
+    def _event(self):
+        return self._pool.pop() if self._pool else self.torch.cuda.Event(enable_timing=True)
 
     def begin(self):
-        e = self.torch.cuda.Event(enable_timing=True)
+        e = self._event()
         e.record()
         return e
 
     def end(self, name, e0, flops=0.0, nbytes=0.0):
-        e1 = self.torch.cuda.Event(enable_timing=True)
+        e1 = self._event()
         e1.record()
         self.records.append((name, e0, e1, float(flops), float(nbytes)))
         self.launches += 1
