@@ -37,7 +37,9 @@ for rep in range(REPS):
         times.append(e0.elapsed_time(e1))
     phase = res.phase
     if os.environ.get("AB_VERBOSE"):
-        print(f"rep {rep}: {e0.elapsed_time(e1):.1f} ms {[(kk, round(1e3 * v, 1)) for kk, v in phase.items()]}", flush=True)
+        ms = torch.cuda.memory_stats()
+        print(f"rep {rep}: {e0.elapsed_time(e1):.1f} ms {[(kk, round(1e3 * v, 1)) for kk, v in phase.items()]} "
+              f"cudaMalloc calls so far {ms.get('num_device_alloc')} frees {ms.get('num_device_free')}", flush=True)
     h = hashlib.sha1(res.loop.assign_dev.cpu().numpy().tobytes()).hexdigest()[:12] \
         if hasattr(res.loop, "assign_dev") else None
 times.sort()
